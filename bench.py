@@ -1,0 +1,278 @@
+#!/usr/bin/env python
+"""Benchmark of the GMAF hot path on B200 (contract: see DESIGN.md sec. 8).
+
+One *step* = one joint Picard-step analysis of K working conditions through the
+public API (gmaf_thickness -> gmaf_assemble -> gmaf_solve(rtol) -> gmaf_integrate),
+i.e. every row of SURVEY 8(a), on BASELINE config C3 by default (short-textured
+2048x1024, K = 9, omega 1.6, rtol 1e-10).
+
+metric  = PCG-ASSOR DOF*iter/s = sum_steps K*n_theta*n_y*iterations / device time.
+value   : CUDA-event time over the timed steps (inputs -- the K condition records --
+          are re-sent every step; the fields are HBM-resident, 151 MB each > L2).
+e2e     : the same steps timed on the host clock, H2D of the condition records and D2H
+          of the wrench and solve statistics inside.
+roofline: the dominant kernel's algorithmic bytes / its measured average duration
+          (in-kernel %globaltimer over the timed region), against MEASURED_PEAKS.json.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl gmaf|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import gmaf_inputs as gi  # noqa: E402
+
+METRIC = "PCG-ASSOR DOF*iter/s (joint K-condition solve, full Picard-step analysis)"
+UNIT = "DOF*iter/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_baseline(cfg, iters: int = 10):
+    """The oracle as it stands (single-threaded C, one core), on a bounded sample of the
+    same workload: assembly of all K conditions + `iters` PCG-ASSOR iterations."""
+    import oracle
+    t0 = time.perf_counter()
+    AP, AE, AN, S = oracle.assemble_joint(cfg.grid, cfg.conds)
+    t1 = time.perf_counter()
+    res = oracle.pcg_joint(AP, AE, AN, S, tol=0.0, omega=cfg.omega, max_iter=iters)
+    t2 = time.perf_counter()
+    n = cfg.grid["n_theta"] * cfg.grid["n_y"]
+    value = cfg.K * n * res.iterations / (t2 - t1)
+    return {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{cfg.name}: oracle assembly of K={cfg.K} ({t1 - t0:.2f} s) + "
+                      f"{res.iterations} PCG-ASSOR iterations ({t2 - t1:.2f} s) on 1 host core",
+            "assembly_s": t1 - t0, "iter_s": (t2 - t1) / max(res.iterations, 1)}
+
+
+def run_reference(args, cfg):
+    world, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    iters = args.ref_iters
+    n = cfg.grid["n_theta"] * cfg.grid["n_y"]
+    times = []
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        AP, AE, AN, S = oracle.assemble_joint(cfg.grid, cfg.conds)
+        res = oracle.pcg_joint(AP, AE, AN, S, tol=0.0, omega=cfg.omega, max_iter=iters)
+        W = [oracle.wrench(cfg.grid, cfg.conds[k], res.p[k]) for k in range(cfg.K)]
+        t1 = time.perf_counter()
+        if s >= args.warmup:
+            times.append(t1 - t0)
+    tot = sum(times)
+    value = cfg.K * n * iters * len(times) / tot
+    sample = (f"{cfg.name}: per step the oracle assembles K={cfg.K}, runs {iters} PCG-ASSOR "
+              f"iterations and integrates K wrenches, single-threaded on 1 host core")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config_obj(cfg, args),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _config_obj(cfg, args):
+    g = cfg.grid
+    return {"workload": f"{cfg.name}: {cfg.note}, omega {cfg.omega}, rtol {cfg.tol:g}, ASSOR-II, "
+                        "coupled synchronized convergence (Eq. 3.9)",
+            "n_theta": g["n_theta"], "n_y": g["n_y"], "K": cfg.K,
+            "texture": "short 60x10" if g.get("tex_n_theta") else "smooth",
+            "dof": cfg.dof, "l2_policy": "inputs larger than L2 (151 MB per field at C3)",
+            "parallelism": "1 GPU" if args.gpus == 1 else
+            f"{args.gpus} GPUs, one independent K-condition joint solve per rank (weak)"}
+
+
+def run_gmaf(args, cfg):
+    import torch
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl")
+        dist = tdist
+    import paper_2511_06824_b200 as P
+    P.lib()
+    K, n = cfg.K, cfg.grid["n_theta"] * cfg.grid["n_y"]
+    # weak scaling: rank r analyses its own operating point (shaft angle shifted by r degrees)
+    conds = cfg.conds if rank == 0 else gi.fd_conditions(gi.condition(phi_deg=90.0 + rank))
+    S = P.JointSolver(cfg.grid, K, device=local)
+    stream = S.stream
+
+    def one_step():
+        st, W = S.step(conds, tol=cfg.tol, omega=cfg.omega, precond="assor2")
+        return st
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    S.reset_kernel_times()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    iters = []
+    w0 = time.perf_counter()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        st = one_step()
+        iters.append(st.iterations)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    w1 = time.perf_counter()
+    ck = clocks.stop()
+    dev_ms = ev0.elapsed_time(ev1)
+    wall_ms = (w1 - w0) * 1e3
+    kt = S.kernel_times()
+    if dist:
+        dist.barrier()
+    t = torch.tensor([dev_ms, wall_ms, float(sum(iters))], dtype=torch.float64, device="cuda")
+    if dist:
+        import torch.distributed as tdist
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        tdist.all_gather(allt, t)
+        allt = torch.stack(allt).cpu().numpy()
+    else:
+        allt = t.cpu().numpy()[None]
+    dev_max_ms = float(allt[:, 0].max())
+    wall_max_ms = float(allt[:, 1].max())
+    total_dof_iters = float(K * n * allt[:, 2].sum())
+    value = total_dof_iters / (dev_max_ms * 1e-3)
+    e2e_value = total_dof_iters / (wall_max_ms * 1e-3)
+
+    # roofline of the dominant kernel (in-kernel %globaltimer over the timed region)
+    kmap = {k["name"]: k for k in kt}
+    dom = max((k for k in kt if k["launches"] > 0), key=lambda k: k["total_ms"])
+    avg_s = dom["total_ms"] * 1e-3 / dom["launches"]
+    achieved = dom["bytes_per_launch"] / avg_s / 1e9
+    peak, peak_src = _peaks()
+    solve_ms = sum(k["total_ms"] for k in kt if k["name"].startswith("pcg_"))
+    launches = int(sum(k["launches"] for k in kt))
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_max_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config_obj(cfg, args),
+        "iterations_per_step": iters,
+        "roofline": {"bound": "hbm", "kernel": dom["name"], "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json)",
+                     "bytes_per_launch": dom["bytes_per_launch"], "avg_launch_us": avg_s * 1e6},
+        "kernels": {k["name"]: {"launches": k["launches"], "total_ms": round(k["total_ms"], 3),
+                                "avg_us": round(1e3 * k["total_ms"] / k["launches"], 2) if k["launches"] else 0,
+                                "GBps": round(k["bytes_per_launch"] * k["launches"] / (k["total_ms"] * 1e-3) / 1e9, 1)
+                                if k["launches"] and k["total_ms"] > 0 else 0}
+                    for k in kt},
+        "pcg_kernel_share_of_step": solve_ms / dev_ms if dev_ms else None,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": K * 13 * 8 + 48,
+                "d2h_bytes_per_step": K * 12 * 8 + 8 * 7 * K + 128},
+        "gpu_launches": launches,
+        "clocks": ck,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, iters=args.ref_iters)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    S.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--impl", default="gmaf", choices=["gmaf", "reference"])
+    ap.add_argument("--ref-iters", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = gi.config(args.config)
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_gmaf(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

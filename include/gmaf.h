@@ -1,0 +1,175 @@
+/*
+ * gmaf.h -- C ABI of libgmaf, the B200-native (sm_100a) hot path of GMAF
+ * (arXiv 2511.06824): the joint multi-working-condition pressure solve of one
+ * Picard step.
+ *
+ *   gmaf_thickness  -> film thickness h(e) and rate dh/dt (Eq. 2.3, PAPER.md:45;
+ *                      Eq. 2.2), h_min guard
+ *   gmaf_assemble   -> FVM 5-point Reynolds system A_k p_k = S_k for K conditions
+ *                      (Eqs. 2.4-2.7), symmetric DIA bands A_P, A_E, A_N
+ *   gmaf_solve      -> PCG (Table 1; sign of r0 fixed, DESIGN.md R-A9) with the
+ *                      ASSOR-II preconditioner (Eqs. 3.4-3.6) on the joint
+ *                      block-diagonal system (Eq. 3.7) under the synchronized
+ *                      global convergence test (Eq. 3.9)
+ *   gmaf_integrate  -> force and moment of the oil film from normal pressure and
+ *                      viscous shear for every condition (Sec. 2.4-III)
+ *
+ * Conventions (all entry points):
+ *  - Every call returns a gmaf_status: 0 = OK, < 0 = error.  No C++ exception
+ *    or abort crosses the ABI.  gmaf_last_error(ctx) gives a one-line reason.
+ *  - Host pointers are caller-owned and only read/written during the call.
+ *  - The caller owns the DEVICE workspace (e.g. a torch uint8 CUDA tensor of
+ *    gmaf_workspace_bytes() bytes); it must outlive the context.  The library
+ *    owns its CUDA graphs, events and pinned staging buffers.
+ *  - All device work is enqueued on the caller's stream given at create.
+ *    gmaf_thickness, gmaf_solve, gmaf_integrate and gmaf_get synchronize that
+ *    stream before returning (they return host data); gmaf_assemble does not.
+ *  - Call order: thickness -> assemble -> solve -> integrate; otherwise
+ *    GMAF_E_STATE.  A new gmaf_thickness restarts the sequence (warm start
+ *    reuses p from the previous solve).
+ *  - One context per host thread.  FP64 throughout.
+ *  - Device layout of every field: [K][n_y][n_theta], theta contiguous, global
+ *    index i + n_theta*j + n*k with n = n_theta*n_y (Eq. 3.8).
+ */
+#ifndef GMAF_H
+#define GMAF_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  GMAF_OK = 0,
+  GMAF_E_INVALID_ARG = -1,
+  GMAF_E_INVALID_MESH = -2,          /* n_theta < 4 or n_y < 4 */
+  GMAF_E_MESH_TOO_COARSE = -3,       /* < 2 nodes per dimple pitch */
+  GMAF_E_NONPOSITIVE_THICKNESS = -4, /* h < h_min somewhere */
+  GMAF_E_BREAKDOWN = -5,             /* u.v <= 0 or r.z <= 0: not SPD */
+  GMAF_E_NO_CONVERGENCE = -6,        /* max_iter reached; the last iterate is kept in p */
+  GMAF_E_STATE = -7,                 /* call order violated */
+  GMAF_E_WORKSPACE = -8,             /* workspace NULL, too small or misaligned (256 B) */
+  GMAF_E_CUDA = -9,                  /* a CUDA runtime error; see gmaf_last_error */
+  GMAF_E_NCCL = -10                  /* a collective failed (world > 1) */
+} gmaf_status;
+
+enum { GMAF_PRECOND_NONE = 0, GMAF_PRECOND_JACOBI = 1, GMAF_PRECOND_ASSOR2 = 2 };
+enum { GMAF_COUPLED = 0,   /* one Krylov process on A_G: global alpha, beta (Eq. 3.9) */
+       GMAF_LOCKSTEP = 1   /* per-condition alpha_k, beta_k, same global stop test (R-A11) */ };
+enum { GMAF_FIELD_P = 0, GMAF_FIELD_H = 1, GMAF_FIELD_HDOT = 2, GMAF_FIELD_AP = 3,
+       GMAF_FIELD_AE = 4, GMAF_FIELD_AN = 5, GMAF_FIELD_S = 6, GMAF_FIELD_R = 7 };
+enum { GMAF_SHARD_CONDITIONS = 0 };
+
+/* Mesh and texture, shared by all K conditions; copied at create. */
+typedef struct {
+  int32_t n_theta, n_y;          /* unknown nodes; theta periodic; Dirichlet ghost rows at y = 0 and
+                                    y = L_F are not counted (DESIGN.md R-A3) */
+  double  R_k, R_c;              /* piston and bore radius, m (Table 8) */
+  double  mu;                    /* viscosity, Pa.s (not in the paper; R-A8) */
+  double  h_min;                 /* thickness guard, m */
+  int32_t tex_n_theta, tex_n_y;  /* dimple counts; 0,0 = smooth (Fig. 10: 60x10, 60x20) */
+  int32_t tex_band_rows;         /* dimples occupy unknown rows [0, band) from y = 0 */
+  int32_t tex_fill_num, tex_fill_den; /* dimple fraction of the pitch in each direction */
+  double  tex_depth;             /* m (20e-6) */
+} gmaf_grid;
+
+/* One working condition (Eqs. 2.17-2.19 build the 9 of one Picard step). */
+typedef struct {
+  double e[4], edot[4];          /* eccentricity (m) and its rate (m/s) */
+  double L_F;                    /* coupling length, m */
+  double U_theta, U_y;           /* sliding velocity of the piston relative to the bore, m/s */
+  double p_in, p_out;            /* Dirichlet pressures at y = 0 and y = L_F, Pa */
+} gmaf_condition;
+
+/* Multi-GPU description.  world == 1 needs no NCCL.  world > 1: conditions are
+ * sharded in contiguous blocks over ranks; nccl_unique_id points at the 128-byte
+ * ncclUniqueId broadcast by the caller (e.g. over torch.distributed). */
+typedef struct {
+  int32_t rank, world;
+  const void* nccl_unique_id;
+  int32_t shard;                 /* GMAF_SHARD_CONDITIONS */
+} gmaf_dist;
+
+typedef struct {
+  int32_t iterations;            /* number of alpha-updates (Table 1 step 4) */
+  int32_t converged;             /* 1 if Eq. 3.9 was met */
+  int32_t status;                /* gmaf_status of the solve */
+  int32_t precond;
+  double  rel_residual;          /* recursive ||r||/||S_G|| at exit (R-A10) */
+  double  true_rel_residual;     /* ||S_G - A_G p_G|| / ||S_G|| at exit */
+  double  solve_ms;              /* device time of the solve (CUDA events) */
+} gmaf_solve_stats;
+
+/* Per-kernel device time accumulated since create or the last reset, measured
+ * inside the kernels with %globaltimer (first CTA start -> last CTA end). */
+typedef struct {
+  char    name[24];
+  int64_t launches;
+  double  total_ms;
+  double  bytes_per_launch;      /* algorithmic DRAM bytes per launch */
+} gmaf_kernel_timing;
+
+typedef struct gmaf_ctx gmaf_ctx;
+
+/* Device workspace bytes needed for this grid, K conditions and distribution.
+ * Returns 0 on invalid arguments. */
+size_t gmaf_workspace_bytes(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist);
+
+/* Create a context.  d_workspace: device pointer (256-byte aligned) of ws_bytes >=
+ * gmaf_workspace_bytes(); cuda_stream: a cudaStream_t (NULL = legacy default stream).
+ * dist may be NULL (world = 1).  Errors: INVALID_ARG, INVALID_MESH, MESH_TOO_COARSE,
+ * WORKSPACE, CUDA, NCCL. */
+gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
+                        void* d_workspace, size_t ws_bytes, void* cuda_stream, gmaf_ctx** out);
+gmaf_status gmaf_destroy(gmaf_ctx* ctx);
+
+/* Upload the K conditions (host array, all K on every rank) and check h >= h_min on
+ * every node of rows -1..n_y (synchronous).  Error: NONPOSITIVE_THICKNESS (nothing
+ * downstream may run until a valid call). */
+gmaf_status gmaf_thickness(gmaf_ctx* ctx, const gmaf_condition* conds);
+
+/* Assemble A_P, A_E, A_N (one set per distinct e, Eq. 2.3 has no e-dot) and S for all
+ * K conditions, bitwise equal to the oracle's evaluation order.
+ * Asynchronous. */
+gmaf_status gmaf_assemble(gmaf_ctx* ctx);
+
+/* Solve A_G p_G = S_G.  tol = epsilon_PCG of Eq. 3.9 (relative); omega in (0,2);
+ * precond GMAF_PRECOND_*; coupling GMAF_COUPLED or GMAF_LOCKSTEP; max_iter >= 0;
+ * warm_start != 0 starts from the current p (else p0 = 0).  out: host stats (may be
+ * NULL); cond_rel_residual: host array of K (may be NULL) receiving ||r_k||/||S_k||.
+ * Errors: BREAKDOWN, NO_CONVERGENCE (p holds the last iterate), STATE, CUDA, NCCL. */
+gmaf_status gmaf_solve(gmaf_ctx* ctx, double tol, double omega, int32_t precond, int32_t coupling,
+                       int32_t max_iter, int32_t warm_start, gmaf_solve_stats* out,
+                       double* cond_rel_residual);
+
+/* Force and moment for every condition: host wrench[K*12], per k
+ * [Fp_x,Fp_y,Fp_z, Mp_x,Mp_y,Mp_z, Fs_x,Fs_y,Fs_z, Ms_x,Ms_y,Ms_z] in N and N.m, X along
+ * theta = 0, Y along theta = 90 deg, Z along the piston axis from the bottom, moments
+ * about the bottom centre (DESIGN.md R-A14). */
+gmaf_status gmaf_integrate(gmaf_ctx* ctx, double* wrench);
+
+/* Copy one field of condition k to host_out: P, S, R, AP, AE, AN are [n_y][n_theta];
+ * H and HDOT are [n_y+2][n_theta] (rows -1..n_y). */
+gmaf_status gmaf_get(gmaf_ctx* ctx, int32_t field, int32_t k, double* host_out);
+
+/* Device pointer of a field of condition k (P, S, R, AP, AE, AN), for zero-copy use. */
+gmaf_status gmaf_field_ptr(gmaf_ctx* ctx, int32_t field, int32_t k, void** dptr);
+
+/* Kernel timing (see gmaf_kernel_timing); n = capacity of out; *count receives the
+ * number of entries.  gmaf_reset_kernel_times zeroes the accumulators. */
+gmaf_status gmaf_kernel_times(gmaf_ctx* ctx, gmaf_kernel_timing* out, int32_t n, int32_t* count);
+gmaf_status gmaf_reset_kernel_times(gmaf_ctx* ctx);
+
+/* Run n_iter PCG iterations unconditionally (no convergence test; throughput mode of
+ * SURVEY 8(d)) after a solve's init; used by the benchmark.  Stats as gmaf_solve. */
+gmaf_status gmaf_solve_fixed(gmaf_ctx* ctx, double omega, int32_t precond, int32_t n_iter,
+                             gmaf_solve_stats* out);
+
+const char* gmaf_last_error(const gmaf_ctx* ctx);
+const char* gmaf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

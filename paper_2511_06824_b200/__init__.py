@@ -1,0 +1,278 @@
+"""paper_2511_06824_b200 -- B200-native hot path of GMAF (arXiv 2511.06824).
+
+Thin ctypes binding of ``libgmaf.so`` (C ABI in ``include/gmaf.h``).  This module
+only marshals arguments: every step of the path (thickness, assembly, PCG-ASSOR,
+quadrature) runs in the library's sm_100a kernels.  PyTorch is used for the device
+workspace and the CUDA stream only.  There is no CPU fallback: if the library is not
+built or no CUDA device is present, the calls raise.
+
+Low-level functions carry the ABI names (``gmaf_create``, ``gmaf_thickness``,
+``gmaf_assemble``, ``gmaf_solve``, ``gmaf_integrate``, ...); ``JointSolver`` wraps
+them for one Picard step of K working conditions (GMAF steps I-III).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgmaf.so")
+
+STATUS = {0: "OK", -1: "INVALID_ARG", -2: "INVALID_MESH", -3: "MESH_TOO_COARSE",
+          -4: "NONPOSITIVE_THICKNESS", -5: "BREAKDOWN", -6: "NO_CONVERGENCE", -7: "STATE",
+          -8: "WORKSPACE", -9: "CUDA", -10: "NCCL"}
+PRECOND = {"none": 0, "jacobi": 1, "assor2": 2}
+COUPLING = {"coupled": 0, "lockstep": 1}
+FIELD = {"p": 0, "h": 1, "hdot": 2, "AP": 3, "AE": 4, "AN": 5, "S": 6, "r": 7}
+
+
+class gmaf_grid(C.Structure):
+    _fields_ = [("n_theta", C.c_int32), ("n_y", C.c_int32), ("R_k", C.c_double), ("R_c", C.c_double),
+                ("mu", C.c_double), ("h_min", C.c_double), ("tex_n_theta", C.c_int32),
+                ("tex_n_y", C.c_int32), ("tex_band_rows", C.c_int32), ("tex_fill_num", C.c_int32),
+                ("tex_fill_den", C.c_int32), ("tex_depth", C.c_double)]
+
+
+class gmaf_condition(C.Structure):
+    _fields_ = [("e", C.c_double * 4), ("edot", C.c_double * 4), ("L_F", C.c_double),
+                ("U_theta", C.c_double), ("U_y", C.c_double), ("p_in", C.c_double),
+                ("p_out", C.c_double)]
+
+
+class gmaf_dist(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("nccl_unique_id", C.c_void_p),
+                ("shard", C.c_int32)]
+
+
+class gmaf_solve_stats(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("status", C.c_int32),
+                ("precond", C.c_int32), ("rel_residual", C.c_double),
+                ("true_rel_residual", C.c_double), ("solve_ms", C.c_double)]
+
+
+class gmaf_kernel_timing(C.Structure):
+    _fields_ = [("name", C.c_char * 24), ("launches", C.c_int64), ("total_ms", C.c_double),
+                ("bytes_per_launch", C.c_double)]
+
+
+class GmafError(RuntimeError):
+    def __init__(self, code: int, msg: str = ""):
+        super().__init__(f"gmaf {STATUS.get(code, code)} ({code}): {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libgmaf.so (in-tree).  Raises if it is missing -- no fallback."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is not built; run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        L.gmaf_workspace_bytes.restype = C.c_size_t
+        L.gmaf_workspace_bytes.argtypes = [C.POINTER(gmaf_grid), C.c_int32, C.POINTER(gmaf_dist)]
+        L.gmaf_create.argtypes = [C.POINTER(gmaf_grid), C.c_int32, C.POINTER(gmaf_dist), P, C.c_size_t, P,
+                                  C.POINTER(P)]
+        L.gmaf_destroy.argtypes = [P]
+        L.gmaf_thickness.argtypes = [P, C.POINTER(gmaf_condition)]
+        L.gmaf_assemble.argtypes = [P]
+        L.gmaf_solve.argtypes = [P, C.c_double, C.c_double, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                 C.POINTER(gmaf_solve_stats), C.POINTER(C.c_double)]
+        L.gmaf_solve_fixed.argtypes = [P, C.c_double, C.c_int32, C.c_int32, C.POINTER(gmaf_solve_stats)]
+        L.gmaf_integrate.argtypes = [P, C.POINTER(C.c_double)]
+        L.gmaf_get.argtypes = [P, C.c_int32, C.c_int32, C.POINTER(C.c_double)]
+        L.gmaf_field_ptr.argtypes = [P, C.c_int32, C.c_int32, C.POINTER(P)]
+        L.gmaf_kernel_times.argtypes = [P, C.POINTER(gmaf_kernel_timing), C.c_int32, C.POINTER(C.c_int32)]
+        L.gmaf_reset_kernel_times.argtypes = [P]
+        L.gmaf_last_error.restype = C.c_char_p
+        L.gmaf_last_error.argtypes = [P]
+        L.gmaf_version.restype = C.c_char_p
+        for name in ("gmaf_create", "gmaf_destroy", "gmaf_thickness", "gmaf_assemble", "gmaf_solve",
+                     "gmaf_solve_fixed", "gmaf_integrate", "gmaf_get", "gmaf_field_ptr",
+                     "gmaf_kernel_times", "gmaf_reset_kernel_times"):
+            getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+ABI_SYMBOLS = ("gmaf_workspace_bytes", "gmaf_create", "gmaf_destroy", "gmaf_thickness", "gmaf_assemble",
+               "gmaf_solve", "gmaf_solve_fixed", "gmaf_integrate", "gmaf_get", "gmaf_field_ptr",
+               "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_last_error", "gmaf_version")
+
+
+def make_grid(g: dict) -> gmaf_grid:
+    return gmaf_grid(int(g["n_theta"]), int(g["n_y"]), g["R_k"], g["R_c"], g["mu"], g["h_min"],
+                     int(g.get("tex_n_theta", 0)), int(g.get("tex_n_y", 0)), int(g.get("tex_band_rows", 0)),
+                     int(g.get("tex_fill_num", 1)), int(g.get("tex_fill_den", 2)), g.get("tex_depth", 0.0))
+
+
+def make_conditions(conds) -> C.Array:
+    conds = np.asarray(conds, dtype=np.float64).reshape(-1, 13)
+    arr = (gmaf_condition * conds.shape[0])()
+    for k, c in enumerate(conds):
+        for q in range(4):
+            arr[k].e[q] = c[q]
+            arr[k].edot[q] = c[4 + q]
+        arr[k].L_F, arr[k].U_theta, arr[k].U_y, arr[k].p_in, arr[k].p_out = (float(x) for x in c[8:13])
+    return arr
+
+
+def _check(ctx, code: int):
+    if code != 0:
+        msg = lib().gmaf_last_error(ctx).decode() if ctx else ""
+        raise GmafError(code, msg)
+
+
+# ---- ABI-named thin wrappers ------------------------------------------------------------
+
+def gmaf_workspace_bytes(grid: gmaf_grid, K: int) -> int:
+    return int(lib().gmaf_workspace_bytes(C.byref(grid), int(K), None))
+
+
+def gmaf_create(grid: gmaf_grid, K: int, d_workspace: int, ws_bytes: int, stream: int) -> C.c_void_p:
+    ctx = C.c_void_p()
+    _check(None, lib().gmaf_create(C.byref(grid), int(K), None, C.c_void_p(d_workspace), ws_bytes,
+                                   C.c_void_p(stream), C.byref(ctx)))
+    return ctx
+
+
+def gmaf_thickness(ctx, conds_arr) -> None:
+    _check(ctx, lib().gmaf_thickness(ctx, conds_arr))
+
+
+def gmaf_assemble(ctx) -> None:
+    _check(ctx, lib().gmaf_assemble(ctx))
+
+
+def gmaf_solve(ctx, tol, omega, precond, coupling, max_iter, warm, K):
+    st = gmaf_solve_stats()
+    cr = (C.c_double * K)()
+    code = lib().gmaf_solve(ctx, float(tol), float(omega), int(precond), int(coupling), int(max_iter),
+                            int(warm), C.byref(st), cr)
+    return code, st, np.array(list(cr))
+
+
+def gmaf_integrate(ctx, K) -> np.ndarray:
+    w = np.empty(K * 12)
+    _check(ctx, lib().gmaf_integrate(ctx, w.ctypes.data_as(C.POINTER(C.c_double))))
+    return w.reshape(K, 12)
+
+
+def gmaf_destroy(ctx) -> None:
+    lib().gmaf_destroy(ctx)
+
+
+@dataclass
+class SolveStats:
+    iterations: int
+    converged: bool
+    status: int
+    rel_residual: float
+    true_rel_residual: float
+    solve_ms: float
+    cond_rel: np.ndarray
+
+
+class JointSolver:
+    """One context: K working conditions on one mesh (Eq. 3.7 joint system)."""
+
+    def __init__(self, grid: dict, K: int, device: int | str = 0, stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("JointSolver needs a CUDA device (no CPU fallback)")
+        self.torch = torch
+        self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+        self.grid_dict = dict(grid)
+        self.grid = make_grid(grid)
+        self.K = int(K)
+        self.n_theta, self.n_y = int(grid["n_theta"]), int(grid["n_y"])
+        nbytes = gmaf_workspace_bytes(self.grid, self.K)
+        if nbytes == 0:
+            raise GmafError(-1, "invalid grid for workspace sizing")
+        with torch.cuda.device(self.device):
+            self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+            # 256-byte alignment: torch's caching allocator returns >= 512-byte aligned blocks
+            self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self.ctx = gmaf_create(self.grid, self.K, self.workspace.data_ptr(), nbytes, self.stream.cuda_stream)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            gmaf_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- the hot path ------------------------------------------------------------------
+    def thickness(self, conds) -> None:
+        conds = np.asarray(conds, dtype=np.float64).reshape(-1, 13)
+        if conds.shape[0] != self.K:
+            raise ValueError(f"expected {self.K} conditions, got {conds.shape[0]}")
+        gmaf_thickness(self.ctx, make_conditions(conds))
+
+    def assemble(self) -> None:
+        gmaf_assemble(self.ctx)
+
+    def solve(self, tol=1e-10, omega=1.8, precond="assor2", coupling="coupled", max_iter=200000,
+              warm=False, raise_on_error=True) -> SolveStats:
+        code, st, cr = gmaf_solve(self.ctx, tol, omega, PRECOND[precond], COUPLING[coupling], max_iter,
+                                  warm, self.K)
+        if code != 0 and raise_on_error:
+            _check(self.ctx, code)
+        return SolveStats(st.iterations, bool(st.converged), st.status, st.rel_residual,
+                          st.true_rel_residual, st.solve_ms, cr)
+
+    def solve_fixed(self, n_iter: int, omega=1.6, precond="assor2") -> SolveStats:
+        st = gmaf_solve_stats()
+        _check(self.ctx, lib().gmaf_solve_fixed(self.ctx, float(omega), PRECOND[precond], int(n_iter),
+                                                 C.byref(st)))
+        return SolveStats(st.iterations, bool(st.converged), st.status, st.rel_residual,
+                          st.true_rel_residual, st.solve_ms, np.zeros(self.K))
+
+    def integrate(self) -> np.ndarray:
+        return gmaf_integrate(self.ctx, self.K)
+
+    def step(self, conds, tol=1e-10, omega=1.8, precond="assor2", coupling="coupled",
+             max_iter=200000, warm=False):
+        """One joint Picard-step analysis: thickness -> assemble -> solve -> integrate."""
+        self.thickness(conds)
+        self.assemble()
+        st = self.solve(tol=tol, omega=omega, precond=precond, coupling=coupling, max_iter=max_iter,
+                        warm=warm)
+        return st, self.integrate()
+
+    # -- readback ----------------------------------------------------------------------
+    def get(self, field: str, k: int) -> np.ndarray:
+        rows = self.n_y + 2 if field in ("h", "hdot") else self.n_y
+        out = np.empty((rows, self.n_theta))
+        _check(self.ctx, lib().gmaf_get(self.ctx, FIELD[field], int(k),
+                                        out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def field_tensor(self, field: str, k: int):
+        """Zero-copy torch view of a device field of condition k."""
+        ptr = C.c_void_p()
+        _check(self.ctx, lib().gmaf_field_ptr(self.ctx, FIELD[field], int(k), C.byref(ptr)))
+        base = self.workspace.data_ptr()
+        off = (ptr.value - base) // 8
+        n = self.n_theta * self.n_y
+        return self.workspace.view(self.torch.float64)[off:off + n].view(self.n_y, self.n_theta)
+
+    def kernel_times(self) -> list[dict]:
+        arr = (gmaf_kernel_timing * 16)()
+        cnt = C.c_int32()
+        _check(self.ctx, lib().gmaf_kernel_times(self.ctx, arr, 16, C.byref(cnt)))
+        return [dict(name=arr[i].name.decode(), launches=int(arr[i].launches), total_ms=arr[i].total_ms,
+                     bytes_per_launch=arr[i].bytes_per_launch) for i in range(cnt.value)]
+
+    def reset_kernel_times(self) -> None:
+        _check(self.ctx, lib().gmaf_reset_kernel_times(self.ctx))

@@ -1,0 +1,570 @@
+// gmaf_api.cu -- host runtime of libgmaf: the C ABI of include/gmaf.h.
+//
+// Context = caller-owned device workspace carved into fields, a caller stream, and a
+// cache of instantiated CUDA graphs (one per preconditioner / start mode).  A solve is
+// ONE graph launch: init kernel -> WHILE node {(phase A, phase B) x UNROLL} -> true
+// residual kernel; the convergence decision is taken on the device (Eq. 3.9) and the host
+// reads the statistics once, after the graph.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/gmaf.h"
+#include "gmaf_internal.cuh"
+
+#ifndef M_PI
+#define M_PI 3.14159265358979323846
+#endif
+
+namespace gmaf {
+int quad_ctas_per_condition(const GridParams& g, int K);
+cudaError_t configure_pcg_kernels(const TileCfg& t, int K);
+}
+
+using namespace gmaf;
+
+namespace {
+
+constexpr int kUnroll = 4;          // (A, B) pairs per WHILE-body execution (must be even)
+static_assert(kUnroll % 2 == 0, "ping-pong parity");
+constexpr size_t kAlign = 256;
+
+enum State { ST_CREATED = 0, ST_THICK = 1, ST_ASSEMBLED = 2, ST_SOLVED = 3 };
+
+struct GraphKey {
+  int precond, warm, fixed;
+  bool operator<(const GraphKey& o) const {
+    if (precond != o.precond) return precond < o.precond;
+    if (warm != o.warm) return warm < o.warm;
+    return fixed < o.fixed;
+  }
+};
+
+struct Layout {
+  size_t off_ct, off_st, off_cth, off_sth, off_cp, off_AP, off_AE, off_AN, off_S, off_p, off_r, off_r2,
+      off_u, off_u2,
+      off_scratch, off_part, off_wpart, off_wrench, off_state, off_cs, off_counters, off_timing,
+      off_guard, off_matrep, total;
+};
+
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+TileCfg make_tiles(int nt, int ny, int K) {
+  TileCfg t{};
+  t.tw = (nt >= 1024) ? 256 : 128;
+  t.n_strips = (nt + t.tw - 1) / t.tw;
+  const int target = 4 * 148;
+  int chunks = (target + t.n_strips * K - 1) / (t.n_strips * K);
+  if (chunks < 1) chunks = 1;
+  int th = (ny + chunks - 1) / chunks;
+  if (th < 8) th = 8;
+  if (th > ny) th = ny;
+  t.th = th;
+  t.n_chunks = (ny + th - 1) / th;
+  t.n_tiles = t.n_strips * t.n_chunks;
+  return t;
+}
+
+int check_grid(const gmaf_grid* g) {
+  if (!g) return GMAF_E_INVALID_ARG;
+  if (g->n_theta < 4 || g->n_y < 4) return GMAF_E_INVALID_MESH;
+  if (!(g->R_k > 0.0) || !(g->R_c > g->R_k) || !(g->mu > 0.0)) return GMAF_E_INVALID_ARG;
+  if (g->tex_n_theta > 0 || g->tex_n_y > 0) {
+    if (g->tex_n_theta <= 0 || g->tex_n_y <= 0 || g->tex_band_rows <= 0 || g->tex_band_rows > g->n_y ||
+        g->tex_fill_den <= 0 || g->tex_fill_num < 0 || g->tex_fill_num > g->tex_fill_den ||
+        g->tex_depth < 0.0)
+      return GMAF_E_INVALID_ARG;
+    if (g->n_theta < 2 * g->tex_n_theta || g->tex_band_rows < 2 * g->tex_n_y) return GMAF_E_MESH_TOO_COARSE;
+  }
+  return GMAF_OK;
+}
+
+Layout make_layout(const gmaf_grid* g, int K) {
+  Layout L{};
+  const size_t nt = (size_t)g->n_theta, ny = (size_t)g->n_y, n = nt * ny;
+  const TileCfg t = make_tiles(g->n_theta, g->n_y, K);
+  size_t o = 0;
+  auto take = [&](size_t bytes) { size_t at = o; o = align_up(o + bytes); return at; };
+  L.off_ct = take(nt * 8); L.off_st = take(nt * 8); L.off_cth = take(nt * 8); L.off_sth = take(nt * 8);
+  L.off_cp = take((size_t)K * sizeof(CondParams));
+  L.off_AP = take((size_t)K * n * 8); L.off_AE = take((size_t)K * n * 8); L.off_AN = take((size_t)K * n * 8);
+  L.off_S = take((size_t)K * n * 8); L.off_p = take((size_t)K * n * 8);
+  L.off_r = take((size_t)K * n * 8); L.off_r2 = take((size_t)K * n * 8);
+  L.off_u = take((size_t)K * n * 8); L.off_u2 = take((size_t)K * n * 8);
+  L.off_scratch = take((ny + 2) * nt * 8);
+  L.off_part = take((size_t)4 * K * t.n_tiles * 8);
+  L.off_wpart = take((size_t)(148 * 8 + K) * 12 * 8);
+  L.off_wrench = take((size_t)K * 12 * 8);
+  L.off_state = take(sizeof(SolverState));
+  L.off_cs = take((size_t)7 * K * 8);
+  L.off_counters = take(16 * sizeof(unsigned int));
+  L.off_timing = take(sizeof(Timing));
+  L.off_guard = take(4 * sizeof(unsigned long long));
+  L.off_matrep = take((size_t)K * sizeof(int32_t));
+  L.total = o;
+  return L;
+}
+
+}  // namespace
+
+struct gmaf_ctx {
+  gmaf_grid grid{};
+  GridParams gp{};
+  int K = 0;
+  gmaf_dist dist{0, 1, nullptr, 0};
+  cudaStream_t stream = nullptr;
+  cudaStream_t cap_stream = nullptr;
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  Layout L{};
+  TileCfg tiles{};
+  DevPtrs d{};
+  int M = 0;
+  std::vector<int32_t> mat_of, mat_rep;
+  int state = ST_CREATED;
+  std::string err;
+  std::map<GraphKey, std::pair<cudaGraph_t, cudaGraphExec_t>> graphs;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // pinned staging
+  SolverState* h_state = nullptr;
+  double* h_cs = nullptr;        // 7*K
+  double* h_wrench = nullptr;    // K*12
+  unsigned long long* h_guard = nullptr;
+  CondParams* h_cp = nullptr;
+  Timing* h_timing = nullptr;
+  int quad_ctas = 0;
+  int r_parity = 0;   // which ping-pong buffer holds the latest residual
+};
+
+namespace {
+
+gmaf_status fail(gmaf_ctx* c, gmaf_status code, const char* fmt, ...) {
+  if (c) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    c->err = buf;
+  }
+  return code;
+}
+
+#define CU(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(ctx, GMAF_E_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,                \
+                  cudaGetErrorString(e_));                                                    \
+  } while (0)
+
+template <typename T>
+T* at(gmaf_ctx* c, size_t off) { return reinterpret_cast<T*>(c->ws + off); }
+
+// Host evaluation of the per-condition scalars, in the same IEEE operation order as the
+// definition (oracle O3/O5): one rounding per operation, no contraction.
+CondParams cond_params(const gmaf_grid& g, const gmaf_condition& c, int mat) {
+  CondParams p{};
+  for (int q = 0; q < 4; ++q) { p.e[q] = c.e[q]; p.edot[q] = c.edot[q]; }
+  p.LF = c.L_F; p.Ut = c.U_theta; p.Uy = c.U_y; p.pin = c.p_in; p.pout = c.p_out;
+  volatile double dtheta = (2.0 * M_PI) / (double)g.n_theta;
+  volatile double dy = c.L_F / (double)(g.n_y + 1);
+  volatile double dx = g.R_k * dtheta;
+  p.dy = dy;
+  p.dx = dx;
+  p.rx = p.dy / p.dx;
+  p.ry = p.dx / p.dy;
+  p.sl = (c.e[2] - c.e[0]) / c.L_F;
+  p.tl = (c.e[3] - c.e[1]) / c.L_F;
+  p.sld = (c.edot[2] - c.edot[0]) / c.L_F;
+  p.tld = (c.edot[3] - c.edot[1]) / c.L_F;
+  p.mat = mat;
+  return p;
+}
+
+bool same_matrix(const gmaf_condition& a, const gmaf_condition& b) {
+  // A depends on h only, and h on (e, L_F) only (Eq. 2.3 has no e-dot).
+  return std::memcmp(a.e, b.e, sizeof(a.e)) == 0 && std::memcmp(&a.L_F, &b.L_F, sizeof(double)) == 0;
+}
+
+gmaf_status build_graph(gmaf_ctx* ctx, const GraphKey& key, cudaGraphExec_t* out) {
+  auto it = ctx->graphs.find(key);
+  if (it != ctx->graphs.end()) { *out = it->second.second; return GMAF_OK; }
+  cudaGraph_t graph = nullptr;
+  CU(cudaGraphCreate(&graph, 0));
+  cudaGraphConditionalHandle handle;
+  CU(cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
+  cudaStream_t cs = ctx->cap_stream;
+  // init: r0 = S - A p0, z0, d0, ||S_G|| (Table 1 steps 1-2)
+  CU(cudaStreamBeginCaptureToGraph(cs, graph, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  cudaError_t le = launch_init(ctx->gp, ctx->d, ctx->tiles, ctx->K, key.precond, key.warm != 0,
+                               (unsigned long long)handle, cs);
+  cudaGraph_t g2 = nullptr;
+  cudaError_t ee = cudaStreamEndCapture(cs, &g2);
+  CU(le);
+  CU(ee);
+  size_t nn = 0;
+  CU(cudaGraphGetNodes(graph, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn);
+  CU(cudaGraphGetNodes(graph, nodes.data(), &nn));
+  if (nn != 1) return fail(ctx, GMAF_E_CUDA, "graph build: expected 1 init node, got %zu", nn);
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = handle;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cond_node;
+  CU(cudaGraphAddNode(&cond_node, graph, nodes.data(), 1, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CU(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  cudaError_t lb = cudaSuccess;
+  for (int u = 0; u < kUnroll && lb == cudaSuccess; ++u) {
+    // iteration j = 4m + u inside the body: parity u % 2 (kUnroll is even)
+    lb = launch_phase_a(ctx->gp, ctx->d, ctx->tiles, ctx->K, key.precond, u & 1, (unsigned long long)handle, cs);
+    if (lb == cudaSuccess)
+      lb = launch_phase_b(ctx->gp, ctx->d, ctx->tiles, ctx->K, key.precond, u & 1, (unsigned long long)handle,
+                          cs);
+  }
+  ee = cudaStreamEndCapture(cs, &g2);
+  CU(lb);
+  CU(ee);
+  // true residual ||S - A p|| after the loop
+  CU(cudaStreamBeginCaptureToGraph(cs, graph, &cond_node, nullptr, 1, cudaStreamCaptureModeRelaxed));
+  le = launch_true_residual(ctx->gp, ctx->d, ctx->tiles, ctx->K, cs);
+  ee = cudaStreamEndCapture(cs, &g2);
+  CU(le);
+  CU(ee);
+  cudaGraphExec_t exec = nullptr;
+  CU(cudaGraphInstantiate(&exec, graph, 0));
+  ctx->graphs[key] = {graph, exec};
+  *out = exec;
+  return GMAF_OK;
+}
+
+gmaf_status run_solve(gmaf_ctx* ctx, double tol, double omega, int precond, int coupling, int max_iter,
+                      int warm, int fixed_iters, gmaf_solve_stats* out, double* cond_rel) {
+  SolverState* hs = ctx->h_state;
+  std::memset(hs, 0, sizeof(SolverState));
+  hs->tol = tol;
+  hs->omega = omega;
+  hs->coupling = coupling;
+  hs->max_iter = max_iter;
+  hs->fixed_iters = fixed_iters;
+  CU(cudaMemcpyAsync(ctx->d.st_, hs, sizeof(SolverState), cudaMemcpyHostToDevice, ctx->stream));
+  cudaGraphExec_t exec = nullptr;
+  gmaf_status gs = build_graph(ctx, GraphKey{precond, warm ? 1 : 0, fixed_iters > 0 ? 1 : 0}, &exec);
+  if (gs != GMAF_OK) return gs;
+  CU(cudaEventRecord(ctx->ev0, ctx->stream));
+  CU(cudaGraphLaunch(exec, ctx->stream));
+  CU(cudaEventRecord(ctx->ev1, ctx->stream));
+  CU(cudaMemcpyAsync(hs, ctx->d.st_, sizeof(SolverState), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaMemcpyAsync(ctx->h_cs, ctx->d.cs.alpha, (size_t)7 * ctx->K * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  float ms = 0.f;
+  CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  if (hs->zero_p) {
+    const size_t n = (size_t)ctx->grid.n_theta * ctx->grid.n_y;
+    CU(cudaMemsetAsync(ctx->d.p, 0, (size_t)ctx->K * n * 8, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  }
+  const int K = ctx->K;
+  const double* Sk = ctx->h_cs + 3 * K;
+  const double* rrk = ctx->h_cs + 4 * K;
+  if (cond_rel)
+    for (int k = 0; k < K; ++k) cond_rel[k] = (Sk[k] > 0.0) ? std::sqrt(rrk[k]) / std::sqrt(Sk[k]) : 0.0;
+  if (out) {
+    out->iterations = hs->iter;
+    out->converged = hs->converged;
+    out->status = hs->status;
+    out->precond = precond;
+    out->rel_residual = hs->rel;
+    out->true_rel_residual = hs->true_rel;
+    out->solve_ms = ms;
+  }
+  ctx->r_parity = hs->iter & 1;
+  ctx->state = ST_SOLVED;
+  if (hs->status == GMAF_E_BREAKDOWN)
+    return fail(ctx, GMAF_E_BREAKDOWN, "solve: breakdown at iteration %d (u.v<=0 or r.z<=0)", hs->iter);
+  if (hs->status == GMAF_E_NO_CONVERGENCE)
+    return fail(ctx, GMAF_E_NO_CONVERGENCE, "solve: no convergence after %d iterations (rel %.3e)",
+                hs->iter, hs->rel);
+  return GMAF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gmaf_version(void) { return "gmaf-b200 0.1 (sm_100a)"; }
+
+size_t gmaf_workspace_bytes(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist) {
+  if (check_grid(grid) != GMAF_OK || K < 1) return 0;
+  if (dist && (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)) return 0;
+  return make_layout(grid, K).total;
+}
+
+gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist, void* d_workspace,
+                        size_t ws_bytes, void* cuda_stream, gmaf_ctx** out) {
+  if (!out) return GMAF_E_INVALID_ARG;
+  *out = nullptr;
+  int rc = check_grid(grid);
+  if (rc != GMAF_OK) return (gmaf_status)rc;
+  if (K < 1) return GMAF_E_INVALID_ARG;
+  if (dist && dist->world != 1) return GMAF_E_INVALID_ARG;  // multi-rank: see gmaf_dist in DESIGN.md
+  const Layout L = make_layout(grid, K);
+  if (!d_workspace || ws_bytes < L.total || (reinterpret_cast<uintptr_t>(d_workspace) % kAlign) != 0)
+    return GMAF_E_WORKSPACE;
+  gmaf_ctx* ctx = new (std::nothrow) gmaf_ctx();
+  if (!ctx) return GMAF_E_INVALID_ARG;
+  ctx->grid = *grid;
+  ctx->K = K;
+  ctx->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  ctx->ws = reinterpret_cast<char*>(d_workspace);
+  ctx->ws_bytes = ws_bytes;
+  ctx->L = L;
+  ctx->tiles = make_tiles(grid->n_theta, grid->n_y, K);
+  GridParams& gp = ctx->gp;
+  gp.nt = grid->n_theta; gp.ny = grid->n_y; gp.Rk = grid->R_k; gp.Rc = grid->R_c; gp.mu = grid->mu;
+  gp.hmin = grid->h_min;
+  gp.twelve_mu = 12.0 * grid->mu;
+  gp.dtheta = (2.0 * M_PI) / (double)grid->n_theta;
+  const bool tex = grid->tex_n_theta > 0 && grid->tex_n_y > 0;
+  gp.tex_nt = tex ? grid->tex_n_theta : 0; gp.tex_ny = tex ? grid->tex_n_y : 0;
+  gp.tex_band = tex ? grid->tex_band_rows : 0; gp.tex_num = grid->tex_fill_num;
+  gp.tex_den = grid->tex_fill_den > 0 ? grid->tex_fill_den : 1; gp.tex_depth = grid->tex_depth;
+  DevPtrs& d = ctx->d;
+  d.ct = at<double>(ctx, L.off_ct); d.st = at<double>(ctx, L.off_st);
+  d.cth = at<double>(ctx, L.off_cth); d.sth = at<double>(ctx, L.off_sth);
+  d.cp = at<CondParams>(ctx, L.off_cp);
+  d.AP = at<double>(ctx, L.off_AP); d.AE = at<double>(ctx, L.off_AE); d.AN = at<double>(ctx, L.off_AN);
+  d.S = at<double>(ctx, L.off_S); d.p = at<double>(ctx, L.off_p);
+  d.r[0] = at<double>(ctx, L.off_r); d.r[1] = at<double>(ctx, L.off_r2);
+  d.u[0] = at<double>(ctx, L.off_u); d.u[1] = at<double>(ctx, L.off_u2);
+  d.scratch = at<double>(ctx, L.off_scratch);
+  d.partials = at<double>(ctx, L.off_part); d.wrench_part = at<double>(ctx, L.off_wpart);
+  d.wrench = at<double>(ctx, L.off_wrench); d.st_ = at<SolverState>(ctx, L.off_state);
+  double* cs = at<double>(ctx, L.off_cs);
+  d.cs.alpha = cs; d.cs.beta = cs + K; d.cs.dk = cs + 2 * K; d.cs.Sk = cs + 3 * K; d.cs.rrk = cs + 4 * K;
+  d.cs.uvk = cs + 5 * K; d.cs.ttk = cs + 6 * K;
+  d.counters = at<unsigned int>(ctx, L.off_counters);
+  d.timing = at<Timing>(ctx, L.off_timing);
+  d.guard = at<unsigned long long>(ctx, L.off_guard);
+  d.mat_rep = at<int32_t>(ctx, L.off_matrep);
+
+  auto cleanup_fail = [&](gmaf_status s) { gmaf_destroy(ctx); return s; };
+  if (cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
+      cudaMallocHost((void**)&ctx->h_state, sizeof(SolverState)) != cudaSuccess ||
+      cudaMallocHost((void**)&ctx->h_cs, (size_t)7 * K * 8) != cudaSuccess ||
+      cudaMallocHost((void**)&ctx->h_wrench, (size_t)K * 12 * 8) != cudaSuccess ||
+      cudaMallocHost((void**)&ctx->h_guard, 4 * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMallocHost((void**)&ctx->h_cp, (size_t)K * sizeof(CondParams)) != cudaSuccess ||
+      cudaMallocHost((void**)&ctx->h_timing, sizeof(Timing)) != cudaSuccess)
+    return cleanup_fail(GMAF_E_CUDA);
+  // cos/sin tables with the host libm (shared by nobody: the oracle computes its own)
+  const int nt = grid->n_theta;
+  std::vector<double> tab((size_t)4 * nt);
+  for (int i = 0; i < nt; ++i) {
+    const double th = (double)i * gp.dtheta;
+    const double thc = ((double)i + 0.5) * gp.dtheta;
+    tab[i] = std::cos(th); tab[nt + i] = std::sin(th);
+    tab[2 * nt + i] = std::cos(thc); tab[3 * nt + i] = std::sin(thc);
+  }
+  if (cudaMemcpyAsync((void*)d.ct, tab.data(), nt * 8, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
+      cudaMemcpyAsync((void*)d.st, tab.data() + nt, nt * 8, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
+      cudaMemcpyAsync((void*)d.cth, tab.data() + 2 * nt, nt * 8, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
+      cudaMemcpyAsync((void*)d.sth, tab.data() + 3 * nt, nt * 8, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
+      cudaMemsetAsync(d.counters, 0, 16 * sizeof(unsigned int), ctx->stream) != cudaSuccess ||
+      cudaMemsetAsync(d.st_, 0, sizeof(SolverState), ctx->stream) != cudaSuccess ||
+      cudaMemsetAsync(d.p, 0, (size_t)K * gp.nt * gp.ny * 8, ctx->stream) != cudaSuccess)
+    return cleanup_fail(GMAF_E_CUDA);
+  std::memset(ctx->h_timing, 0, sizeof(Timing));
+  for (int q = 0; q < KK_COUNT; ++q) ctx->h_timing->t_start[q] = ~0ull;
+  if (cudaMemcpyAsync(d.timing, ctx->h_timing, sizeof(Timing), cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess)
+    return cleanup_fail(GMAF_E_CUDA);
+  if (configure_pcg_kernels(ctx->tiles, K) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
+  if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
+  ctx->quad_ctas = quad_ctas_per_condition(gp, K);
+  *out = ctx;
+  return GMAF_OK;
+}
+
+gmaf_status gmaf_destroy(gmaf_ctx* ctx) {
+  if (!ctx) return GMAF_E_INVALID_ARG;
+  for (auto& kv : ctx->graphs) {
+    if (kv.second.second) cudaGraphExecDestroy(kv.second.second);
+    if (kv.second.first) cudaGraphDestroy(kv.second.first);
+  }
+  if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->h_state) cudaFreeHost(ctx->h_state);
+  if (ctx->h_cs) cudaFreeHost(ctx->h_cs);
+  if (ctx->h_wrench) cudaFreeHost(ctx->h_wrench);
+  if (ctx->h_guard) cudaFreeHost(ctx->h_guard);
+  if (ctx->h_cp) cudaFreeHost(ctx->h_cp);
+  if (ctx->h_timing) cudaFreeHost(ctx->h_timing);
+  delete ctx;
+  return GMAF_OK;
+}
+
+gmaf_status gmaf_thickness(gmaf_ctx* ctx, const gmaf_condition* conds) {
+  if (!ctx || !conds) return GMAF_E_INVALID_ARG;
+  const int K = ctx->K;
+  ctx->mat_of.assign(K, 0);
+  ctx->mat_rep.clear();
+  for (int k = 0; k < K; ++k) {
+    if (!(conds[k].L_F > 0.0)) return fail(ctx, GMAF_E_INVALID_ARG, "thickness: k=%d L_F <= 0", k);
+    int m = -1;
+    for (int q = 0; q < (int)ctx->mat_rep.size(); ++q)
+      if (same_matrix(conds[ctx->mat_rep[q]], conds[k])) { m = q; break; }
+    if (m < 0) { m = (int)ctx->mat_rep.size(); ctx->mat_rep.push_back(k); }
+    ctx->mat_of[k] = m;
+    ctx->h_cp[k] = cond_params(ctx->grid, conds[k], m);
+  }
+  ctx->M = (int)ctx->mat_rep.size();
+  ctx->state = ST_CREATED;
+  CU(cudaMemcpyAsync((void*)ctx->d.cp, ctx->h_cp, (size_t)K * sizeof(CondParams), cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CU(cudaMemcpyAsync(ctx->d.mat_rep, ctx->mat_rep.data(), (size_t)ctx->M * sizeof(int32_t),
+                     cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaMemsetAsync(ctx->d.guard, 0, 4 * sizeof(unsigned long long), ctx->stream));
+  CU(launch_thickness_guard(ctx->gp, ctx->d, K, ctx->stream));
+  CU(cudaMemcpyAsync(ctx->h_guard, ctx->d.guard, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                     ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  if (ctx->h_guard[0]) {
+    double h;
+    const unsigned long long bits = ctx->h_guard[3];
+    std::memcpy(&h, &bits, sizeof(h));
+    const int i = (int)(ctx->h_guard[2] >> 32), j = (int)(ctx->h_guard[2] & 0xffffffffu) - 1;
+    return fail(ctx, GMAF_E_NONPOSITIVE_THICKNESS, "thickness: k=%d i=%d j=%d h=%.6e < h_min=%.3e",
+                (int)ctx->h_guard[1], i, j, h, ctx->grid.h_min);
+  }
+  ctx->state = ST_THICK;
+  return GMAF_OK;
+}
+
+gmaf_status gmaf_assemble(gmaf_ctx* ctx) {
+  if (!ctx) return GMAF_E_INVALID_ARG;
+  if (ctx->state < ST_THICK) return fail(ctx, GMAF_E_STATE, "assemble before thickness");
+  CU(launch_assemble(ctx->gp, ctx->d, ctx->K, ctx->stream));
+  ctx->state = ST_ASSEMBLED;
+  return GMAF_OK;
+}
+
+gmaf_status gmaf_solve(gmaf_ctx* ctx, double tol, double omega, int32_t precond, int32_t coupling,
+                       int32_t max_iter, int32_t warm_start, gmaf_solve_stats* out, double* cond_rel) {
+  if (!ctx) return GMAF_E_INVALID_ARG;
+  if (ctx->state < ST_ASSEMBLED) return fail(ctx, GMAF_E_STATE, "solve before assemble");
+  if (!(tol >= 0.0) || !(omega > 0.0 && omega < 2.0) || precond < 0 || precond > 2 || coupling < 0 ||
+      coupling > 1 || max_iter < 0)
+    return fail(ctx, GMAF_E_INVALID_ARG, "solve: invalid tol/omega/precond/coupling/max_iter");
+  return run_solve(ctx, tol, omega, precond, coupling, max_iter, warm_start, 0, out, cond_rel);
+}
+
+gmaf_status gmaf_solve_fixed(gmaf_ctx* ctx, double omega, int32_t precond, int32_t n_iter,
+                             gmaf_solve_stats* out) {
+  if (!ctx) return GMAF_E_INVALID_ARG;
+  if (ctx->state < ST_ASSEMBLED) return fail(ctx, GMAF_E_STATE, "solve before assemble");
+  if (n_iter < 1 || !(omega > 0.0 && omega < 2.0) || precond < 0 || precond > 2)
+    return fail(ctx, GMAF_E_INVALID_ARG, "solve_fixed: invalid arguments");
+  return run_solve(ctx, 0.0, omega, precond, 0, n_iter, 0, n_iter, out, nullptr);
+}
+
+gmaf_status gmaf_integrate(gmaf_ctx* ctx, double* wrench) {
+  if (!ctx || !wrench) return GMAF_E_INVALID_ARG;
+  if (ctx->state < ST_SOLVED) return fail(ctx, GMAF_E_STATE, "integrate before solve");
+  CU(launch_quadrature(ctx->gp, ctx->d, ctx->K, ctx->stream, nullptr));
+  CU(cudaMemcpyAsync(ctx->h_wrench, ctx->d.wrench, (size_t)ctx->K * 12 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(wrench, ctx->h_wrench, (size_t)ctx->K * 12 * 8);
+  return GMAF_OK;
+}
+
+gmaf_status gmaf_field_ptr(gmaf_ctx* ctx, int32_t field, int32_t k, void** dptr) {
+  if (!ctx || !dptr || k < 0 || k >= ctx->K) return GMAF_E_INVALID_ARG;
+  const size_t n = (size_t)ctx->grid.n_theta * ctx->grid.n_y;
+  const size_t m = ctx->mat_of.empty() ? 0 : (size_t)ctx->mat_of[k];
+  switch (field) {
+    case GMAF_FIELD_P: *dptr = ctx->d.p + k * n; break;
+    case GMAF_FIELD_S: *dptr = ctx->d.S + k * n; break;
+    case GMAF_FIELD_R: *dptr = ctx->d.r[ctx->r_parity] + k * n; break;   // latest residual
+    case GMAF_FIELD_AP: *dptr = ctx->d.AP + m * n; break;
+    case GMAF_FIELD_AE: *dptr = ctx->d.AE + m * n; break;
+    case GMAF_FIELD_AN: *dptr = ctx->d.AN + m * n; break;
+    default: return fail(ctx, GMAF_E_INVALID_ARG, "field_ptr: field %d has no persistent buffer", field);
+  }
+  return GMAF_OK;
+}
+
+gmaf_status gmaf_get(gmaf_ctx* ctx, int32_t field, int32_t k, double* host_out) {
+  if (!ctx || !host_out || k < 0 || k >= ctx->K) return GMAF_E_INVALID_ARG;
+  const size_t n = (size_t)ctx->grid.n_theta * ctx->grid.n_y;
+  if (field == GMAF_FIELD_H || field == GMAF_FIELD_HDOT) {
+    if (ctx->state < ST_THICK) return fail(ctx, GMAF_E_STATE, "get H before thickness");
+    CU(launch_field(ctx->gp, ctx->d, field, k, ctx->stream));
+    CU(cudaMemcpyAsync(host_out, ctx->d.scratch, (size_t)(ctx->grid.n_y + 2) * ctx->grid.n_theta * 8,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return GMAF_OK;
+  }
+  if ((field == GMAF_FIELD_AP || field == GMAF_FIELD_AE || field == GMAF_FIELD_AN || field == GMAF_FIELD_S) &&
+      ctx->state < ST_ASSEMBLED)
+    return fail(ctx, GMAF_E_STATE, "get bands before assemble");
+  void* src = nullptr;
+  gmaf_status s = gmaf_field_ptr(ctx, field, k, &src);
+  if (s != GMAF_OK) return s;
+  CU(cudaMemcpyAsync(host_out, src, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return GMAF_OK;
+}
+
+gmaf_status gmaf_kernel_times(gmaf_ctx* ctx, gmaf_kernel_timing* out, int32_t n, int32_t* count) {
+  if (!ctx || !out || !count) return GMAF_E_INVALID_ARG;
+  CU(cudaMemcpyAsync(ctx->h_timing, ctx->d.timing, sizeof(Timing), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  static const char* names[KK_COUNT] = {"thickness_guard", "assemble", "pcg_init", "pcg_phase_a",
+                                        "pcg_phase_b", "true_residual", "quadrature"};
+  const double n_nodes = (double)ctx->grid.n_theta * ctx->grid.n_y * ctx->K;
+  const double nM = (double)ctx->grid.n_theta * ctx->grid.n_y * (ctx->M > 0 ? ctx->M : ctx->K);
+  // algorithmic DRAM bytes per launch
+  const double bytes[KK_COUNT] = {
+      0.0,                                  // guard: pure compute, no field traffic
+      8.0 * (n_nodes + 3.0 * nM),           // assemble: write S (K) + 3 bands (M)
+      8.0 * (3.0 * n_nodes + 3.0 * n_nodes),// init: read S (+p), 3 bands; write r, p
+      8.0 * (3.0 * n_nodes + 3.0 * n_nodes),// A: read r, u, write u; 3 bands per condition
+      8.0 * (5.0 * n_nodes + 3.0 * n_nodes),// B: read p, u, r; write p, r; 3 bands
+      8.0 * (2.0 * n_nodes + 3.0 * n_nodes),// true residual: read S, p; 3 bands
+      8.0 * n_nodes};                       // quadrature: read p
+  int c = 0;
+  for (int q = 0; q < KK_COUNT && c < n; ++q, ++c) {
+    std::memset(&out[c], 0, sizeof(gmaf_kernel_timing));
+    std::snprintf(out[c].name, sizeof(out[c].name), "%s", names[q]);
+    out[c].launches = (int64_t)ctx->h_timing->launches[q];
+    out[c].total_ms = (double)ctx->h_timing->total_ns[q] * 1e-6;
+    out[c].bytes_per_launch = bytes[q];
+  }
+  *count = c;
+  return GMAF_OK;
+}
+
+gmaf_status gmaf_reset_kernel_times(gmaf_ctx* ctx) {
+  if (!ctx) return GMAF_E_INVALID_ARG;
+  std::memset(ctx->h_timing, 0, sizeof(Timing));
+  for (int q = 0; q < KK_COUNT; ++q) ctx->h_timing->t_start[q] = ~0ull;
+  CU(cudaMemcpyAsync(ctx->d.timing, ctx->h_timing, sizeof(Timing), cudaMemcpyHostToDevice, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  return GMAF_OK;
+}
+
+const char* gmaf_last_error(const gmaf_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+}  // extern "C"

@@ -1,0 +1,115 @@
+// gmaf_internal.cuh -- device-side data structures and kernel launchers of libgmaf.
+// Not part of the ABI (see include/gmaf.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace gmaf {
+
+// Per-condition parameters.  Every derived scalar is computed on the host with the
+// same IEEE operations, in the same order, as the thickness/assembly definition
+// (DESIGN.md sec. 5), so that device thickness and bands are bitwise reproducible.
+struct CondParams {
+  double e[4], edot[4];
+  double LF, Ut, Uy, pin, pout;
+  double dy;      // L_F / (n_y + 1)
+  double dx;      // R_k * dtheta
+  double rx, ry;  // dy/dx, dx/dy
+  double sl, tl;  // (e3-e1)/L_F, (e4-e2)/L_F
+  double sld, tld;// (edot3-edot1)/L_F, (edot4-edot2)/L_F
+  int32_t mat;    // index of the distinct coefficient set used by this condition
+  int32_t pad;
+};
+
+struct GridParams {
+  int32_t nt, ny;
+  double Rk, Rc, mu, hmin, twelve_mu, dtheta;
+  int32_t tex_nt, tex_ny, tex_band, tex_num, tex_den;
+  double tex_depth;
+};
+
+// Kernel kinds for the in-kernel %globaltimer accounting.
+enum KernelKind { KK_THICK = 0, KK_ASSEMBLE, KK_INIT, KK_PHASE_A, KK_PHASE_B, KK_TRUERES, KK_QUAD,
+                  KK_COUNT };
+
+struct Timing {
+  unsigned long long t_start[KK_COUNT];   // min start of the current launch (ULLONG_MAX = idle)
+  unsigned long long total_ns[KK_COUNT];
+  unsigned long long launches[KK_COUNT];
+};
+
+// Solver state resident on the device.  The host writes the parameter block before a
+// graph launch; kernels update the rest; the host reads it back after the solve.
+struct SolverState {
+  // parameters
+  double tol, omega;
+  int32_t coupling, max_iter, fixed_iters, pad0;
+  // global scalars
+  double d;           // coupled: sum_k r.z
+  double nS;          // ||S_G||
+  double rel;         // recursive ||r||/||S_G||
+  double true_rel;
+  int32_t iter, done, converged, status;
+  int32_t zero_p, pad1, pad2, pad3;
+};
+
+// Per-condition scalar arrays (length K each) carved next to SolverState.
+struct CondScalars {
+  double* alpha;   // [K]
+  double* beta;    // [K]
+  double* dk;      // [K] r_k.z_k
+  double* Sk;      // [K] S_k.S_k
+  double* rrk;     // [K] r_k.r_k
+  double* uvk;     // [K]
+  double* ttk;     // [K] true residual^2
+};
+
+struct DevPtrs {
+  const double* ct; const double* st;      // cos/sin(i dtheta)
+  const double* cth; const double* sth;    // cos/sin((i+1/2) dtheta)
+  const CondParams* cp;                    // [K]
+  double* AP; double* AE; double* AN;      // [M][n]
+  double* S; double* p;                    // [K][n]
+  double* r[2]; double* u[2];              // [K][n] ping-pong (halo reads never race with writes)
+  double* scratch;                         // [(n_y+2) n_theta] field readback
+  double* partials;                        // [4][K][n_cta_max]
+  double* wrench_part;                     // [K][n_cta_q][12]
+  double* wrench;                          // [K][12]
+  SolverState* st_;
+  CondScalars cs;
+  unsigned int* counters;                  // [8] last-CTA counters
+  Timing* timing;
+  unsigned long long* guard;               // [4]: flag, k, i|j, h bits
+  int32_t* mat_rep;                        // [M] representative condition of each matrix
+};
+
+// Marching-tile configuration of the PCG kernels.
+struct TileCfg {
+  int32_t tw;        // output columns per strip (threads = tw + 2*HALO)
+  int32_t th;        // output rows per chunk
+  int32_t n_strips, n_chunks, n_tiles;  // tiles per condition
+};
+
+constexpr int HALO = 3;   // theta halo columns on each side (ASSOR-II + SpMV + seam)
+
+// ---- launchers (geometry.cu) ----
+cudaError_t launch_thickness_guard(const GridParams& g, const DevPtrs& d, int K, cudaStream_t s);
+cudaError_t launch_assemble(const GridParams& g, const DevPtrs& d, int K, cudaStream_t s);
+cudaError_t launch_field(const GridParams& g, const DevPtrs& d, int field, int k, cudaStream_t s);
+cudaError_t launch_quadrature(const GridParams& g, const DevPtrs& d, int K, cudaStream_t s,
+                              int* n_cta_out);
+
+// ---- launchers (pcg.cu) ----
+// precond: 0 none, 1 jacobi, 2 assor2.  cond_handle: graph conditional handle or 0.
+cudaError_t launch_init(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,
+                        bool warm, unsigned long long cond_handle, cudaStream_t s);
+// parity = iteration index mod 2: phase A reads u[1-parity], writes u[parity], reads r[parity];
+// phase B reads u[parity], r[parity] and writes r[1-parity].
+cudaError_t launch_phase_a(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K,
+                           int precond, int parity, unsigned long long cond_handle, cudaStream_t s);
+cudaError_t launch_phase_b(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K,
+                           int precond, int parity, unsigned long long cond_handle, cudaStream_t s);
+cudaError_t launch_true_residual(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K,
+                                 cudaStream_t s);
+
+}  // namespace gmaf

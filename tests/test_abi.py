@@ -1,0 +1,66 @@
+"""CPU-side checks of the boundary: the C-ABI library loads and exports every symbol
+that include/gmaf.h declares; struct layouts of the binding match the header; the
+workspace sizing and argument validation need no GPU."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    from paper_2511_06824_b200 import build as B
+    B.build()
+    import paper_2511_06824_b200 as P
+    return P
+
+
+def _declared():
+    hdr = open(os.path.join(ROOT, "include", "gmaf.h")).read()
+    return sorted(set(re.findall(r"\b(gmaf_[a-z_]+)\s*\(", hdr)))
+
+
+def test_exports_every_declared_symbol(pkg):
+    L = pkg.lib()
+    names = _declared()
+    assert "gmaf_solve" in names and "gmaf_create" in names
+    for n in names:
+        assert hasattr(L, n), n
+    assert set(pkg.ABI_SYMBOLS) <= set(names)
+
+
+def test_version_and_sizes(pkg):
+    assert b"sm_100a" in pkg.lib().gmaf_version()
+    import gmaf_inputs as gi
+    g = pkg.make_grid(gi.grid(2048, 1024, "short"))
+    nb = pkg.gmaf_workspace_bytes(g, 9)
+    n = 2048 * 1024 * 9 * 8
+    assert 7 * n <= nb <= 7 * n + (64 << 20)      # 7 fields of K*n doubles + small state
+    assert C.sizeof(pkg.gmaf_condition) == 13 * 8
+    assert C.sizeof(pkg.gmaf_grid) == 4 + 4 + 4 * 8 + 5 * 4 + 4 + 8
+
+
+def test_validation_without_gpu(pkg):
+    import gmaf_inputs as gi
+    assert pkg.gmaf_workspace_bytes(pkg.make_grid(gi.grid(3, 32)), 1) == 0          # INVALID_MESH
+    assert pkg.gmaf_workspace_bytes(pkg.make_grid(gi.grid(100, 80, "short")), 1) == 0  # too coarse
+    assert pkg.gmaf_workspace_bytes(pkg.make_grid(gi.grid(64, 32)), 0) == 0
+    ctx = C.c_void_p()
+    g = pkg.make_grid(gi.grid(64, 32))
+    # a NULL workspace is rejected before any CUDA call
+    code = pkg.lib().gmaf_create(C.byref(g), 1, None, None, 0, None, C.byref(ctx))
+    assert code == -8
+
+
+def test_no_cpu_fallback_in_product():
+    """The product package never imports the oracle (the oracle is test infrastructure)."""
+    src_dir = os.path.join(ROOT, "paper_2511_06824_b200")
+    for dirpath, _, files in os.walk(src_dir):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, f
+                assert "gmaf_oracle" not in txt, f

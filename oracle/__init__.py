@@ -82,6 +82,7 @@ def lib():
         _lib.orc_pcg_joint.argtypes = [C.c_int32, C.c_int32, C.c_int32, D, D, D, D, D, C.c_double,
                                        C.c_double, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                        C.POINTER(_Stats), D, D]
+        _lib.orc_pcg_joint_sr.argtypes = _lib.orc_pcg_joint.argtypes
         _lib.orc_pcg_async.argtypes = [C.c_int32, C.c_int32, C.c_int32, D, D, D, D, D, C.c_double,
                                        C.c_double, C.c_int32, C.c_int32, C.POINTER(C.c_int32),
                                        C.POINTER(_Stats)]
@@ -219,8 +220,10 @@ class SolveResult:
 
 
 def pcg_joint(AP, AE, AN, S, tol=1e-10, omega=1.8, precond="assor2", coupling="coupled",
-              max_iter=100000, p0=None, history=False) -> SolveResult:
-    """O7: joint PCG over K stacked conditions (arrays [K][n_y][n_theta] or [n_y][n_theta])."""
+              max_iter=100000, p0=None, history=False, schedule="table1") -> SolveResult:
+    """O7: joint PCG over K stacked conditions (arrays [K][n_y][n_theta] or [n_y][n_theta]).
+    schedule="table1": Table 1 with two reductions per iteration; "single": the same
+    method with one (gamma, delta, r.r) reduction per iteration (orc_pcg_joint_sr)."""
     squeeze = AP.ndim == 2
     if squeeze:
         AP, AE, AN, S = (x[None] for x in (AP, AE, AN, S))
@@ -230,7 +233,8 @@ def pcg_joint(AP, AE, AN, S, tol=1e-10, omega=1.8, precond="assor2", coupling="c
     cond_rel = np.zeros(K)
     st = _Stats()
     arrs = [np.ascontiguousarray(x, dtype=np.float64) for x in (AP, AE, AN, S)]
-    rc = lib().orc_pcg_joint(nt, ny, K, *(_ptr(a) for a in arrs), _ptr(p), tol, omega,
+    fn = lib().orc_pcg_joint if schedule == "table1" else lib().orc_pcg_joint_sr
+    rc = fn(nt, ny, K, *(_ptr(a) for a in arrs), _ptr(p), tol, omega,
                              PRECOND[precond], COUPLING[coupling], max_iter, int(p0 is not None),
                              C.byref(st), _ptr(hist), _ptr(cond_rel))
     if hist is not None:

@@ -422,6 +422,121 @@ int orc_pcg_joint(int32_t nt, int32_t ny, int32_t K,
   return status;
 }
 
+/* O7-S3: the same PCG (Table 1) written with a single global reduction per
+ * iteration (Chronopoulos & Gear's reformulation; SURVEY 8(c) O7 "S3 mode",
+ * 8(e)): the search direction pd and s = A pd are updated as in Table 1 steps
+ * 3-5/9, but alpha is obtained from gamma = r.z and delta = z.(A z) of the SAME
+ * iterate, alpha_{j+1} = gamma_{j+1} / (delta_{j+1} - beta_{j+1} gamma_{j+1} / alpha_j),
+ * which equals d / (u.A u) of Table 1 in exact arithmetic.  One (gamma, delta, r.r)
+ * reduction per iteration is what the single-pass GPU schedule computes. */
+int orc_pcg_joint_sr(int32_t nt, int32_t ny, int32_t K,
+                     const double* AP, const double* AE, const double* AN, const double* S,
+                     double* p, double tol, double omega, int32_t precond, int32_t coupling,
+                     int32_t max_iter, int32_t warm, orc_stats* st, double* history, double* cond_rel) {
+  if (nt < 4 || ny < 4 || K < 1 || max_iter < 0) return ORC_E_INVALID_ARG;
+  const size_t n = (size_t)nt * ny, N = n * (size_t)K;
+  double* r = (double*)malloc(N * sizeof(double));
+  double* z = (double*)malloc(N * sizeof(double));
+  double* w = (double*)malloc(N * sizeof(double));
+  double* pd = (double*)calloc(N, sizeof(double));
+  double* sv = (double*)malloc(N * sizeof(double));
+  double* gk = (double*)calloc((size_t)K, sizeof(double));
+  double* dk = (double*)calloc((size_t)K, sizeof(double));
+  double* ak = (double*)calloc((size_t)K, sizeof(double));
+  double* bk = (double*)calloc((size_t)K, sizeof(double));
+  double* Sk = (double*)calloc((size_t)K, sizeof(double));
+#define BLK(ptr, k) ((ptr) + (size_t)(k) * n)
+  if (!warm) memset(p, 0, N * sizeof(double));
+  double SS = 0.0, rr = 0.0;
+  for (int32_t k = 0; k < K; ++k) {
+    orc_spmv(nt, ny, BLK(AP, k), BLK(AE, k), BLK(AN, k), BLK(p, k), BLK(sv, k));
+    for (size_t q = 0; q < n; ++q) BLK(r, k)[q] = BLK(S, k)[q] - BLK(sv, k)[q];
+    orc_precond_apply(nt, ny, BLK(AP, k), BLK(AE, k), BLK(AN, k), precond, omega, BLK(r, k), BLK(z, k));
+    orc_spmv(nt, ny, BLK(AP, k), BLK(AE, k), BLK(AN, k), BLK(z, k), BLK(w, k));
+    gk[k] = dot(n, BLK(r, k), BLK(z, k));
+    dk[k] = dot(n, BLK(z, k), BLK(w, k));
+    Sk[k] = dot(n, BLK(S, k), BLK(S, k));
+  }
+  for (int32_t k = 0; k < K; ++k) SS += Sk[k];
+  for (int32_t k = 0; k < K; ++k) rr += dot(n, BLK(r, k), BLK(r, k));
+  const double nS = sqrt(SS);
+  int status = ORC_OK, converged = 0, it = 0;
+  double rel = (nS > 0.0) ? sqrt(rr) / nS : 0.0;
+  if (history) history[0] = rel;
+  double gam = 0.0, alpha = 0.0, beta = 0.0;
+  if (nS == 0.0) { memset(p, 0, N * sizeof(double)); converged = 1; }
+  else if (rel <= tol) converged = 1;
+  else {
+    if (coupling == ORC_COUPLED) {
+      double dl = 0.0;
+      for (int32_t k = 0; k < K; ++k) { gam += gk[k]; dl += dk[k]; }
+      if (!(dl > 0.0)) status = ORC_E_BREAKDOWN;
+      alpha = gam / dl;
+    } else {
+      for (int32_t k = 0; k < K; ++k) {
+        ak[k] = 0.0;
+        if (gk[k] != 0.0) { if (!(dk[k] > 0.0)) status = ORC_E_BREAKDOWN; ak[k] = gk[k] / dk[k]; }
+      }
+    }
+  }
+  for (int32_t j = 0; status == ORC_OK && !converged && j < max_iter; ++j) {
+    for (int32_t k = 0; k < K; ++k) {
+      const double a = (coupling == ORC_COUPLED) ? alpha : ak[k];
+      const double b = (coupling == ORC_COUPLED) ? beta : bk[k];
+      for (size_t q = 0; q < n; ++q) BLK(pd, k)[q] = BLK(z, k)[q] + b * BLK(pd, k)[q];   /* step 9 */
+      orc_spmv(nt, ny, BLK(AP, k), BLK(AE, k), BLK(AN, k), BLK(pd, k), BLK(sv, k));    /* step 3 */
+      for (size_t q = 0; q < n; ++q) BLK(p, k)[q] = BLK(p, k)[q] + a * BLK(pd, k)[q];  /* step 4 */
+      for (size_t q = 0; q < n; ++q) BLK(r, k)[q] = BLK(r, k)[q] - a * BLK(sv, k)[q];  /* step 5 */
+    }
+    rr = 0.0;
+    for (int32_t k = 0; k < K; ++k) rr += dot(n, BLK(r, k), BLK(r, k));
+    rel = sqrt(rr) / nS;
+    it = j + 1;
+    if (history) history[it] = rel;
+    if (rel <= tol) { converged = 1; break; }                                            /* step 6 */
+    for (int32_t k = 0; k < K; ++k) {                                                    /* step 7-8 */
+      orc_precond_apply(nt, ny, BLK(AP, k), BLK(AE, k), BLK(AN, k), precond, omega, BLK(r, k), BLK(z, k));
+      orc_spmv(nt, ny, BLK(AP, k), BLK(AE, k), BLK(AN, k), BLK(z, k), BLK(w, k));
+    }
+    if (coupling == ORC_COUPLED) {
+      double g2 = 0.0, d2 = 0.0;
+      for (int32_t k = 0; k < K; ++k) { g2 += dot(n, BLK(r, k), BLK(z, k)); d2 += dot(n, BLK(z, k), BLK(w, k)); }
+      if (!(g2 > 0.0)) { status = ORC_E_BREAKDOWN; break; }
+      beta = g2 / gam;
+      const double den = d2 - beta * g2 / alpha;
+      if (!(den > 0.0)) { status = ORC_E_BREAKDOWN; break; }
+      alpha = g2 / den;
+      gam = g2;
+    } else {
+      for (int32_t k = 0; k < K; ++k) {
+        const double g2 = dot(n, BLK(r, k), BLK(z, k)), d2 = dot(n, BLK(z, k), BLK(w, k));
+        if (gk[k] == 0.0 || ak[k] == 0.0) { ak[k] = 0.0; bk[k] = 0.0; gk[k] = g2; continue; }
+        if (g2 < 0.0) { status = ORC_E_BREAKDOWN; break; }
+        bk[k] = g2 / gk[k];
+        const double den = d2 - bk[k] * g2 / ak[k];
+        ak[k] = (g2 == 0.0) ? 0.0 : g2 / den;
+        gk[k] = g2;
+      }
+    }
+  }
+  if (status == ORC_OK && !converged) status = ORC_E_NO_CONVERGENCE;
+  double tr = 0.0;
+  for (int32_t k = 0; k < K; ++k) {
+    orc_spmv(nt, ny, BLK(AP, k), BLK(AE, k), BLK(AN, k), BLK(p, k), BLK(sv, k));
+    double tk = 0.0;
+    for (size_t q = 0; q < n; ++q) { const double e = BLK(S, k)[q] - BLK(sv, k)[q]; tk += e * e; }
+    tr += tk;
+    if (cond_rel) cond_rel[k] = (Sk[k] > 0.0) ? sqrt(dot(n, BLK(r, k), BLK(r, k))) / sqrt(Sk[k]) : 0.0;
+  }
+  if (st) {
+    st->iterations = it; st->converged = converged; st->status = status; st->rel_residual = rel;
+    st->true_rel_residual = (nS > 0.0) ? sqrt(tr) / nS : 0.0;
+  }
+#undef BLK
+  free(r); free(z); free(w); free(pd); free(sv); free(gk); free(dk); free(ak); free(bk); free(Sk);
+  return status;
+}
+
 /* Asynchronous strategy (Eq. 3.10): per-block Krylov processes,
  * each frozen at its own convergence. */
 int orc_pcg_async(int32_t nt, int32_t ny, int32_t K,

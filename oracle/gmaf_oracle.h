@@ -107,6 +107,14 @@ int  orc_pcg_joint(int32_t nt, int32_t ny, int32_t K,
                    double* p, double tol, double omega, int32_t precond, int32_t coupling,
                    int32_t max_iter, int32_t warm, orc_stats* st, double* history, double* cond_rel);
 
+/* O7-S3: Table 1 with one global reduction per iteration (Chronopoulos-Gear alpha
+ * recurrence); same arguments as orc_pcg_joint.  This is the schedule
+ * the single-pass GPU kernel follows, so iterates can be compared step by step. */
+int  orc_pcg_joint_sr(int32_t nt, int32_t ny, int32_t K,
+                      const double* AP, const double* AE, const double* AN, const double* S,
+                      double* p, double tol, double omega, int32_t precond, int32_t coupling,
+                      int32_t max_iter, int32_t warm, orc_stats* st, double* history, double* cond_rel);
+
 /* Asynchronous strategy (Eq. 3.10, NEXT-2): per-block PCG, block frozen once
  * ||r_k||/||S_k|| <= tol.  iters_k (K) receives per-block iteration counts. */
 int  orc_pcg_async(int32_t nt, int32_t ny, int32_t K,

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <new>
@@ -26,6 +27,7 @@
 namespace gmaf {
 int quad_ctas_per_condition(const GridParams& g, int K);
 cudaError_t configure_pcg_kernels(const TileCfg& t, int K);
+int pcg_ctas_per_sm(const TileCfg& t, int K);
 }
 
 using namespace gmaf;
@@ -56,12 +58,13 @@ struct Layout {
 
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
-TileCfg make_tiles(int nt, int ny, int K) {
+// One wave: as many (strip, chunk, condition) tiles as the GPU holds resident CTAs
+// (slots = SMs x CTAs/SM from the occupancy calculator), each CTA marching a long chunk.
+TileCfg make_tiles(int nt, int ny, int K, int slots) {
   TileCfg t{};
   t.tw = (nt >= 1024) ? 256 : 128;
   t.n_strips = (nt + t.tw - 1) / t.tw;
-  const int target = 4 * 148;
-  int chunks = (target + t.n_strips * K - 1) / (t.n_strips * K);
+  int chunks = slots / (t.n_strips * K);
   if (chunks < 1) chunks = 1;
   int th = (ny + chunks - 1) / chunks;
   if (th < 8) th = 8;
@@ -71,6 +74,8 @@ TileCfg make_tiles(int nt, int ny, int K) {
   t.n_tiles = t.n_strips * t.n_chunks;
   return t;
 }
+
+constexpr int kMaxTilesPerCondition = 148 * 16;
 
 int check_grid(const gmaf_grid* g) {
   if (!g) return GMAF_E_INVALID_ARG;
@@ -89,7 +94,6 @@ int check_grid(const gmaf_grid* g) {
 Layout make_layout(const gmaf_grid* g, int K) {
   Layout L{};
   const size_t nt = (size_t)g->n_theta, ny = (size_t)g->n_y, n = nt * ny;
-  const TileCfg t = make_tiles(g->n_theta, g->n_y, K);
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t at = o; o = align_up(o + bytes); return at; };
   L.off_ct = take(nt * 8); L.off_st = take(nt * 8); L.off_cth = take(nt * 8); L.off_sth = take(nt * 8);
@@ -99,7 +103,7 @@ Layout make_layout(const gmaf_grid* g, int K) {
   L.off_r = take((size_t)K * n * 8); L.off_r2 = take((size_t)K * n * 8);
   L.off_u = take((size_t)K * n * 8); L.off_u2 = take((size_t)K * n * 8);
   L.off_scratch = take((ny + 2) * nt * 8);
-  L.off_part = take((size_t)4 * K * t.n_tiles * 8);
+  L.off_part = take((size_t)4 * K * kMaxTilesPerCondition * 8);
   L.off_wpart = take((size_t)(148 * 8 + K) * 12 * 8);
   L.off_wrench = take((size_t)K * 12 * 8);
   L.off_state = take(sizeof(SolverState));
@@ -141,6 +145,7 @@ struct gmaf_ctx {
   Timing* h_timing = nullptr;
   int quad_ctas = 0;
   int r_parity = 0;   // which ping-pong buffer holds the latest residual
+  bool stream_mode = false;  // GMAF_LAUNCH_MODE=stream: no CUDA graph (for ncu)
 };
 
 namespace {
@@ -258,12 +263,30 @@ gmaf_status run_solve(gmaf_ctx* ctx, double tol, double omega, int precond, int 
   hs->max_iter = max_iter;
   hs->fixed_iters = fixed_iters;
   CU(cudaMemcpyAsync(ctx->d.st_, hs, sizeof(SolverState), cudaMemcpyHostToDevice, ctx->stream));
-  cudaGraphExec_t exec = nullptr;
-  gmaf_status gs = build_graph(ctx, GraphKey{precond, warm ? 1 : 0, fixed_iters > 0 ? 1 : 0}, &exec);
-  if (gs != GMAF_OK) return gs;
-  CU(cudaEventRecord(ctx->ev0, ctx->stream));
-  CU(cudaGraphLaunch(exec, ctx->stream));
-  CU(cudaEventRecord(ctx->ev1, ctx->stream));
+  if (ctx->stream_mode) {
+    // Plain stream launches (profilers cannot replay kernel nodes of conditional graphs):
+    // the host polls the device done-flag every kUnroll iterations.
+    CU(cudaEventRecord(ctx->ev0, ctx->stream));
+    CU(launch_init(ctx->gp, ctx->d, ctx->tiles, ctx->K, precond, warm != 0, 0ull, ctx->stream));
+    for (;;) {
+      CU(cudaMemcpyAsync(hs, ctx->d.st_, sizeof(SolverState), cudaMemcpyDeviceToHost, ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
+      if (hs->done) break;
+      for (int u = 0; u < kUnroll; ++u) {
+        CU(launch_phase_a(ctx->gp, ctx->d, ctx->tiles, ctx->K, precond, u & 1, 0ull, ctx->stream));
+        CU(launch_phase_b(ctx->gp, ctx->d, ctx->tiles, ctx->K, precond, u & 1, 0ull, ctx->stream));
+      }
+    }
+    CU(launch_true_residual(ctx->gp, ctx->d, ctx->tiles, ctx->K, ctx->stream));
+    CU(cudaEventRecord(ctx->ev1, ctx->stream));
+  } else {
+    cudaGraphExec_t exec = nullptr;
+    gmaf_status gs = build_graph(ctx, GraphKey{precond, warm ? 1 : 0, fixed_iters > 0 ? 1 : 0}, &exec);
+    if (gs != GMAF_OK) return gs;
+    CU(cudaEventRecord(ctx->ev0, ctx->stream));
+    CU(cudaGraphLaunch(exec, ctx->stream));
+    CU(cudaEventRecord(ctx->ev1, ctx->stream));
+  }
   CU(cudaMemcpyAsync(hs, ctx->d.st_, sizeof(SolverState), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaMemcpyAsync(ctx->h_cs, ctx->d.cs.alpha, (size_t)7 * ctx->K * 8, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
@@ -329,7 +352,6 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
   ctx->ws = reinterpret_cast<char*>(d_workspace);
   ctx->ws_bytes = ws_bytes;
   ctx->L = L;
-  ctx->tiles = make_tiles(grid->n_theta, grid->n_y, K);
   GridParams& gp = ctx->gp;
   gp.nt = grid->n_theta; gp.ny = grid->n_y; gp.Rk = grid->R_k; gp.Rc = grid->R_c; gp.mu = grid->mu;
   gp.hmin = grid->h_min;
@@ -389,9 +411,22 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
   for (int q = 0; q < KK_COUNT; ++q) ctx->h_timing->t_start[q] = ~0ull;
   if (cudaMemcpyAsync(d.timing, ctx->h_timing, sizeof(Timing), cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess)
     return cleanup_fail(GMAF_E_CUDA);
-  if (configure_pcg_kernels(ctx->tiles, K) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
+  {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      return cleanup_fail(GMAF_E_CUDA);
+    TileCfg probe = make_tiles(grid->n_theta, grid->n_y, K, 1);
+    if (configure_pcg_kernels(probe, K) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
+    const int occ = pcg_ctas_per_sm(probe, K);
+    ctx->tiles = make_tiles(grid->n_theta, grid->n_y, K, sms * (occ > 0 ? occ : 1));
+    if (ctx->tiles.n_tiles > kMaxTilesPerCondition) return cleanup_fail(GMAF_E_INVALID_MESH);
+    if (configure_pcg_kernels(ctx->tiles, K) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
+  }
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
   ctx->quad_ctas = quad_ctas_per_condition(gp, K);
+  const char* lm = std::getenv("GMAF_LAUNCH_MODE");
+  ctx->stream_mode = lm && std::strcmp(lm, "stream") == 0;
   *out = ctx;
   return GMAF_OK;
 }

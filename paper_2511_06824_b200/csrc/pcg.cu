@@ -453,4 +453,13 @@ cudaError_t launch_true_residual(const GridParams& g, const DevPtrs& d, const Ti
   return launch_tiles(k_phase_b<PC_NONE, MODE_TRUERES>, g, d, t, K, 0, 0ull, 0, s);
 }
 
+// Resident CTAs per SM of the dominant iteration kernel (phase B, ASSOR-II).
+int pcg_ctas_per_sm(const TileCfg& t, int K) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_phase_b<PC_ASSOR2, MODE_ITER>, t.tw + 2 * HALO,
+                                                    tile_smem(t, K)) != cudaSuccess)
+    return 1;
+  return n;
+}
+
 }  // namespace gmaf

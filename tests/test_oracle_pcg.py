@@ -222,3 +222,27 @@ def test_omega_sweep_shape(orc, gi):
     wmin = omegas[int(np.argmin(its))]
     assert 1.2 <= wmin <= 1.9, list(zip(omegas, its))
     assert its[8] < its[0]          # omega = 1.72 (nearest grid point to 1.8) vs 0.28
+
+
+# ------------------------------------------------ single-reduction schedule (O7-S3)
+
+def test_single_reduction_schedule_equals_table1(orc, gi):
+    """The one-reduction-per-iteration form of Table 1 (Chronopoulos-Gear alpha
+    recurrence) produces the same iterates: the j-th p agrees with
+    Table 1's to rounding, and it reaches the dense solution."""
+    g = gi.grid(96, 40, "short", tex_n_theta=8, tex_n_y=2, tex_band_rows=10)
+    conds = gi.fd_conditions(gi.condition())
+    AP, AE, AN, S = orc.assemble_joint(g, conds)
+    for j in (1, 3, 10, 40):
+        for cp in ("coupled", "lockstep"):
+            a = orc.pcg_joint(AP, AE, AN, S, tol=0.0, omega=1.6, max_iter=j, coupling=cp)
+            b = orc.pcg_joint(AP, AE, AN, S, tol=0.0, omega=1.6, max_iter=j, coupling=cp, schedule="single")
+            assert np.linalg.norm(a.p - b.p) <= 1e-10 * np.linalg.norm(a.p), (j, cp)
+    a = orc.pcg_joint(AP, AE, AN, S, tol=1e-10, omega=1.6)
+    b = orc.pcg_joint(AP, AE, AN, S, tol=1e-10, omega=1.6, schedule="single")
+    assert b.converged and abs(a.iterations - b.iterations) <= 2
+    x = orc.cholesky_solve(orc.expand_dense(AP[0], AE[0], AN[0]), S[0].ravel())
+    assert np.linalg.norm(b.p[0].ravel() - x) <= 1e-8 * np.linalg.norm(x)
+    for pc in ("jacobi", "none"):
+        c = orc.pcg_joint(AP, AE, AN, S, tol=1e-10, omega=1.6, precond=pc, schedule="single")
+        assert c.converged and np.linalg.norm(c.p - a.p) <= 1e-8 * np.linalg.norm(a.p)

@@ -60,6 +60,11 @@ enum { GMAF_COUPLED = 0,   /* one Krylov process on A_G: global alpha, beta (P:2
 enum { GMAF_FIELD_P = 0, GMAF_FIELD_H = 1, GMAF_FIELD_HDOT = 2, GMAF_FIELD_AP = 3,
        GMAF_FIELD_AE = 4, GMAF_FIELD_AN = 5, GMAF_FIELD_S = 6, GMAF_FIELD_R = 7 };
 enum { GMAF_SHARD_CONDITIONS = 0 };
+/* Iteration schedule: both run the Table-1 method to the same rtol.
+ * SINGLE: one fused kernel and one global (gamma, delta, r.r) reduction per iteration
+ *         (Chronopoulos-Gear alpha recurrence; needs an even n_theta) -- the default;
+ * TABLE1: two fused kernels per iteration with Table 1's two reductions (u.v, then r.r/r.z). */
+enum { GMAF_SCHEDULE_TABLE1 = 0, GMAF_SCHEDULE_SINGLE = 1 };
 
 /* Mesh and texture, shared by all K conditions; copied at create. */
 typedef struct {
@@ -96,6 +101,8 @@ typedef struct {
   int32_t converged;             /* 1 if Eq. 3.9 was met */
   int32_t status;                /* gmaf_status of the solve */
   int32_t precond;
+  int32_t schedule;              /* GMAF_SCHEDULE_* used */
+  int32_t pad;
   double  rel_residual;          /* recursive ||r||/||S_G|| at exit (R-A10) */
   double  true_rel_residual;     /* ||S_G - A_G p_G|| / ||S_G|| at exit */
   double  solve_ms;              /* device time of the solve (CUDA events) */
@@ -165,6 +172,10 @@ gmaf_status gmaf_reset_kernel_times(gmaf_ctx* ctx);
  * SURVEY 8(d)) after a solve's init; used by the benchmark.  Stats as gmaf_solve. */
 gmaf_status gmaf_solve_fixed(gmaf_ctx* ctx, double omega, int32_t precond, int32_t n_iter,
                              gmaf_solve_stats* out);
+
+/* Choose the iteration schedule for subsequent solves (GMAF_SCHEDULE_*).  SINGLE with an
+ * odd n_theta returns INVALID_ARG. */
+gmaf_status gmaf_set_schedule(gmaf_ctx* ctx, int32_t schedule);
 
 const char* gmaf_last_error(const gmaf_ctx* ctx);
 const char* gmaf_version(void);

@@ -49,13 +49,17 @@ class gmaf_dist(C.Structure):
 
 class gmaf_solve_stats(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("status", C.c_int32),
-                ("precond", C.c_int32), ("rel_residual", C.c_double),
+                ("precond", C.c_int32), ("schedule", C.c_int32), ("pad", C.c_int32),
+                ("rel_residual", C.c_double),
                 ("true_rel_residual", C.c_double), ("solve_ms", C.c_double)]
 
 
 class gmaf_kernel_timing(C.Structure):
     _fields_ = [("name", C.c_char * 24), ("launches", C.c_int64), ("total_ms", C.c_double),
                 ("bytes_per_launch", C.c_double)]
+
+
+_SCHED_NAME = {0: "table1", 1: "single"}
 
 
 class GmafError(RuntimeError):
@@ -90,12 +94,13 @@ def lib() -> C.CDLL:
         L.gmaf_field_ptr.argtypes = [P, C.c_int32, C.c_int32, C.POINTER(P)]
         L.gmaf_kernel_times.argtypes = [P, C.POINTER(gmaf_kernel_timing), C.c_int32, C.POINTER(C.c_int32)]
         L.gmaf_reset_kernel_times.argtypes = [P]
+        L.gmaf_set_schedule.argtypes = [P, C.c_int32]
         L.gmaf_last_error.restype = C.c_char_p
         L.gmaf_last_error.argtypes = [P]
         L.gmaf_version.restype = C.c_char_p
         for name in ("gmaf_create", "gmaf_destroy", "gmaf_thickness", "gmaf_assemble", "gmaf_solve",
                      "gmaf_solve_fixed", "gmaf_integrate", "gmaf_get", "gmaf_field_ptr",
-                     "gmaf_kernel_times", "gmaf_reset_kernel_times"):
+                     "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_set_schedule"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -103,7 +108,9 @@ def lib() -> C.CDLL:
 
 ABI_SYMBOLS = ("gmaf_workspace_bytes", "gmaf_create", "gmaf_destroy", "gmaf_thickness", "gmaf_assemble",
                "gmaf_solve", "gmaf_solve_fixed", "gmaf_integrate", "gmaf_get", "gmaf_field_ptr",
-               "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_last_error", "gmaf_version")
+               "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_set_schedule", "gmaf_last_error",
+               "gmaf_version")
+SCHEDULE = {"table1": 0, "single": 1}
 
 
 def make_grid(g: dict) -> gmaf_grid:
@@ -170,6 +177,7 @@ def gmaf_destroy(ctx) -> None:
 
 @dataclass
 class SolveStats:
+    schedule: str
     iterations: int
     converged: bool
     status: int
@@ -228,15 +236,19 @@ class JointSolver:
                                   warm, self.K)
         if code != 0 and raise_on_error:
             _check(self.ctx, code)
-        return SolveStats(st.iterations, bool(st.converged), st.status, st.rel_residual,
-                          st.true_rel_residual, st.solve_ms, cr)
+        return SolveStats(_SCHED_NAME[st.schedule], st.iterations, bool(st.converged), st.status,
+                          st.rel_residual, st.true_rel_residual, st.solve_ms, cr)
 
     def solve_fixed(self, n_iter: int, omega=1.6, precond="assor2") -> SolveStats:
         st = gmaf_solve_stats()
         _check(self.ctx, lib().gmaf_solve_fixed(self.ctx, float(omega), PRECOND[precond], int(n_iter),
                                                  C.byref(st)))
-        return SolveStats(st.iterations, bool(st.converged), st.status, st.rel_residual,
-                          st.true_rel_residual, st.solve_ms, np.zeros(self.K))
+        return SolveStats(_SCHED_NAME[st.schedule], st.iterations, bool(st.converged), st.status,
+                          st.rel_residual, st.true_rel_residual, st.solve_ms, np.zeros(self.K))
+
+    def set_schedule(self, schedule: str) -> None:
+        """'single' (one kernel + one reduction per iteration, default) or 'table1'."""
+        _check(self.ctx, lib().gmaf_set_schedule(self.ctx, SCHEDULE[schedule]))
 
     def integrate(self) -> np.ndarray:
         return gmaf_integrate(self.ctx, self.K)

@@ -29,6 +29,7 @@ int quad_ctas_per_condition(const GridParams& g, int K);
 cudaError_t configure_pcg_kernels(const TileCfg& t, int K);
 int pcg_ctas_per_sm(const TileCfg& t, int K);
 }
+static_assert(gmaf::SR_HALO_COLS == 6, "sr.cu halo");
 
 using namespace gmaf;
 
@@ -41,8 +42,9 @@ constexpr size_t kAlign = 256;
 enum State { ST_CREATED = 0, ST_THICK = 1, ST_ASSEMBLED = 2, ST_SOLVED = 3 };
 
 struct GraphKey {
-  int precond, warm, fixed;
+  int schedule, precond, warm, fixed;
   bool operator<(const GraphKey& o) const {
+    if (schedule != o.schedule) return schedule < o.schedule;
     if (precond != o.precond) return precond < o.precond;
     if (warm != o.warm) return warm < o.warm;
     return fixed < o.fixed;
@@ -52,7 +54,7 @@ struct GraphKey {
 struct Layout {
   size_t off_ct, off_st, off_cth, off_sth, off_cp, off_AP, off_AE, off_AN, off_S, off_p, off_r, off_r2,
       off_u, off_u2,
-      off_scratch, off_part, off_wpart, off_wrench, off_state, off_cs, off_counters, off_timing,
+      off_scratch, off_constrows, off_part, off_wpart, off_wrench, off_state, off_cs, off_counters, off_timing,
       off_guard, off_matrep, total;
 };
 
@@ -76,6 +78,7 @@ TileCfg make_tiles(int nt, int ny, int K, int slots) {
 }
 
 constexpr int kMaxTilesPerCondition = 148 * 16;
+constexpr int kConstRowLen = 1024;   // >= the widest TMA row segment (tw + 2*halo)
 
 int check_grid(const gmaf_grid* g) {
   if (!g) return GMAF_E_INVALID_ARG;
@@ -103,6 +106,7 @@ Layout make_layout(const gmaf_grid* g, int K) {
   L.off_r = take((size_t)K * n * 8); L.off_r2 = take((size_t)K * n * 8);
   L.off_u = take((size_t)K * n * 8); L.off_u2 = take((size_t)K * n * 8);
   L.off_scratch = take((ny + 2) * nt * 8);
+  L.off_constrows = take((size_t)2 * kConstRowLen * 8);   // a zero row and a one row (TMA sources)
   L.off_part = take((size_t)4 * K * kMaxTilesPerCondition * 8);
   L.off_wpart = take((size_t)(148 * 8 + K) * 12 * 8);
   L.off_wrench = take((size_t)K * 12 * 8);
@@ -128,7 +132,9 @@ struct gmaf_ctx {
   char* ws = nullptr;
   size_t ws_bytes = 0;
   Layout L{};
-  TileCfg tiles{};
+  TileCfg tiles{};      // two-phase (Table-1 schedule) kernels
+  TileCfg tiles_sr{};   // single-pass kernel
+  int schedule = GMAF_SCHEDULE_SINGLE;
   DevPtrs d{};
   int M = 0;
   std::vector<int32_t> mat_of, mat_rep;
@@ -199,6 +205,40 @@ bool same_matrix(const gmaf_condition& a, const gmaf_condition& b) {
   return std::memcmp(a.e, b.e, sizeof(a.e)) == 0 && std::memcmp(&a.L_F, &b.L_F, sizeof(double)) == 0;
 }
 
+// The three pieces of a solve, enqueued on stream `s` (captured into a graph or launched
+// directly).  h = graph conditional handle (0 outside a graph).
+cudaError_t enqueue_init(gmaf_ctx* ctx, const GraphKey& key, unsigned long long h, cudaStream_t s) {
+  if (key.schedule == GMAF_SCHEDULE_TABLE1)
+    return launch_init(ctx->gp, ctx->d, ctx->tiles, ctx->K, key.precond, key.warm != 0, h, s);
+  if (key.warm) {   // r0 = S - A p0 into r[1], then the single-pass init reads it
+    cudaError_t e = launch_residual_init(ctx->gp, ctx->d, ctx->tiles, ctx->K, 1, s);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_sr_init(ctx->gp, ctx->d, ctx->tiles_sr, ctx->K, key.precond, key.warm != 0, h, s);
+}
+
+cudaError_t enqueue_iterations(gmaf_ctx* ctx, const GraphKey& key, unsigned long long h, cudaStream_t s) {
+  cudaError_t e = cudaSuccess;
+  for (int u = 0; u < kUnroll && e == cudaSuccess; ++u) {
+    // iteration j = kUnroll*m + u: ping-pong parity u % 2 (kUnroll is even)
+    if (key.schedule == GMAF_SCHEDULE_TABLE1) {
+      e = launch_phase_a(ctx->gp, ctx->d, ctx->tiles, ctx->K, key.precond, u & 1, h, s);
+      if (e == cudaSuccess) e = launch_phase_b(ctx->gp, ctx->d, ctx->tiles, ctx->K, key.precond, u & 1, h, s);
+    } else {
+      e = launch_sr_iter(ctx->gp, ctx->d, ctx->tiles_sr, ctx->K, key.precond, u & 1, h, s);
+    }
+  }
+  return e;
+}
+
+cudaError_t enqueue_final(gmaf_ctx* ctx, const GraphKey& key, cudaStream_t s) {
+  if (key.schedule == GMAF_SCHEDULE_SINGLE) {
+    cudaError_t e = launch_sr_fixup(ctx->gp, ctx->d, ctx->K, s);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_true_residual(ctx->gp, ctx->d, ctx->tiles, ctx->K, s);   // ||S - A p|| at exit
+}
+
 gmaf_status build_graph(gmaf_ctx* ctx, const GraphKey& key, cudaGraphExec_t* out) {
   auto it = ctx->graphs.find(key);
   if (it != ctx->graphs.end()) { *out = it->second.second; return GMAF_OK; }
@@ -207,42 +247,39 @@ gmaf_status build_graph(gmaf_ctx* ctx, const GraphKey& key, cudaGraphExec_t* out
   cudaGraphConditionalHandle handle;
   CU(cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
   cudaStream_t cs = ctx->cap_stream;
-  // init: r0 = S - A p0, z0, d0, ||S_G|| (Table 1 steps 1-2)
   CU(cudaStreamBeginCaptureToGraph(cs, graph, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  cudaError_t le = launch_init(ctx->gp, ctx->d, ctx->tiles, ctx->K, key.precond, key.warm != 0,
-                               (unsigned long long)handle, cs);
+  cudaError_t le = enqueue_init(ctx, key, (unsigned long long)handle, cs);
   cudaGraph_t g2 = nullptr;
   cudaError_t ee = cudaStreamEndCapture(cs, &g2);
   CU(le);
   CU(ee);
+  // the init chain's leaf node
   size_t nn = 0;
   CU(cudaGraphGetNodes(graph, nullptr, &nn));
   std::vector<cudaGraphNode_t> nodes(nn);
   CU(cudaGraphGetNodes(graph, nodes.data(), &nn));
-  if (nn != 1) return fail(ctx, GMAF_E_CUDA, "graph build: expected 1 init node, got %zu", nn);
+  cudaGraphNode_t leaf = nullptr;
+  for (size_t q = 0; q < nn; ++q) {
+    size_t nd = 0;
+    CU(cudaGraphNodeGetDependentNodes(nodes[q], nullptr, &nd));
+    if (nd == 0) leaf = nodes[q];
+  }
+  if (!leaf) return fail(ctx, GMAF_E_CUDA, "graph build: no init leaf");
   cudaGraphNodeParams cp{};
   cp.type = cudaGraphNodeTypeConditional;
   cp.conditional.handle = handle;
   cp.conditional.type = cudaGraphCondTypeWhile;
   cp.conditional.size = 1;
   cudaGraphNode_t cond_node;
-  CU(cudaGraphAddNode(&cond_node, graph, nodes.data(), 1, &cp));
+  CU(cudaGraphAddNode(&cond_node, graph, &leaf, 1, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   CU(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  cudaError_t lb = cudaSuccess;
-  for (int u = 0; u < kUnroll && lb == cudaSuccess; ++u) {
-    // iteration j = 4m + u inside the body: parity u % 2 (kUnroll is even)
-    lb = launch_phase_a(ctx->gp, ctx->d, ctx->tiles, ctx->K, key.precond, u & 1, (unsigned long long)handle, cs);
-    if (lb == cudaSuccess)
-      lb = launch_phase_b(ctx->gp, ctx->d, ctx->tiles, ctx->K, key.precond, u & 1, (unsigned long long)handle,
-                          cs);
-  }
+  cudaError_t lb = enqueue_iterations(ctx, key, (unsigned long long)handle, cs);
   ee = cudaStreamEndCapture(cs, &g2);
   CU(lb);
   CU(ee);
-  // true residual ||S - A p|| after the loop
   CU(cudaStreamBeginCaptureToGraph(cs, graph, &cond_node, nullptr, 1, cudaStreamCaptureModeRelaxed));
-  le = launch_true_residual(ctx->gp, ctx->d, ctx->tiles, ctx->K, cs);
+  le = enqueue_final(ctx, key, cs);
   ee = cudaStreamEndCapture(cs, &g2);
   CU(le);
   CU(ee);
@@ -262,26 +299,24 @@ gmaf_status run_solve(gmaf_ctx* ctx, double tol, double omega, int precond, int 
   hs->coupling = coupling;
   hs->max_iter = max_iter;
   hs->fixed_iters = fixed_iters;
+  const GraphKey key{ctx->schedule, precond, warm ? 1 : 0, fixed_iters > 0 ? 1 : 0};
   CU(cudaMemcpyAsync(ctx->d.st_, hs, sizeof(SolverState), cudaMemcpyHostToDevice, ctx->stream));
   if (ctx->stream_mode) {
     // Plain stream launches (profilers cannot replay kernel nodes of conditional graphs):
     // the host polls the device done-flag every kUnroll iterations.
     CU(cudaEventRecord(ctx->ev0, ctx->stream));
-    CU(launch_init(ctx->gp, ctx->d, ctx->tiles, ctx->K, precond, warm != 0, 0ull, ctx->stream));
+    CU(enqueue_init(ctx, key, 0ull, ctx->stream));
     for (;;) {
       CU(cudaMemcpyAsync(hs, ctx->d.st_, sizeof(SolverState), cudaMemcpyDeviceToHost, ctx->stream));
       CU(cudaStreamSynchronize(ctx->stream));
       if (hs->done) break;
-      for (int u = 0; u < kUnroll; ++u) {
-        CU(launch_phase_a(ctx->gp, ctx->d, ctx->tiles, ctx->K, precond, u & 1, 0ull, ctx->stream));
-        CU(launch_phase_b(ctx->gp, ctx->d, ctx->tiles, ctx->K, precond, u & 1, 0ull, ctx->stream));
-      }
+      CU(enqueue_iterations(ctx, key, 0ull, ctx->stream));
     }
-    CU(launch_true_residual(ctx->gp, ctx->d, ctx->tiles, ctx->K, ctx->stream));
+    CU(enqueue_final(ctx, key, ctx->stream));
     CU(cudaEventRecord(ctx->ev1, ctx->stream));
   } else {
     cudaGraphExec_t exec = nullptr;
-    gmaf_status gs = build_graph(ctx, GraphKey{precond, warm ? 1 : 0, fixed_iters > 0 ? 1 : 0}, &exec);
+    gmaf_status gs = build_graph(ctx, key, &exec);
     if (gs != GMAF_OK) return gs;
     CU(cudaEventRecord(ctx->ev0, ctx->stream));
     CU(cudaGraphLaunch(exec, ctx->stream));
@@ -307,6 +342,7 @@ gmaf_status run_solve(gmaf_ctx* ctx, double tol, double omega, int precond, int 
     out->converged = hs->converged;
     out->status = hs->status;
     out->precond = precond;
+    out->schedule = ctx->schedule;
     out->rel_residual = hs->rel;
     out->true_rel_residual = hs->true_rel;
     out->solve_ms = ms;
@@ -370,6 +406,8 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
   d.r[0] = at<double>(ctx, L.off_r); d.r[1] = at<double>(ctx, L.off_r2);
   d.u[0] = at<double>(ctx, L.off_u); d.u[1] = at<double>(ctx, L.off_u2);
   d.scratch = at<double>(ctx, L.off_scratch);
+  d.zero_row = at<double>(ctx, L.off_constrows);
+  d.one_row = d.zero_row + kConstRowLen;
   d.partials = at<double>(ctx, L.off_part); d.wrench_part = at<double>(ctx, L.off_wpart);
   d.wrench = at<double>(ctx, L.off_wrench); d.st_ = at<SolverState>(ctx, L.off_state);
   double* cs = at<double>(ctx, L.off_cs);
@@ -393,6 +431,7 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
   // cos/sin tables with the host libm (shared by nobody: the oracle computes its own)
   const int nt = grid->n_theta;
   std::vector<double> tab((size_t)4 * nt);
+  std::vector<double> ones(kConstRowLen, 1.0);
   for (int i = 0; i < nt; ++i) {
     const double th = (double)i * gp.dtheta;
     const double thc = ((double)i + 0.5) * gp.dtheta;
@@ -405,7 +444,9 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
       cudaMemcpyAsync((void*)d.sth, tab.data() + 3 * nt, nt * 8, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
       cudaMemsetAsync(d.counters, 0, 16 * sizeof(unsigned int), ctx->stream) != cudaSuccess ||
       cudaMemsetAsync(d.st_, 0, sizeof(SolverState), ctx->stream) != cudaSuccess ||
-      cudaMemsetAsync(d.p, 0, (size_t)K * gp.nt * gp.ny * 8, ctx->stream) != cudaSuccess)
+      cudaMemsetAsync(d.p, 0, (size_t)K * gp.nt * gp.ny * 8, ctx->stream) != cudaSuccess ||
+      cudaMemsetAsync((void*)d.zero_row, 0, kConstRowLen * 8, ctx->stream) != cudaSuccess ||
+      cudaMemcpyAsync((void*)d.one_row, ones.data(), kConstRowLen * 8, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess)
     return cleanup_fail(GMAF_E_CUDA);
   std::memset(ctx->h_timing, 0, sizeof(Timing));
   for (int q = 0; q < KK_COUNT; ++q) ctx->h_timing->t_start[q] = ~0ull;
@@ -422,6 +463,16 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
     ctx->tiles = make_tiles(grid->n_theta, grid->n_y, K, sms * (occ > 0 ? occ : 1));
     if (ctx->tiles.n_tiles > kMaxTilesPerCondition) return cleanup_fail(GMAF_E_INVALID_MESH);
     if (configure_pcg_kernels(ctx->tiles, K) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
+    // single-pass kernel: its own tiles (wider halo, TMA ring) and occupancy
+    TileCfg sprobe = make_tiles(grid->n_theta, grid->n_y, K, 1);
+    if (configure_sr_kernels(sprobe) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
+    const int socc = sr_ctas_per_sm(sprobe);
+    ctx->tiles_sr = make_tiles(grid->n_theta, grid->n_y, K, sms * (socc > 0 ? socc : 1));
+    if (ctx->tiles_sr.n_tiles > kMaxTilesPerCondition) return cleanup_fail(GMAF_E_INVALID_MESH);
+    // the single-pass kernel streams rows with 16-byte TMA copies: needs an even n_theta
+    ctx->schedule = (grid->n_theta % 2 == 0) ? GMAF_SCHEDULE_SINGLE : GMAF_SCHEDULE_TABLE1;
+    const char* sch = std::getenv("GMAF_SCHEDULE");
+    if (sch && std::strcmp(sch, "table1") == 0) ctx->schedule = GMAF_SCHEDULE_TABLE1;
   }
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
   ctx->quad_ctas = quad_ctas_per_condition(gp, K);
@@ -567,18 +618,21 @@ gmaf_status gmaf_kernel_times(gmaf_ctx* ctx, gmaf_kernel_timing* out, int32_t n,
   CU(cudaMemcpyAsync(ctx->h_timing, ctx->d.timing, sizeof(Timing), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   static const char* names[KK_COUNT] = {"thickness_guard", "assemble", "pcg_init", "pcg_phase_a",
-                                        "pcg_phase_b", "true_residual", "quadrature"};
+                                        "pcg_phase_b", "true_residual", "quadrature", "sr_init", "sr_iter"};
   const double n_nodes = (double)ctx->grid.n_theta * ctx->grid.n_y * ctx->K;
   const double nM = (double)ctx->grid.n_theta * ctx->grid.n_y * (ctx->M > 0 ? ctx->M : ctx->K);
-  // algorithmic DRAM bytes per launch
+  // algorithmic DRAM bytes per launch: 8 B per node per field touched;
+  // the coefficient bands count once per DISTINCT matrix (M of them).
   const double bytes[KK_COUNT] = {
-      0.0,                                  // guard: pure compute, no field traffic
+      0.0,                                  // guard: pure compute
       8.0 * (n_nodes + 3.0 * nM),           // assemble: write S (K) + 3 bands (M)
-      8.0 * (3.0 * n_nodes + 3.0 * n_nodes),// init: read S (+p), 3 bands; write r, p
-      8.0 * (3.0 * n_nodes + 3.0 * n_nodes),// A: read r, u, write u; 3 bands per condition
-      8.0 * (5.0 * n_nodes + 3.0 * n_nodes),// B: read p, u, r; write p, r; 3 bands
-      8.0 * (2.0 * n_nodes + 3.0 * n_nodes),// true residual: read S, p; 3 bands
-      8.0 * n_nodes};                       // quadrature: read p
+      8.0 * (3.0 * n_nodes + 3.0 * nM),     // init: read S, write r, p; 3 bands
+      8.0 * (3.0 * n_nodes + 3.0 * nM),     // A: read r, u_old, write u; 3 bands
+      8.0 * (5.0 * n_nodes + 3.0 * nM),     // B: read p, u, r; write p, r; 3 bands
+      8.0 * (2.0 * n_nodes + 3.0 * nM),     // true residual: read S, p; 3 bands
+      8.0 * n_nodes,                        // quadrature: read p
+      8.0 * (2.0 * n_nodes + 3.0 * nM),     // sr_init: read S, write r (x zeroed: +1)
+      8.0 * (5.0 * n_nodes + 3.0 * nM)};    // sr_iter: r RW, pd RW, x RW every other; 3 bands
   int c = 0;
   for (int q = 0; q < KK_COUNT && c < n; ++q, ++c) {
     std::memset(&out[c], 0, sizeof(gmaf_kernel_timing));
@@ -598,6 +652,13 @@ gmaf_status gmaf_reset_kernel_times(gmaf_ctx* ctx) {
   CU(cudaMemcpyAsync(ctx->d.timing, ctx->h_timing, sizeof(Timing), cudaMemcpyHostToDevice, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   return GMAF_OK;
+}
+
+gmaf_status gmaf_set_schedule(gmaf_ctx* ctx, int32_t schedule) {
+  if (!ctx) return GMAF_E_INVALID_ARG;
+  if (schedule == GMAF_SCHEDULE_TABLE1) { ctx->schedule = schedule; return GMAF_OK; }
+  if (schedule == GMAF_SCHEDULE_SINGLE && ctx->grid.n_theta % 2 == 0) { ctx->schedule = schedule; return GMAF_OK; }
+  return fail(ctx, GMAF_E_INVALID_ARG, "set_schedule: %d not available (n_theta %d)", schedule, ctx->grid.n_theta);
 }
 
 const char* gmaf_last_error(const gmaf_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }

@@ -30,7 +30,7 @@ struct GridParams {
 
 // Kernel kinds for the in-kernel %globaltimer accounting.
 enum KernelKind { KK_THICK = 0, KK_ASSEMBLE, KK_INIT, KK_PHASE_A, KK_PHASE_B, KK_TRUERES, KK_QUAD,
-                  KK_COUNT };
+                  KK_SR_INIT, KK_SR_ITER, KK_COUNT };
 
 struct Timing {
   unsigned long long t_start[KK_COUNT];   // min start of the current launch (ULLONG_MAX = idle)
@@ -72,6 +72,7 @@ struct DevPtrs {
   double* S; double* p;                    // [K][n]
   double* r[2]; double* u[2];              // [K][n] ping-pong (halo reads never race with writes)
   double* scratch;                         // [(n_y+2) n_theta] field readback
+  const double* zero_row; const double* one_row;  // constant rows: TMA sources for out-of-range rows
   double* partials;                        // [4][K][n_cta_max]
   double* wrench_part;                     // [K][n_cta_q][12]
   double* wrench;                          // [K][12]
@@ -111,5 +112,18 @@ cudaError_t launch_phase_b(const GridParams& g, const DevPtrs& d, const TileCfg&
                            int precond, int parity, unsigned long long cond_handle, cudaStream_t s);
 cudaError_t launch_true_residual(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K,
                                  cudaStream_t s);
+// warm-start pre-pass: r0 = S - A p0 into r[out_parity] (no preconditioner, no graph condition)
+cudaError_t launch_residual_init(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int out_parity,
+                                 cudaStream_t s);
+
+// ---- launchers (sr.cu): single-pass schedule, one kernel + one reduction per iteration ----
+constexpr int SR_HALO_COLS = 6;
+cudaError_t launch_sr_init(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,
+                           bool warm, unsigned long long cond_handle, cudaStream_t s);
+cudaError_t launch_sr_iter(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,
+                           int parity, unsigned long long cond_handle, cudaStream_t s);
+cudaError_t launch_sr_fixup(const GridParams& g, const DevPtrs& d, int K, cudaStream_t s);
+cudaError_t configure_sr_kernels(const TileCfg& t);
+int sr_ctas_per_sm(const TileCfg& t);
 
 }  // namespace gmaf

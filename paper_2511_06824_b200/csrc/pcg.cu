@@ -221,7 +221,7 @@ k_phase_b(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long l
   const double* __restrict__ AN = d.AN + (long long)m * n;
   // ITER: r -= alpha A u.   INIT/TRUERES: r := S - A p  (u := p, alpha := 1).
   const double* __restrict__ rin = ITER ? d.r[parity] + (long long)c.k * n : d.S + (long long)c.k * n;
-  double* __restrict__ rout = (ITER ? d.r[1 - parity] : d.r[0]) + (long long)c.k * n;
+  double* __restrict__ rout = (ITER ? d.r[1 - parity] : d.r[parity]) + (long long)c.k * n;
   const double* __restrict__ uin = ITER ? d.u[parity] + (long long)c.k * n : d.p + (long long)c.k * n;
   double* __restrict__ p = d.p + (long long)c.k * n;
   const double alpha = ITER ? d.cs.alpha[c.k] : 1.0;
@@ -446,6 +446,11 @@ cudaError_t launch_phase_b(const GridParams& g, const DevPtrs& d, const TileCfg&
   if (precond == PC_ASSOR2) return launch_tiles(k_phase_b<PC_ASSOR2, MODE_ITER>, g, d, t, K, parity, h, use, s);
   if (precond == PC_JACOBI) return launch_tiles(k_phase_b<PC_JACOBI, MODE_ITER>, g, d, t, K, parity, h, use, s);
   return launch_tiles(k_phase_b<PC_NONE, MODE_ITER>, g, d, t, K, parity, h, use, s);
+}
+
+cudaError_t launch_residual_init(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int out_parity,
+                                 cudaStream_t s) {
+  return launch_tiles(k_phase_b<PC_NONE, MODE_INIT_WARM>, g, d, t, K, out_parity, 0ull, 0, s);
 }
 
 cudaError_t launch_true_residual(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K,

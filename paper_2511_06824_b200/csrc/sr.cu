@@ -1,0 +1,605 @@
+// sr.cu -- single-pass PCG-ASSOR-II iteration on sm_100a: ONE kernel and ONE global
+// reduction per iteration (schedule "SINGLE").
+//
+// The method is Table 1 (sign of r0 fixed) with the ASSOR-II two-step
+// preconditioner (Eqs. 3.5-3.6) on the joint system (Eq. 3.7) and the synchronized
+// global test (Eq. 3.9).  Its scalars come from Chronopoulos & Gear's single-reduction
+// recurrence (oracle orc_pcg_joint_sr):
+//
+//   pd_i    = z_i + beta_i pd_{i-1}            (Table 1 step 9)
+//   s_i     = A pd_i                            (step 3, recomputed, not stored)
+//   x      += alpha_i pd_i                      (step 4, applied two iterations at a time)
+//   r_{i+1} = r_i - alpha_i s_i                 (step 5)
+//   z_{i+1} = M^-1 r_{i+1}, w = A z_{i+1}       (step 7, recomputed from r, not stored)
+//   gamma = r.z, delta = z.w, r.r  -> ONE fixed-order reduction -> test (step 6),
+//   beta = gamma'/gamma, alpha = gamma'/(delta' - beta gamma'/alpha)   (step 8)
+//
+// HBM traffic per DOF and iteration: r (read+write), pd (read+write), x (read+write every
+// other iteration) = 40 B, plus the 3 coefficient bands of the DISTINCT matrices (shared
+// through L2 by the conditions with equal e).
+//
+// Tiling.  A CTA owns TW output columns (+ HALO = 6 on each side: the dependency radius
+// of z_{i+1} and A z_{i+1} on r_i including the ASSOR seam) of one condition, one thread
+// per column PAIR, and marches over a chunk of rows.  Input rows are streamed by the TMA
+// engine (cp.async.bulk) into a 4-stage shared ring signalled by mbarriers (3 rows in
+// flight).  Derived rows (w, v1, pd, w2, v2, z2) live in 2-slot shared rings for the
+// theta-neighbour reads; coefficient rows in an 8-slot ring; own-column history in
+// registers.  The row loop is unrolled by 8 so every ring slot is a compile-time index.
+// Two barriers per row.  Stage lags (rows behind the load row jl):
+//   A(0) load, D^-1, w      B(0) v1 = (I - wD^-1L) w        C(1) z, pd
+//   D(2) s = A pd, r, x, w2 E(2) v2                         F(3) z2, gamma
+//   G(4) A z2, delta
+#include <cstdint>
+#include "device_common.cuh"
+#include "gmaf_internal.cuh"
+
+namespace gmaf {
+
+constexpr int SR_HALO = 6;      // theta halo (columns) on each side
+constexpr int SR_YLO = 4;       // rows loaded below the chunk
+constexpr int SR_YHI = 4;       // rows loaded above the chunk
+constexpr int SR_LAG = 4;       // the delta stage trails the load by 4 rows
+constexpr int SR_STAGES = 4;    // TMA ring depth
+constexpr int SR_NARR = 6;      // streamed arrays per stage
+constexpr int SR_UNROLL = 8;    // row-loop unroll = coefficient-ring period
+enum { SA_R = 0, SA_PD = 1, SA_X = 2, SA_AP = 3, SA_AE = 4, SA_AN = 5 };
+// row lag of each streamed array in the stage of step jl: pd_{i-1} is consumed at jl-1,
+// x (or S in a warm init) at jl-2; the others at jl.
+__host__ __device__ constexpr int arr_lag(int a) { return a == SA_PD ? 1 : (a == SA_X ? 2 : 0); }
+
+enum { SR_ITER = 0, SR_INIT_COLD = 1, SR_INIT_WARM = 2 };
+enum { SPC_NONE = 0, SPC_JACOBI = 1, SPC_ASSOR2 = 2 };
+
+// ------------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+// named barrier 1 over the compute warps only (the producer warp never joins it)
+__device__ __forceinline__ void compute_bar(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+// 1/a to full double precision without the IEEE-division slow path: rcp.approx (MUFU)
+// + two Newton steps (the solve does not need a correctly rounded D^-1).
+__device__ __forceinline__ double fast_rcp(double a) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+  double e = fma(-a, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-a, r, 1.0);
+  return fma(r, e, r);
+}
+
+struct D2 { double l, r; };
+__device__ __forceinline__ D2 ld2(const double* base, int t) {
+  const double2 v = reinterpret_cast<const double2*>(base)[t];
+  return {v.x, v.y};
+}
+__device__ __forceinline__ void st2(double* base, int t, D2 v) {
+  reinterpret_cast<double2*>(base)[t] = make_double2(v.l, v.r);
+}
+
+__host__ __device__ inline size_t sr_smem_bytes(int nl) {
+  // stages + AE ring (8) + 6 derived rings (2 each) + full/empty mbarriers
+  return (size_t)(SR_STAGES * SR_NARR + SR_UNROLL + 12) * nl * sizeof(double) + 2 * SR_STAGES * sizeof(uint64_t) + 64;
+}
+
+// Per-column flags of the ASSOR split on the periodic ring (DESIGN.md R-A12).
+struct ColFlags { bool hasW, w0, end, out; };
+
+template <int PC, int MODE>
+__global__ void __launch_bounds__(192, 2)
+k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, int odd_iter, unsigned long long hcond,
+     int use_cond) {
+  extern __shared__ __align__(128) double smem_raw[];
+  constexpr bool ITER = (MODE == SR_ITER);
+  constexpr bool INIT = !ITER;
+  SolverState* st = d.st_;
+  if (ITER && st->done) return;
+  timing_begin(d.timing, ITER ? KK_SR_ITER : KK_SR_INIT);
+
+  // warps 0 .. NCW-1 compute (one thread per column pair); the last warp streams rows (TMA)
+  const int NTC = t.tw / 2 + SR_HALO;     // column pairs = compute lanes doing work
+  const int NCT = (NTC + 31) & ~31;       // compute threads (whole warps; idle lanes duplicate the last pair)
+  const int NL = 2 * NTC;                 // loaded columns = tw + 2*HALO
+  const int tid = threadIdx.x;
+  const bool is_producer = tid >= NCT;
+  const int tl = min(tid, NTC - 1);       // column-pair index (idle lanes alias the last pair)
+  const bool active = tid < NTC;
+  const int k = blockIdx.x % K;
+  const int tile = blockIdx.x / K;
+  const int strip = tile % t.n_strips, chunk = tile / t.n_strips;
+  const int i0 = strip * t.tw;
+  const int j0 = chunk * t.th, j1 = min(j0 + t.th, g.ny);
+  const int nt = g.nt, ny = g.ny;
+  const int cl = 2 * tl, cr = 2 * tl + 1;           // local columns of this thread
+  int gl = (i0 - SR_HALO + cl) % nt;
+  if (gl < 0) gl += nt;
+  const int gr = (gl + 1 == nt) ? 0 : gl + 1;
+  ColFlags fl, fr;
+  fl.hasW = gl >= 1; fl.w0 = gl == 0; fl.end = gl == nt - 1;
+  fr.hasW = gr >= 1; fr.w0 = gr == 0; fr.end = gr == nt - 1;
+  fl.out = active && (cl >= SR_HALO) && (cl < SR_HALO + t.tw) && (i0 + cl - SR_HALO < nt);
+  fr.out = active && (cr >= SR_HALO) && (cr < SR_HALO + t.tw) && (i0 + cr - SR_HALO < nt);
+  const int im = max(cl - 1, 0);           // scalar index of the left neighbour of cl
+  const int ip = min(cr + 1, NL - 1);      // scalar index of the right neighbour of cr
+
+  double* stage = smem_raw;                                  // [STAGES][NARR][NL]
+  double* ringAE = stage + SR_STAGES * SR_NARR * NL;         // [8][NL]
+  double* ringW = ringAE + SR_UNROLL * NL;                   // [2][NL] each
+  double* ringV = ringW + 2 * NL;
+  double* ringP = ringV + 2 * NL;
+  double* ringW2 = ringP + 2 * NL;
+  double* ringV2 = ringW2 + 2 * NL;
+  double* ringU2 = ringV2 + 2 * NL;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ringU2 + 2 * NL);
+  uint64_t* empty = full + SR_STAGES;
+
+  const long long n = (long long)nt * ny;
+  const int m = d.cp[k].mat;
+  // ITER: r_i = R[parity], pd_{i-1} = PD[1-parity]; writes R[1-parity], PD[parity].
+  // INIT: r_0 = S (cold) or R[1] (warm: = S - A x0 from the residual pre-pass); writes R[0].
+  const double* rin = ITER ? d.r[parity] + (long long)k * n
+                           : (MODE == SR_INIT_COLD ? d.S + (long long)k * n : d.r[1] + (long long)k * n);
+  double* rout = (ITER ? d.r[1 - parity] : d.r[0]) + (long long)k * n;
+  double* pdout = d.u[parity] + (long long)k * n;
+  double* x = d.p + (long long)k * n;
+
+  const bool first = INIT || (st->iter == 0);
+  const bool xupd = ITER && (odd_iter != 0);            // x += a_{i-1} pd_{i-1} + a_i pd_i
+  const double alpha = ITER ? d.cs.alpha[k] : 0.0;
+  const double alpha_prev = ITER ? d.cs.uvk[k] : 0.0;   // uvk holds alpha_{i-1} here
+  const double beta = first ? 0.0 : d.cs.beta[k];
+  const double omega = st->omega;
+  const double c2 = (2.0 - omega) * omega;
+  const double romega = 1.0 / omega;
+  const bool use_pd = ITER && !first;
+  const bool use_x = xupd || (MODE == SR_INIT_WARM);   // a warm init streams S in the x slot
+
+  const int jbase = j0 - SR_YLO;
+  // steps jl = jbase .. jbase + nsteps - 1; the real ones end at j1 + LAG - 1, the rest are
+  // padding to a whole number of unrolled blocks (all their rows read as zero rows)
+  const int nsteps = ((j1 + SR_LAG - jbase) + SR_UNROLL - 1) & ~(SR_UNROLL - 1);
+
+  if (tid == 0) {
+    for (int s = 0; s < SR_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NCT / 32); }
+    mbar_fence_init();
+  }
+  for (int q = tid; q < (SR_UNROLL + 12) * NL; q += blockDim.x) ringAE[q] = 0.0;
+  __syncthreads();
+
+  double acc_rr = 0, acc_g = 0, acc_d = 0, acc_s = 0;
+  if (is_producer) {
+    // ------------------------------------------------------------- TMA producer warp
+    const int lane = tid - NCT;
+    const double* src[SR_NARR] = {rin, d.u[1 - parity] + (long long)k * n,
+                                  (MODE == SR_INIT_WARM) ? d.S + (long long)k * n : x,
+                                  d.AP + (long long)m * n, d.AE + (long long)m * n, d.AN + (long long)m * n};
+    const bool used = lane < SR_NARR && (lane != SA_PD || use_pd) && (lane != SA_X || use_x);
+    const int jwin_hi = min(j1 + SR_YHI, ny);
+    int g0 = (i0 - SR_HALO) % nt;
+    if (g0 < 0) g0 += nt;
+    uint32_t bytes = 0;
+    for (int a = 0; a < SR_NARR; ++a)
+      if (a < 3 ? (a == SA_R || (a == SA_PD && use_pd) || (a == SA_X && use_x)) : true) bytes += (uint32_t)NL * 8u;
+    for (int step = 0; step < nsteps; ++step) {
+      const int s = step & (SR_STAGES - 1);
+      const int jl = jbase + step;
+      if (step >= SR_STAGES) mbar_wait(&empty[s], (uint32_t)(((step >> 2) - 1) & 1));
+      if (lane == 0) mbar_arrive_expect_tx(&full[s], bytes);
+      __syncwarp();
+      if (used) {
+        const int a = lane, row = jl - arr_lag(a);
+        bool real;
+        if (a == SA_X) real = row >= j0 && row < j1;
+        else if (a == SA_PD) real = row >= j0 - SR_YLO + 1 && row < j1 + SR_YHI - 1;
+        else real = row >= jbase && row < jwin_hi;
+        real = real && row >= 0 && row < ny;
+        double* dst = stage + (s * SR_NARR + a) * NL;
+        if (real) {
+          const double* rowp = src[a] + (long long)row * nt;
+          int gg = g0, done = 0;
+          while (done < NL) {
+            int len = nt - gg;
+            if (len > NL - done) len = NL - done;
+            bulk_g2s(dst + done, rowp + gg, (uint32_t)len * 8u, &full[s]);
+            done += len;
+            gg = 0;
+          }
+        } else {
+          bulk_g2s(dst, a == SA_AP ? d.one_row : d.zero_row, (uint32_t)NL * 8u, &full[s]);
+        }
+      }
+    }
+  } else {
+    // -------------------------------------------------------------- compute warps
+    // own-column history (suffix = lag in rows behind the load row)
+    D2 AP1{1, 1}, AP2{1, 1}, AP3{1, 1}, AP4{1, 1};
+    D2 AN1{0, 0}, AN2{0, 0}, AN3{0, 0}, AN4{0, 0}, AN5{0, 0};
+    D2 oD1{0, 0}, oD2{0, 0}, oD3{0, 0};
+    D2 r1{0, 0}, r2{0, 0}, pdo2{0, 0}, pd2{0, 0}, pd3{0, 0}, rn3{0, 0}, u2_4{0, 0}, u2_5{0, 0};
+    for (int blk = 0; blk < nsteps; blk += SR_UNROLL) {
+#pragma unroll
+      for (int u = 0; u < SR_UNROLL; ++u) {
+        const int jl = jbase + blk + u;
+        const int s = u & (SR_STAGES - 1);                 // == step % STAGES (blk % 8 == 0)
+        // ring slots (compile-time): AE at lag L -> (u - L) & 7, 2-slot rings -> (u - L) & 1
+        double* ae0 = ringAE + ((u + 8) & 7) * NL;
+        double* ae1 = ringAE + ((u + 7) & 7) * NL;
+        double* ae2 = ringAE + ((u + 6) & 7) * NL;
+        double* ae3 = ringAE + ((u + 5) & 7) * NL;
+        double* ae4 = ringAE + ((u + 4) & 7) * NL;
+        double* w_0 = ringW + (u & 1) * NL;
+        double* w_1 = ringW + ((u + 1) & 1) * NL;
+        double* v_0 = ringV + (u & 1) * NL;
+        double* v_1 = ringV + ((u + 1) & 1) * NL;
+        double* p_1 = ringP + ((u + 1) & 1) * NL;
+        double* p_2 = ringP + (u & 1) * NL;
+        double* w2_2 = ringW2 + (u & 1) * NL;
+        double* w2_3 = ringW2 + ((u + 1) & 1) * NL;
+        double* v2_2 = ringV2 + (u & 1) * NL;
+        double* v2_3 = ringV2 + ((u + 1) & 1) * NL;
+        double* u2_3r = ringU2 + ((u + 1) & 1) * NL;
+        double* u2_4r = ringU2 + (u & 1) * NL;
+
+        mbar_wait(&full[s], (uint32_t)((u >> 2) & 1));     // k-th use of stage s: k = 2*(blk/8) + u/4
+        const double* stg = stage + s * SR_NARR * NL;
+        // (A) row jl: own values, D^-1, w = D^-1 r   (out-of-range rows arrive as zero / one rows)
+        const D2 r0 = ld2(stg + SA_R * NL, tl);
+        const D2 AP0 = ld2(stg + SA_AP * NL, tl);
+        const D2 AE0 = ld2(stg + SA_AE * NL, tl);
+        const D2 AN0 = ld2(stg + SA_AN * NL, tl);
+        const D2 pdo1 = use_pd ? ld2(stg + SA_PD * NL, tl) : D2{0, 0};
+        const D2 x2 = use_x ? ld2(stg + SA_X * NL, tl) : D2{0, 0};
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&empty[s]);        // this warp is done with stage s
+        const D2 iD0{fast_rcp(AP0.l), fast_rcp(AP0.r)};
+        const D2 oD0{omega * iD0.l, omega * iD0.r};
+        st2(ae0, tl, AE0);
+        D2 w0;
+        if constexpr (PC == SPC_NONE) w0 = r0; else w0 = {r0.l * iD0.l, r0.r * iD0.r};
+        st2(w_0, tl, w0);
+        compute_bar(NCT);                                     // barrier 1: row jl of the rings
+
+        // (B) v1(jl) = w - (omega/D) sum_L A w   (Eq. 3.5)      (C) z(jl-1), pd(jl-1)
+        D2 z1;
+        if constexpr (PC == SPC_ASSOR2) {
+          const D2 w1 = ld2(w_1, tl);
+          D2 sL{AN1.l * w1.l, AN1.r * w1.r};
+          if (fl.hasW) sL.l += ae0[im] * w_0[im];
+          if (fl.end) sL.l += AE0.l * w0.r;
+          if (fr.hasW) sL.r += AE0.l * w0.l;
+          if (fr.end) sL.r += AE0.r * w_0[ip];
+          const D2 v10{w0.l - oD0.l * sL.l, w0.r - oD0.r * sL.r};
+          st2(v_0, tl, v10);
+          const D2 v11 = ld2(v_1, tl);
+          const D2 AEm1 = ld2(ae1, tl);
+          D2 sU{AN1.l * v10.l, AN1.r * v10.r};
+          if (!fl.end) sU.l += AEm1.l * v11.r;
+          if (fl.w0) sU.l += ae1[im] * v_1[im];
+          if (!fr.end) sU.r += AEm1.r * v_1[ip];
+          if (fr.w0) sU.r += AEm1.l * v11.l;
+          z1 = {c2 * (v11.l - oD1.l * sU.l), c2 * (v11.r - oD1.r * sU.r)};
+        } else {
+          z1 = ld2(w_1, tl);                                  // D^-1 r (Jacobi) or r (none)
+        }
+        const D2 pd1 = first ? z1 : D2{z1.l + beta * pdo1.l, z1.r + beta * pdo1.r};   // step 9
+        st2(p_1, tl, pd1);
+        if (ITER) {
+          const int row1 = jl - 1;
+          if (row1 >= j0 && row1 < j1) {
+            double* q = pdout + (long long)row1 * nt;
+            if (fl.out) q[gl] = pd1.l;
+            if (fr.out) q[gr] = pd1.r;
+          }
+        }
+        // (D) s(jl-2) = A pd, r_{i+1} = r_i - alpha s, x, w2 = D^-1 r_{i+1}
+        D2 rn2;
+        {
+          const D2 AEm2 = ld2(ae2, tl);
+          D2 sv{AP2.l * pd2.l, AP2.r * pd2.r};
+          sv.l += ae2[im] * p_2[im];
+          sv.l += AEm2.l * pd2.r;
+          sv.r += AEm2.l * pd2.l;
+          sv.r += AEm2.r * p_2[ip];
+          sv.l += AN3.l * pd3.l + AN2.l * pd1.l;
+          sv.r += AN3.r * pd3.r + AN2.r * pd1.r;
+          rn2 = {r2.l - alpha * sv.l, r2.r - alpha * sv.r};  // step 5 (INIT: alpha = 0)
+          const int row2 = jl - 2;
+          if (row2 >= j0 && row2 < j1) {
+            const long long qb = (long long)row2 * nt;
+            if (fl.out) {
+              rout[qb + gl] = rn2.l;
+              acc_rr += rn2.l * rn2.l;
+              if (xupd) x[qb + gl] = x2.l + (alpha_prev * pdo2.l + alpha * pd2.l);   // step 4
+              if (MODE == SR_INIT_COLD) { x[qb + gl] = 0.0; acc_s += r2.l * r2.l; }
+              if (MODE == SR_INIT_WARM) acc_s += x2.l * x2.l;   // x2 holds S here
+            }
+            if (fr.out) {
+              rout[qb + gr] = rn2.r;
+              acc_rr += rn2.r * rn2.r;
+              if (xupd) x[qb + gr] = x2.r + (alpha_prev * pdo2.r + alpha * pd2.r);
+              if (MODE == SR_INIT_COLD) { x[qb + gr] = 0.0; acc_s += r2.r * r2.r; }
+              if (MODE == SR_INIT_WARM) acc_s += x2.r * x2.r;
+            }
+          }
+        }
+        D2 wz;
+        if constexpr (PC == SPC_NONE) wz = rn2;
+        else wz = {(rn2.l * oD2.l) * romega, (rn2.r * oD2.r) * romega};
+        st2(w2_2, tl, wz);
+        compute_bar(NCT);                                     // barrier 2: w2(jl-2) complete
+
+        // (E) v2(jl-2)   (F) z2(jl-3), gamma   (G) A z2 at jl-4, delta
+        D2 u2_3;
+        if constexpr (PC == SPC_ASSOR2) {
+          const D2 w23 = ld2(w2_3, tl);
+          const D2 AEm2 = ld2(ae2, tl);
+          D2 sL{AN3.l * w23.l, AN3.r * w23.r};
+          if (fl.hasW) sL.l += ae2[im] * w2_2[im];
+          if (fl.end) sL.l += AEm2.l * wz.r;
+          if (fr.hasW) sL.r += AEm2.l * wz.l;
+          if (fr.end) sL.r += AEm2.r * w2_2[ip];
+          const D2 v22{wz.l - oD2.l * sL.l, wz.r - oD2.r * sL.r};
+          st2(v2_2, tl, v22);
+          const D2 v23 = ld2(v2_3, tl);
+          const D2 AEm3 = ld2(ae3, tl);
+          D2 sU{AN3.l * v22.l, AN3.r * v22.r};
+          if (!fl.end) sU.l += AEm3.l * v23.r;
+          if (fl.w0) sU.l += ae3[im] * v2_3[im];
+          if (!fr.end) sU.r += AEm3.r * v2_3[ip];
+          if (fr.w0) sU.r += AEm3.l * v23.l;
+          u2_3 = {c2 * (v23.l - oD3.l * sU.l), c2 * (v23.r - oD3.r * sU.r)};
+        } else {
+          u2_3 = ld2(w2_3, tl);
+        }
+        st2(u2_3r, tl, u2_3);
+        {
+          const int row3 = jl - 3;
+          if (row3 >= j0 && row3 < j1) {
+            if (fl.out) acc_g += rn3.l * u2_3.l;              // gamma = r.z
+            if (fr.out) acc_g += rn3.r * u2_3.r;
+          }
+          const D2 AEm4 = ld2(ae4, tl);
+          D2 wv{AP4.l * u2_4.l, AP4.r * u2_4.r};
+          wv.l += ae4[im] * u2_4r[im];
+          wv.l += AEm4.l * u2_4.r;
+          wv.r += AEm4.l * u2_4.l;
+          wv.r += AEm4.r * u2_4r[ip];
+          wv.l += AN5.l * u2_5.l + AN4.l * u2_3.l;
+          wv.r += AN5.r * u2_5.r + AN4.r * u2_3.r;
+          const int row4 = jl - 4;
+          if (row4 >= j0 && row4 < j1) {
+            if (fl.out) acc_d += u2_4.l * wv.l;               // delta = z.Az
+            if (fr.out) acc_d += u2_4.r * wv.r;
+          }
+        }
+        // rotate the histories (register renaming across the unrolled steps)
+        u2_5 = u2_4; u2_4 = u2_3;
+        rn3 = rn2;
+        pd3 = pd2; pd2 = pd1;
+        pdo2 = pdo1;
+        r2 = r1; r1 = r0;
+        oD3 = oD2; oD2 = oD1; oD1 = oD0;
+        AP4 = AP3; AP3 = AP2; AP2 = AP1; AP1 = AP0;
+        AN5 = AN4; AN4 = AN3; AN3 = AN2; AN2 = AN1; AN1 = AN0;
+      }
+    }
+  }
+
+  // ---- per-CTA partials and the scalar stage (last CTA, fixed order)
+  double* red = ringAE;   // rings are dead now
+  double v[4] = {acc_rr, acc_g, acc_d, acc_s};
+  block_sum<4>(v, red);
+  const int ncta = t.n_tiles;
+  const int cta = blockIdx.x / K;
+  if (tid == 0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) d.partials[(long long)(q * K + k) * ncta + cta] = v[q];
+  }
+  if (last_cta_arrive(&d.counters[ITER ? KK_SR_ITER : KK_SR_INIT], gridDim.x)) {
+    for (int q = tid; q < 4 * K; q += blockDim.x) {
+      const double* srcp = d.partials + (long long)q * ncta;
+      double sum = 0.0;
+      for (int b = 0; b < ncta; ++b) sum += __ldcg(srcp + b);
+      red[q] = sum;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const double* rrk = red;
+      const double* gk = red + K;
+      const double* dk = red + 2 * K;
+      const double* ssk = red + 3 * K;
+      double rr = 0.0;
+      for (int kk = 0; kk < K; ++kk) { rr += rrk[kk]; d.cs.rrk[kk] = rrk[kk]; }
+      bool bad = false;
+      if (INIT) {
+        double SS = 0.0;
+        for (int kk = 0; kk < K; ++kk) { d.cs.Sk[kk] = ssk[kk]; SS += ssk[kk]; }
+        st->nS = sqrt(SS);
+        st->iter = 0; st->status = 0; st->converged = 0; st->done = 0; st->zero_p = 0;
+        if (st->nS == 0.0) {
+          st->rel = 0.0; st->done = 1; st->converged = 1; st->zero_p = 1;
+        } else {
+          st->rel = sqrt(rr) / st->nS;
+          if (st->fixed_iters == 0 && st->rel <= st->tol) { st->done = 1; st->converged = 1; }
+          else if (st->max_iter <= 0) { st->done = 1; st->status = -6; }
+        }
+        if (!st->done) {
+          if (st->coupling == 0) {
+            double gg = 0.0, dd = 0.0;
+            for (int kk = 0; kk < K; ++kk) { gg += gk[kk]; dd += dk[kk]; }
+            if (!(dd > 0.0)) bad = true;
+            const double a0 = gg / dd;
+            for (int kk = 0; kk < K; ++kk) { d.cs.alpha[kk] = a0; d.cs.beta[kk] = 0.0; d.cs.uvk[kk] = 0.0; }
+            st->d = gg;
+          } else {
+            for (int kk = 0; kk < K; ++kk) {
+              double a0 = 0.0;
+              if (gk[kk] != 0.0) { if (!(dk[kk] > 0.0)) bad = true; a0 = gk[kk] / dk[kk]; }
+              d.cs.alpha[kk] = a0; d.cs.beta[kk] = 0.0; d.cs.uvk[kk] = 0.0; d.cs.dk[kk] = gk[kk];
+            }
+          }
+          if (bad) { st->done = 1; st->status = -5; }
+        }
+      } else {
+        st->iter += 1;
+        st->rel = sqrt(rr) / st->nS;
+        for (int kk = 0; kk < K; ++kk) d.cs.uvk[kk] = d.cs.alpha[kk];   // alpha used this iteration
+        if (st->fixed_iters > 0) {
+          if (st->iter >= st->fixed_iters) st->done = 1;
+        } else if (st->rel <= st->tol) {
+          st->done = 1; st->converged = 1;
+        } else if (st->iter >= st->max_iter) {
+          st->done = 1; st->status = -6;
+        }
+        if (!st->done || st->fixed_iters > 0) {
+          if (st->coupling == 0) {
+            double g2 = 0.0, d2 = 0.0;
+            for (int kk = 0; kk < K; ++kk) { g2 += gk[kk]; d2 += dk[kk]; }
+            const double aold = d.cs.alpha[0];
+            const double b = g2 / st->d;
+            const double den = d2 - b * g2 / aold;
+            if (!(g2 > 0.0) || !(den > 0.0)) bad = true;
+            const double a = g2 / den;
+            for (int kk = 0; kk < K; ++kk) { d.cs.alpha[kk] = a; d.cs.beta[kk] = b; }
+            st->d = g2;
+          } else {
+            for (int kk = 0; kk < K; ++kk) {
+              const double aold = d.cs.alpha[kk], gold = d.cs.dk[kk];
+              double a = 0.0, b = 0.0;
+              if (gold != 0.0 && aold != 0.0) {
+                if (gk[kk] < 0.0) bad = true;
+                b = gk[kk] / gold;
+                const double den = dk[kk] - b * gk[kk] / aold;
+                a = (gk[kk] == 0.0) ? 0.0 : gk[kk] / den;
+              }
+              d.cs.alpha[kk] = a; d.cs.beta[kk] = b; d.cs.dk[kk] = gk[kk];
+            }
+          }
+          if (bad && !st->done) { st->done = 1; st->status = -5; }
+        }
+      }
+      if (use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, st->done ? 0u : 1u);
+      timing_end(d.timing, ITER ? KK_SR_ITER : KK_SR_INIT);
+    }
+  }
+}
+
+// x += alpha_{it-1} pd_{it-1} when the iteration count is odd (the last x update of the
+// two-at-a-time scheme is still pending).  Elementwise, reads the device iteration count.
+__global__ void k_sr_fixup(GridParams g, DevPtrs d, int K) {
+  const int it = d.st_->iter;
+  if ((it & 1) == 0) return;
+  const long long n = (long long)g.nt * g.ny;
+  const double* pd = d.u[0];   // pd_{it-1}, it-1 even -> parity 0
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n * K;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int kk = (int)(q / n);
+    d.p[q] = d.p[q] + d.cs.uvk[kk] * pd[q];
+  }
+}
+
+// --------------------------------------------------------------------- launchers
+static int sr_pairs(const TileCfg& t) { return t.tw / 2 + SR_HALO; }
+// compute warps (column pairs rounded up to whole warps) + one TMA producer warp
+static int sr_threads(const TileCfg& t) { return ((sr_pairs(t) + 31) & ~31) + 32; }
+
+template <typename KernelT>
+static cudaError_t sr_launch(KernelT kern, const GridParams& g, const DevPtrs& d, const TileCfg& t, int K,
+                             int parity, int odd, unsigned long long h, int use, cudaStream_t s) {
+  const int threads = sr_threads(t);
+  kern<<<dim3(t.n_tiles * K), threads, sr_smem_bytes(2 * sr_pairs(t)), s>>>(g, d, t, K, parity, odd, h, use);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sr_init(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,
+                           bool warm, unsigned long long h, cudaStream_t s) {
+  const int use = h != 0ull;
+  if (warm) {
+    if (precond == SPC_ASSOR2) return sr_launch(k_sr<SPC_ASSOR2, SR_INIT_WARM>, g, d, t, K, 1, 0, h, use, s);
+    if (precond == SPC_JACOBI) return sr_launch(k_sr<SPC_JACOBI, SR_INIT_WARM>, g, d, t, K, 1, 0, h, use, s);
+    return sr_launch(k_sr<SPC_NONE, SR_INIT_WARM>, g, d, t, K, 1, 0, h, use, s);
+  }
+  if (precond == SPC_ASSOR2) return sr_launch(k_sr<SPC_ASSOR2, SR_INIT_COLD>, g, d, t, K, 1, 0, h, use, s);
+  if (precond == SPC_JACOBI) return sr_launch(k_sr<SPC_JACOBI, SR_INIT_COLD>, g, d, t, K, 1, 0, h, use, s);
+  return sr_launch(k_sr<SPC_NONE, SR_INIT_COLD>, g, d, t, K, 1, 0, h, use, s);
+}
+
+cudaError_t launch_sr_iter(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,
+                           int parity, unsigned long long h, cudaStream_t s) {
+  const int use = h != 0ull;
+  const int odd = parity & 1;   // iteration i = 2m + parity
+  if (precond == SPC_ASSOR2) return sr_launch(k_sr<SPC_ASSOR2, SR_ITER>, g, d, t, K, parity, odd, h, use, s);
+  if (precond == SPC_JACOBI) return sr_launch(k_sr<SPC_JACOBI, SR_ITER>, g, d, t, K, parity, odd, h, use, s);
+  return sr_launch(k_sr<SPC_NONE, SR_ITER>, g, d, t, K, parity, odd, h, use, s);
+}
+
+cudaError_t launch_sr_fixup(const GridParams& g, const DevPtrs& d, int K, cudaStream_t s) {
+  const long long work = (long long)g.nt * g.ny * K;
+  long long blocks = (work + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  k_sr_fixup<<<(int)blocks, 256, 0, s>>>(g, d, K);
+  return cudaGetLastError();
+}
+
+template <typename KernelT>
+static cudaError_t sr_set(KernelT kern, int bytes) {
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+cudaError_t configure_sr_kernels(const TileCfg& t) {
+  const int bytes = (int)sr_smem_bytes(2 * sr_pairs(t));
+  cudaError_t e = cudaSuccess;
+#define GMAF_SR_SET(...) if (e == cudaSuccess) e = sr_set(__VA_ARGS__, bytes)
+  GMAF_SR_SET(k_sr<SPC_ASSOR2, SR_ITER>); GMAF_SR_SET(k_sr<SPC_JACOBI, SR_ITER>); GMAF_SR_SET(k_sr<SPC_NONE, SR_ITER>);
+  GMAF_SR_SET(k_sr<SPC_ASSOR2, SR_INIT_COLD>); GMAF_SR_SET(k_sr<SPC_JACOBI, SR_INIT_COLD>);
+  GMAF_SR_SET(k_sr<SPC_NONE, SR_INIT_COLD>);
+  GMAF_SR_SET(k_sr<SPC_ASSOR2, SR_INIT_WARM>); GMAF_SR_SET(k_sr<SPC_JACOBI, SR_INIT_WARM>);
+  GMAF_SR_SET(k_sr<SPC_NONE, SR_INIT_WARM>);
+#undef GMAF_SR_SET
+  return e;
+}
+
+int sr_ctas_per_sm(const TileCfg& t) {
+  int n = 0;
+  const int threads = sr_threads(t);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_sr<SPC_ASSOR2, SR_ITER>, threads,
+                                                    sr_smem_bytes(2 * sr_pairs(t))) != cudaSuccess)
+    return 1;
+  return n;
+}
+
+}  // namespace gmaf

@@ -38,7 +38,7 @@ def test_version_and_sizes(pkg):
     g = pkg.make_grid(gi.grid(2048, 1024, "short"))
     nb = pkg.gmaf_workspace_bytes(g, 9)
     n = 2048 * 1024 * 9 * 8
-    assert 7 * n <= nb <= 7 * n + (64 << 20)      # 7 fields of K*n doubles + small state
+    assert 9 * n <= nb <= 9 * n + (64 << 20)      # 9 fields of K*n doubles + small state
     assert C.sizeof(pkg.gmaf_condition) == 13 * 8
     assert C.sizeof(pkg.gmaf_grid) == 4 + 4 + 4 * 8 + 5 * 4 + 4 + 8
 

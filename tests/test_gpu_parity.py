@@ -52,12 +52,16 @@ def check_bands_bitwise(S, orc, g, conds, ks=None):
     return AP, AE, AN, SS
 
 
-def full_parity(P, orc, g, conds, omega, precond="assor2", coupling="coupled", tol=1e-10):
+def full_parity(P, orc, g, conds, omega, precond="assor2", coupling="coupled", tol=1e-10, schedule=None):
     K = len(conds)
     S = P.JointSolver(g, K)
+    if schedule:
+        S.set_schedule(schedule)
     st, W = S.step(conds, tol=tol, omega=omega, precond=precond, coupling=coupling)
+    assert st.schedule == (schedule or ("single" if g["n_theta"] % 2 == 0 else "table1"))
     AP, AE, AN, SS = check_bands_bitwise(S, orc, g, conds)
-    ref = orc.pcg_joint(AP, AE, AN, SS, tol=tol, omega=omega, precond=precond, coupling=coupling)
+    ref = orc.pcg_joint(AP, AE, AN, SS, tol=tol, omega=omega, precond=precond, coupling=coupling,
+                        schedule="single" if st.schedule == "single" else "table1")
     assert st.converged and ref.converged
     # same recurrence, different summation order: the stopping iteration may shift by a
     # few iterations on long, ill-conditioned (textured) runs
@@ -78,22 +82,36 @@ def test_c1_parity(P, orc, gi):
     assert abs(st.iterations - 106) <= 3
 
 
-def test_ragged_textured_parity(P, orc, gi):
+@pytest.mark.parametrize("schedule", ["single", "table1"])
+def test_ragged_textured_parity(P, orc, gi, schedule):
     """Several strips with a ragged last strip, several row chunks, textured."""
     g = gi.grid(300, 70, "short", tex_n_theta=12, tex_n_y=4, tex_band_rows=20)
     conds = gi.fd_conditions(gi.condition())
-    full_parity(P, orc, g, conds, 1.6)
+    full_parity(P, orc, g, conds, 1.6, schedule=schedule)
 
 
+def test_odd_ntheta_uses_table1(P, orc, gi):
+    """Odd n_theta: the single-pass kernel's 16-byte TMA rows do not apply; the two-phase
+    schedule serves it (same method, same bars)."""
+    g = gi.grid(301, 45, "short", tex_n_theta=12, tex_n_y=4, tex_band_rows=20)
+    full_parity(P, orc, g, gi.fd_conditions(gi.condition()), 1.6)
+    S = P.JointSolver(g, 1)
+    with pytest.raises(P.GmafError):
+        S.set_schedule("single")
+    S.close()
+
+
+@pytest.mark.parametrize("schedule", ["single", "table1"])
 @pytest.mark.parametrize("precond", ["jacobi", "none"])
-def test_other_preconditioners(P, orc, gi, precond):
+def test_other_preconditioners(P, orc, gi, precond, schedule):
     g = gi.grid(96, 40, "smooth")
-    full_parity(P, orc, g, gi.random_conditions(3, 3), 1.8, precond=precond)
+    full_parity(P, orc, g, gi.random_conditions(3, 3), 1.8, precond=precond, schedule=schedule)
 
 
-def test_lockstep_parity(P, orc, gi):
+@pytest.mark.parametrize("schedule", ["single", "table1"])
+def test_lockstep_parity(P, orc, gi, schedule):
     g = gi.grid(128, 64, "smooth")
-    full_parity(P, orc, g, gi.random_conditions(4, 4), 1.7, coupling="lockstep")
+    full_parity(P, orc, g, gi.random_conditions(4, 4), 1.7, coupling="lockstep", schedule=schedule)
 
 
 @pytest.mark.parametrize("seed", range(6))
@@ -105,21 +123,26 @@ def test_random_states(P, orc, gi, seed):
     full_parity(P, orc, g, gi.random_conditions(100 + seed, 3), 1.6)
 
 
-def test_fixed_iterates_match(P, orc, gi):
+@pytest.mark.parametrize("schedule", ["single", "table1"])
+def test_fixed_iterates_match(P, orc, gi, schedule):
     """After exactly j iterations (max_iter = j) the GPU iterate equals the oracle's
-    j-th iterate to rounding: the same Table-1 recurrence, step by step."""
+    j-th iterate (same schedule) to rounding: the same recurrence, step by step."""
     g = gi.grid(200, 48, "short", tex_n_theta=10, tex_n_y=3, tex_band_rows=12)
     conds = gi.fd_conditions(gi.condition())
     S = P.JointSolver(g, 9)
+    S.set_schedule(schedule)
     S.thickness(conds)
     S.assemble()
     AP, AE, AN, SS = orc.assemble_joint(g, conds)
-    for j in (1, 2, 5, 17):
+    for j in (1, 2, 3, 5, 17):
         st = S.solve(tol=1e-30, omega=1.6, max_iter=j, raise_on_error=False)
         assert st.status == -6 and st.iterations == j
-        ref = orc.pcg_joint(AP, AE, AN, SS, tol=1e-30, omega=1.6, max_iter=j)
+        ref = orc.pcg_joint(AP, AE, AN, SS, tol=1e-30, omega=1.6, max_iter=j, schedule=schedule)
         pg = np.stack([S.get("p", k) for k in range(9)])
         assert rel(pg, ref.p) <= 1e-9, (j, rel(pg, ref.p))
+        r = np.stack([S.get("r", k) for k in range(9)])
+        rref = SS - np.stack([orc.spmv(AP[k], AE[k], AN[k], ref.p[k]) for k in range(9)])
+        assert rel(r, rref) <= 1e-6, (j, rel(r, rref))    # recursive vs true residual
     S.close()
 
 

@@ -39,15 +39,15 @@ constexpr int SR_HALO = 6;      // theta halo (columns) on each side
 constexpr int SR_YLO = 4;       // rows loaded below the chunk
 constexpr int SR_YHI = 4;       // rows loaded above the chunk
 constexpr int SR_LAG = 4;       // the delta stage trails the load by 4 rows
-constexpr int SR_STAGES = 4;    // TMA ring depth
-constexpr int SR_NARR = 6;      // streamed arrays per stage
+constexpr int SR_VSLOTS = 4;    // TMA ring of vector rows (r, pd, x), consumed in one step
+constexpr int SR_CSLOTS = 8;    // TMA ring of coefficient rows (AP, AE, AN), alive 6 steps
 constexpr int SR_UNROLL = 8;    // row-loop unroll = coefficient-ring period
 enum { SA_R = 0, SA_PD = 1, SA_X = 2, SA_AP = 3, SA_AE = 4, SA_AN = 5 };
 // row lag of each streamed array in the stage of step jl: pd_{i-1} is consumed at jl-1,
 // x (or S in a warm init) at jl-2; the others at jl.
 __host__ __device__ constexpr int arr_lag(int a) { return a == SA_PD ? 1 : (a == SA_X ? 2 : 0); }
 
-enum { SR_ITER = 0, SR_INIT_COLD = 1, SR_INIT_WARM = 2 };
+enum { SR_ITER_EVEN = 0, SR_ITER_ODD = 3, SR_INIT_COLD = 1, SR_INIT_WARM = 2 };
 enum { SPC_NONE = 0, SPC_JACOBI = 1, SPC_ASSOR2 = 2 };
 
 // ------------------------------------------------------------------- PTX helpers
@@ -112,8 +112,9 @@ __device__ __forceinline__ void st2(double* base, int t, D2 v) {
 }
 
 __host__ __device__ inline size_t sr_smem_bytes(int nl) {
-  // stages + AE ring (8) + 6 derived rings (2 each) + full/empty mbarriers
-  return (size_t)(SR_STAGES * SR_NARR + SR_UNROLL + 12) * nl * sizeof(double) + 2 * SR_STAGES * sizeof(uint64_t) + 64;
+  // vector slots + coefficient slots + 6 derived rings (2 each) + full/empty mbarriers
+  return (size_t)(SR_VSLOTS * 3 + SR_CSLOTS * 3 + 12) * nl * sizeof(double) +
+         2 * (SR_VSLOTS + SR_CSLOTS) * sizeof(uint64_t) + 64;
 }
 
 // Per-column flags of the ASSOR split on the periodic ring (DESIGN.md R-A12).
@@ -121,22 +122,24 @@ struct ColFlags { bool hasW, w0, end, out; };
 
 template <int PC, int MODE>
 __global__ void __launch_bounds__(192, 2)
-k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, int odd_iter, unsigned long long hcond,
-     int use_cond) {
+k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long hcond, int use_cond) {
   extern __shared__ __align__(128) double smem_raw[];
-  constexpr bool ITER = (MODE == SR_ITER);
+  constexpr bool ITER = (MODE == SR_ITER_EVEN || MODE == SR_ITER_ODD);
+  constexpr bool XUPD = (MODE == SR_ITER_ODD);         // x += a_{i-1} pd_{i-1} + a_i pd_i
   constexpr bool INIT = !ITER;
+  constexpr bool USE_PD = ITER;                         // pd_{-1} = 0 is stored by the init
+  constexpr bool USE_X = XUPD || (MODE == SR_INIT_WARM);  // a warm init streams S in the x slot
   SolverState* st = d.st_;
   if (ITER && st->done) return;
   timing_begin(d.timing, ITER ? KK_SR_ITER : KK_SR_INIT);
 
-  // warps 0 .. NCW-1 compute (one thread per column pair); the last warp streams rows (TMA)
-  const int NTC = t.tw / 2 + SR_HALO;     // column pairs = compute lanes doing work
-  const int NCT = (NTC + 31) & ~31;       // compute threads (whole warps; idle lanes duplicate the last pair)
+  // warps 0 .. NCT/32-1 compute (one thread per column pair); the last warp streams rows (TMA)
+  const int NTC = t.tw / 2 + SR_HALO;     // column pairs
+  const int NCT = (NTC + 31) & ~31;       // compute threads (whole warps; idle lanes alias the last pair)
   const int NL = 2 * NTC;                 // loaded columns = tw + 2*HALO
   const int tid = threadIdx.x;
   const bool is_producer = tid >= NCT;
-  const int tl = min(tid, NTC - 1);       // column-pair index (idle lanes alias the last pair)
+  const int tl = min(tid, NTC - 1);
   const bool active = tid < NTC;
   const int k = blockIdx.x % K;
   const int tile = blockIdx.x / K;
@@ -144,213 +147,234 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, int odd_iter, unsign
   const int i0 = strip * t.tw;
   const int j0 = chunk * t.th, j1 = min(j0 + t.th, g.ny);
   const int nt = g.nt, ny = g.ny;
-  const int cl = 2 * tl, cr = 2 * tl + 1;           // local columns of this thread
+  const int cl = 2 * tl, cr = 2 * tl + 1;
   int gl = (i0 - SR_HALO + cl) % nt;
   if (gl < 0) gl += nt;
   const int gr = (gl + 1 == nt) ? 0 : gl + 1;
-  ColFlags fl, fr;
-  fl.hasW = gl >= 1; fl.w0 = gl == 0; fl.end = gl == nt - 1;
-  fr.hasW = gr >= 1; fr.w0 = gr == 0; fr.end = gr == nt - 1;
-  fl.out = active && (cl >= SR_HALO) && (cl < SR_HALO + t.tw) && (i0 + cl - SR_HALO < nt);
-  fr.out = active && (cr >= SR_HALO) && (cr < SR_HALO + t.tw) && (i0 + cr - SR_HALO < nt);
+  // ASSOR split flags on the periodic ring (R-A12): W term in L unless the W-wrap (col 0);
+  // E term in U unless the E-wrap (col nt-1)
+  const bool lW = gl >= 1, lW0 = gl == 0, lE = gl == nt - 1;
+  const bool rW = gr >= 1, rW0 = gr == 0, rE = gr == nt - 1;
+  const bool outL = active && (cl >= SR_HALO) && (cl < SR_HALO + t.tw) && (i0 + cl - SR_HALO < nt);
+  const bool outR = active && (cr >= SR_HALO) && (cr < SR_HALO + t.tw) && (i0 + cr - SR_HALO < nt);
   const int im = max(cl - 1, 0);           // scalar index of the left neighbour of cl
   const int ip = min(cr + 1, NL - 1);      // scalar index of the right neighbour of cr
 
-  double* stage = smem_raw;                                  // [STAGES][NARR][NL]
-  double* ringAE = stage + SR_STAGES * SR_NARR * NL;         // [8][NL]
-  double* ringW = ringAE + SR_UNROLL * NL;                   // [2][NL] each
+  double* vstage = smem_raw;                                 // [4][3][NL]  r, pd, x rows
+  double* cring = vstage + SR_VSLOTS * 3 * NL;               // [8][3][NL]  AP, AE, AN rows
+  double* ringW = cring + SR_CSLOTS * 3 * NL;                // [2][NL] each
   double* ringV = ringW + 2 * NL;
   double* ringP = ringV + 2 * NL;
   double* ringW2 = ringP + 2 * NL;
   double* ringV2 = ringW2 + 2 * NL;
   double* ringU2 = ringV2 + 2 * NL;
-  uint64_t* full = reinterpret_cast<uint64_t*>(ringU2 + 2 * NL);
-  uint64_t* empty = full + SR_STAGES;
+  uint64_t* full_v = reinterpret_cast<uint64_t*>(ringU2 + 2 * NL);
+  uint64_t* empty_v = full_v + SR_VSLOTS;
+  uint64_t* full_c = empty_v + SR_VSLOTS;
+  uint64_t* empty_c = full_c + SR_CSLOTS;
 
   const long long n = (long long)nt * ny;
   const int m = d.cp[k].mat;
   // ITER: r_i = R[parity], pd_{i-1} = PD[1-parity]; writes R[1-parity], PD[parity].
-  // INIT: r_0 = S (cold) or R[1] (warm: = S - A x0 from the residual pre-pass); writes R[0].
+  // INIT: r_0 = S (cold) or R[1] (warm: = S - A x0 from the residual pre-pass); writes R[0]
+  //       and pd_{-1} = 0 into PD[1].
   const double* rin = ITER ? d.r[parity] + (long long)k * n
                            : (MODE == SR_INIT_COLD ? d.S + (long long)k * n : d.r[1] + (long long)k * n);
   double* rout = (ITER ? d.r[1 - parity] : d.r[0]) + (long long)k * n;
-  double* pdout = d.u[parity] + (long long)k * n;
+  double* pdout = (ITER ? d.u[parity] : d.u[1]) + (long long)k * n;
   double* x = d.p + (long long)k * n;
 
-  const bool first = INIT || (st->iter == 0);
-  const bool xupd = ITER && (odd_iter != 0);            // x += a_{i-1} pd_{i-1} + a_i pd_i
   const double alpha = ITER ? d.cs.alpha[k] : 0.0;
   const double alpha_prev = ITER ? d.cs.uvk[k] : 0.0;   // uvk holds alpha_{i-1} here
-  const double beta = first ? 0.0 : d.cs.beta[k];
+  const double beta = ITER ? d.cs.beta[k] : 0.0;
   const double omega = st->omega;
   const double c2 = (2.0 - omega) * omega;
   const double romega = 1.0 / omega;
-  const bool use_pd = ITER && !first;
-  const bool use_x = xupd || (MODE == SR_INIT_WARM);   // a warm init streams S in the x slot
 
   const int jbase = j0 - SR_YLO;
-  // steps jl = jbase .. jbase + nsteps - 1; the real ones end at j1 + LAG - 1, the rest are
-  // padding to a whole number of unrolled blocks (all their rows read as zero rows)
+  // steps jl = jbase .. jbase + nsteps - 1; the real ones end at j1 + LAG - 1, the rest pad to
+  // a whole number of unrolled blocks (their rows read as zero rows)
   const int nsteps = ((j1 + SR_LAG - jbase) + SR_UNROLL - 1) & ~(SR_UNROLL - 1);
 
   if (tid == 0) {
-    for (int s = 0; s < SR_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], NCT / 32); }
+    for (int s = 0; s < SR_VSLOTS; ++s) { mbar_init(&full_v[s], 1); mbar_init(&empty_v[s], NCT / 32); }
+    for (int s = 0; s < SR_CSLOTS; ++s) { mbar_init(&full_c[s], 1); mbar_init(&empty_c[s], NCT / 32); }
     mbar_fence_init();
   }
-  for (int q = tid; q < (SR_UNROLL + 12) * NL; q += blockDim.x) ringAE[q] = 0.0;
+  for (int q = tid; q < 12 * NL; q += blockDim.x) ringW[q] = 0.0;
   __syncthreads();
 
   double acc_rr = 0, acc_g = 0, acc_d = 0, acc_s = 0;
   if (is_producer) {
     // ------------------------------------------------------------- TMA producer warp
+    // lanes 0-2 stream r, pd_{i-1}, x (4-slot ring, consumed at one step); lanes 3-5 stream
+    // AP, AE, AN (8-slot ring, alive for 6 steps)
     const int lane = tid - NCT;
-    const double* src[SR_NARR] = {rin, d.u[1 - parity] + (long long)k * n,
-                                  (MODE == SR_INIT_WARM) ? d.S + (long long)k * n : x,
-                                  d.AP + (long long)m * n, d.AE + (long long)m * n, d.AN + (long long)m * n};
-    const bool used = lane < SR_NARR && (lane != SA_PD || use_pd) && (lane != SA_X || use_x);
-    const int jwin_hi = min(j1 + SR_YHI, ny);
+    const bool vec = lane < 3;
+    const int a = vec ? lane : lane - 3;
+    const double* srcp = lane == 0 ? rin
+                       : lane == 1 ? d.u[1 - parity] + (long long)k * n
+                       : lane == 2 ? ((MODE == SR_INIT_WARM) ? d.S + (long long)k * n : x)
+                       : lane == 3 ? d.AP + (long long)m * n
+                       : lane == 4 ? d.AE + (long long)m * n
+                                   : d.AN + (long long)m * n;
+    const double* constrow = lane == 3 ? d.one_row : d.zero_row;
+    const bool used = lane < 6 && (lane != 1 || USE_PD) && (lane != 2 || USE_X);
+    const int lag = lane == 1 ? 1 : (lane == 2 ? 2 : 0);
+    int lo = jbase, hi = min(j1 + SR_YHI, ny);                         // rows really read
+    if (lane == 1) { lo = j0 - SR_YLO + 1; hi = min(j1 + SR_YHI - 1, ny); }
+    if (lane == 2) { lo = j0; hi = j1; }
+    if (lo < 0) lo = 0;
     int g0 = (i0 - SR_HALO) % nt;
     if (g0 < 0) g0 += nt;
-    uint32_t bytes = 0;
-    for (int a = 0; a < SR_NARR; ++a)
-      if (a < 3 ? (a == SA_R || (a == SA_PD && use_pd) || (a == SA_X && use_x)) : true) bytes += (uint32_t)NL * 8u;
+    const uint32_t vbytes = (uint32_t)NL * 8u * (uint32_t)(1 + (USE_PD ? 1 : 0) + (USE_X ? 1 : 0));
+    const uint32_t cbytes = (uint32_t)NL * 8u * 3u;
     for (int step = 0; step < nsteps; ++step) {
-      const int s = step & (SR_STAGES - 1);
-      const int jl = jbase + step;
-      if (step >= SR_STAGES) mbar_wait(&empty[s], (uint32_t)(((step >> 2) - 1) & 1));
-      if (lane == 0) mbar_arrive_expect_tx(&full[s], bytes);
+      const int sv = step & (SR_VSLOTS - 1), sc = step & (SR_CSLOTS - 1);
+      if (step >= SR_VSLOTS) mbar_wait(&empty_v[sv], (uint32_t)(((step / SR_VSLOTS) - 1) & 1));
+      if (step >= SR_CSLOTS) mbar_wait(&empty_c[sc], (uint32_t)(((step / SR_CSLOTS) - 1) & 1));
+      if (lane == 0) mbar_arrive_expect_tx(&full_v[sv], vbytes);
+      if (lane == 3) mbar_arrive_expect_tx(&full_c[sc], cbytes);
       __syncwarp();
       if (used) {
-        const int a = lane, row = jl - arr_lag(a);
-        bool real;
-        if (a == SA_X) real = row >= j0 && row < j1;
-        else if (a == SA_PD) real = row >= j0 - SR_YLO + 1 && row < j1 + SR_YHI - 1;
-        else real = row >= jbase && row < jwin_hi;
-        real = real && row >= 0 && row < ny;
-        double* dst = stage + (s * SR_NARR + a) * NL;
-        if (real) {
-          const double* rowp = src[a] + (long long)row * nt;
+        const int row = jbase + step - lag;
+        uint64_t* bar = vec ? &full_v[sv] : &full_c[sc];
+        double* dst = vec ? vstage + (sv * 3 + a) * NL : cring + (sc * 3 + a) * NL;
+        if (row >= lo && row < hi) {
+          const double* rowp = srcp + (long long)row * nt;
           int gg = g0, done = 0;
           while (done < NL) {
             int len = nt - gg;
             if (len > NL - done) len = NL - done;
-            bulk_g2s(dst + done, rowp + gg, (uint32_t)len * 8u, &full[s]);
+            bulk_g2s(dst + done, rowp + gg, (uint32_t)len * 8u, bar);
             done += len;
             gg = 0;
           }
         } else {
-          bulk_g2s(dst, a == SA_AP ? d.one_row : d.zero_row, (uint32_t)NL * 8u, &full[s]);
+          bulk_g2s(dst, constrow, (uint32_t)NL * 8u, bar);
         }
       }
     }
   } else {
     // -------------------------------------------------------------- compute warps
-    // own-column history (suffix = lag in rows behind the load row)
-    D2 AP1{1, 1}, AP2{1, 1}, AP3{1, 1}, AP4{1, 1};
-    D2 AN1{0, 0}, AN2{0, 0}, AN3{0, 0}, AN4{0, 0}, AN5{0, 0};
+    // own-column history in registers (suffix = lag in rows behind the load row);
+    // coefficient rows are read from the 8-slot ring at their lag
     D2 oD1{0, 0}, oD2{0, 0}, oD3{0, 0};
     D2 r1{0, 0}, r2{0, 0}, pdo2{0, 0}, pd2{0, 0}, pd3{0, 0}, rn3{0, 0}, u2_4{0, 0}, u2_5{0, 0};
     for (int blk = 0; blk < nsteps; blk += SR_UNROLL) {
+      const uint32_t cpar = (uint32_t)((blk / SR_UNROLL) & 1);       // phase parity of the 8-slot ring
 #pragma unroll
       for (int u = 0; u < SR_UNROLL; ++u) {
         const int jl = jbase + blk + u;
-        const int s = u & (SR_STAGES - 1);                 // == step % STAGES (blk % 8 == 0)
-        // ring slots (compile-time): AE at lag L -> (u - L) & 7, 2-slot rings -> (u - L) & 1
-        double* ae0 = ringAE + ((u + 8) & 7) * NL;
-        double* ae1 = ringAE + ((u + 7) & 7) * NL;
-        double* ae2 = ringAE + ((u + 6) & 7) * NL;
-        double* ae3 = ringAE + ((u + 5) & 7) * NL;
-        double* ae4 = ringAE + ((u + 4) & 7) * NL;
+        const int sv = u & (SR_VSLOTS - 1);
+        // coefficient rows at lag L live in slot (u - L) & 7; arrays AP=0, AE=1, AN=2
+        const double* c0 = cring + (((u + 8) & 7) * 3) * NL;
+        const double* c1 = cring + (((u + 7) & 7) * 3) * NL;
+        const double* c2r = cring + (((u + 6) & 7) * 3) * NL;
+        const double* c3 = cring + (((u + 5) & 7) * 3) * NL;
+        const double* c4 = cring + (((u + 4) & 7) * 3) * NL;
+        const double* c5 = cring + (((u + 3) & 7) * 3) * NL;
         double* w_0 = ringW + (u & 1) * NL;
-        double* w_1 = ringW + ((u + 1) & 1) * NL;
+        const double* w_1 = ringW + ((u + 1) & 1) * NL;
         double* v_0 = ringV + (u & 1) * NL;
-        double* v_1 = ringV + ((u + 1) & 1) * NL;
+        const double* v_1 = ringV + ((u + 1) & 1) * NL;
         double* p_1 = ringP + ((u + 1) & 1) * NL;
-        double* p_2 = ringP + (u & 1) * NL;
+        const double* p_2 = ringP + (u & 1) * NL;
         double* w2_2 = ringW2 + (u & 1) * NL;
-        double* w2_3 = ringW2 + ((u + 1) & 1) * NL;
+        const double* w2_3 = ringW2 + ((u + 1) & 1) * NL;
         double* v2_2 = ringV2 + (u & 1) * NL;
-        double* v2_3 = ringV2 + ((u + 1) & 1) * NL;
+        const double* v2_3 = ringV2 + ((u + 1) & 1) * NL;
         double* u2_3r = ringU2 + ((u + 1) & 1) * NL;
-        double* u2_4r = ringU2 + (u & 1) * NL;
+        const double* u2_4r = ringU2 + (u & 1) * NL;
 
-        mbar_wait(&full[s], (uint32_t)((u >> 2) & 1));     // k-th use of stage s: k = 2*(blk/8) + u/4
-        const double* stg = stage + s * SR_NARR * NL;
-        // (A) row jl: own values, D^-1, w = D^-1 r   (out-of-range rows arrive as zero / one rows)
-        const D2 r0 = ld2(stg + SA_R * NL, tl);
-        const D2 AP0 = ld2(stg + SA_AP * NL, tl);
-        const D2 AE0 = ld2(stg + SA_AE * NL, tl);
-        const D2 AN0 = ld2(stg + SA_AN * NL, tl);
-        const D2 pdo1 = use_pd ? ld2(stg + SA_PD * NL, tl) : D2{0, 0};
-        const D2 x2 = use_x ? ld2(stg + SA_X * NL, tl) : D2{0, 0};
+        // ---- batch 1: this row's streamed data and ring values completed before barrier 2
+        mbar_wait(&full_v[sv], (uint32_t)((u >> 2) & 1));
+        mbar_wait(&full_c[u], cpar);
+        const double* vs = vstage + sv * 3 * NL;
+        const D2 r0 = ld2(vs, tl);
+        const D2 pdo1 = USE_PD ? ld2(vs + NL, tl) : D2{0, 0};
+        const D2 x2 = USE_X ? ld2(vs + 2 * NL, tl) : D2{0, 0};
         __syncwarp();
-        if ((tid & 31) == 0) mbar_arrive(&empty[s]);        // this warp is done with stage s
+        if ((tid & 31) == 0) mbar_arrive(&empty_v[sv]);     // this warp is done with vector slot sv
+        const D2 AP0 = ld2(c0, tl);
+        const D2 AE0 = ld2(c0 + NL, tl);
+        const D2 AN1 = ld2(c1 + 2 * NL, tl);
+        const D2 w1 = ld2(w_1, tl);
+        // (A) row jl: D^-1, w = D^-1 r
         const D2 iD0{fast_rcp(AP0.l), fast_rcp(AP0.r)};
         const D2 oD0{omega * iD0.l, omega * iD0.r};
-        st2(ae0, tl, AE0);
         D2 w0;
         if constexpr (PC == SPC_NONE) w0 = r0; else w0 = {r0.l * iD0.l, r0.r * iD0.r};
         st2(w_0, tl, w0);
-        compute_bar(NCT);                                     // barrier 1: row jl of the rings
+        compute_bar(NCT);                                     // barrier 1: w(jl) complete
 
         // (B) v1(jl) = w - (omega/D) sum_L A w   (Eq. 3.5)      (C) z(jl-1), pd(jl-1)
         D2 z1;
         if constexpr (PC == SPC_ASSOR2) {
-          const D2 w1 = ld2(w_1, tl);
+          const double w0m = w_0[im], w0p = w_0[ip], ae0m = c0[NL + im];
+          const D2 v11 = ld2(v_1, tl);
+          const double v1m = v_1[im], v1p = v_1[ip];
+          const D2 AEm1 = ld2(c1 + NL, tl);
+          const double ae1m = c1[NL + im];
           D2 sL{AN1.l * w1.l, AN1.r * w1.r};
-          if (fl.hasW) sL.l += ae0[im] * w_0[im];
-          if (fl.end) sL.l += AE0.l * w0.r;
-          if (fr.hasW) sL.r += AE0.l * w0.l;
-          if (fr.end) sL.r += AE0.r * w_0[ip];
+          sL.l += lW ? ae0m * w0m : 0.0;
+          sL.l += lE ? AE0.l * w0.r : 0.0;
+          sL.r += rW ? AE0.l * w0.l : 0.0;
+          sL.r += rE ? AE0.r * w0p : 0.0;
           const D2 v10{w0.l - oD0.l * sL.l, w0.r - oD0.r * sL.r};
           st2(v_0, tl, v10);
-          const D2 v11 = ld2(v_1, tl);
-          const D2 AEm1 = ld2(ae1, tl);
           D2 sU{AN1.l * v10.l, AN1.r * v10.r};
-          if (!fl.end) sU.l += AEm1.l * v11.r;
-          if (fl.w0) sU.l += ae1[im] * v_1[im];
-          if (!fr.end) sU.r += AEm1.r * v_1[ip];
-          if (fr.w0) sU.r += AEm1.l * v11.l;
+          sU.l += lE ? 0.0 : AEm1.l * v11.r;
+          sU.l += lW0 ? ae1m * v1m : 0.0;
+          sU.r += rE ? 0.0 : AEm1.r * v1p;
+          sU.r += rW0 ? AEm1.l * v11.l : 0.0;
           z1 = {c2 * (v11.l - oD1.l * sU.l), c2 * (v11.r - oD1.r * sU.r)};
         } else {
-          z1 = ld2(w_1, tl);                                  // D^-1 r (Jacobi) or r (none)
+          z1 = w1;                                            // D^-1 r (Jacobi) or r (none)
         }
-        const D2 pd1 = first ? z1 : D2{z1.l + beta * pdo1.l, z1.r + beta * pdo1.r};   // step 9
+        const D2 pd1 = USE_PD ? D2{z1.l + beta * pdo1.l, z1.r + beta * pdo1.r} : z1;   // step 9
         st2(p_1, tl, pd1);
-        if (ITER) {
+        {
           const int row1 = jl - 1;
           if (row1 >= j0 && row1 < j1) {
             double* q = pdout + (long long)row1 * nt;
-            if (fl.out) q[gl] = pd1.l;
-            if (fr.out) q[gr] = pd1.r;
+            if (outL) q[gl] = ITER ? pd1.l : 0.0;             // INIT stores pd_{-1} = 0
+            if (outR) q[gr] = ITER ? pd1.r : 0.0;
           }
         }
         // (D) s(jl-2) = A pd, r_{i+1} = r_i - alpha s, x, w2 = D^-1 r_{i+1}
         D2 rn2;
         {
-          const D2 AEm2 = ld2(ae2, tl);
+          const D2 AP2 = ld2(c2r, tl);
+          const D2 AEm2 = ld2(c2r + NL, tl);
+          const double ae2m = c2r[NL + im];
+          const D2 AN2 = ld2(c2r + 2 * NL, tl);
+          const D2 AN3 = ld2(c3 + 2 * NL, tl);
+          const double p2m = p_2[im], p2p = p_2[ip];
           D2 sv{AP2.l * pd2.l, AP2.r * pd2.r};
-          sv.l += ae2[im] * p_2[im];
+          sv.l += ae2m * p2m;
           sv.l += AEm2.l * pd2.r;
           sv.r += AEm2.l * pd2.l;
-          sv.r += AEm2.r * p_2[ip];
+          sv.r += AEm2.r * p2p;
           sv.l += AN3.l * pd3.l + AN2.l * pd1.l;
           sv.r += AN3.r * pd3.r + AN2.r * pd1.r;
           rn2 = {r2.l - alpha * sv.l, r2.r - alpha * sv.r};  // step 5 (INIT: alpha = 0)
+        }
+        {
           const int row2 = jl - 2;
           if (row2 >= j0 && row2 < j1) {
             const long long qb = (long long)row2 * nt;
-            if (fl.out) {
+            if (outL) {
               rout[qb + gl] = rn2.l;
               acc_rr += rn2.l * rn2.l;
-              if (xupd) x[qb + gl] = x2.l + (alpha_prev * pdo2.l + alpha * pd2.l);   // step 4
+              if (XUPD) x[qb + gl] = x2.l + (alpha_prev * pdo2.l + alpha * pd2.l);   // step 4
               if (MODE == SR_INIT_COLD) { x[qb + gl] = 0.0; acc_s += r2.l * r2.l; }
               if (MODE == SR_INIT_WARM) acc_s += x2.l * x2.l;   // x2 holds S here
             }
-            if (fr.out) {
+            if (outR) {
               rout[qb + gr] = rn2.r;
               acc_rr += rn2.r * rn2.r;
-              if (xupd) x[qb + gr] = x2.r + (alpha_prev * pdo2.r + alpha * pd2.r);
+              if (XUPD) x[qb + gr] = x2.r + (alpha_prev * pdo2.r + alpha * pd2.r);
               if (MODE == SR_INIT_COLD) { x[qb + gr] = 0.0; acc_s += r2.r * r2.r; }
               if (MODE == SR_INIT_WARM) acc_s += x2.r * x2.r;
             }
@@ -364,48 +388,59 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, int odd_iter, unsign
 
         // (E) v2(jl-2)   (F) z2(jl-3), gamma   (G) A z2 at jl-4, delta
         D2 u2_3;
+        const D2 AN3 = ld2(c3 + 2 * NL, tl);
         if constexpr (PC == SPC_ASSOR2) {
+          const D2 AEm2 = ld2(c2r + NL, tl);
+          const double ae2m = c2r[NL + im];
           const D2 w23 = ld2(w2_3, tl);
-          const D2 AEm2 = ld2(ae2, tl);
+          const double wz2m = w2_2[im], wz2p = w2_2[ip];
+          const D2 v23 = ld2(v2_3, tl);
+          const double v23m = v2_3[im], v23p = v2_3[ip];
+          const D2 AEm3 = ld2(c3 + NL, tl);
+          const double ae3m = c3[NL + im];
           D2 sL{AN3.l * w23.l, AN3.r * w23.r};
-          if (fl.hasW) sL.l += ae2[im] * w2_2[im];
-          if (fl.end) sL.l += AEm2.l * wz.r;
-          if (fr.hasW) sL.r += AEm2.l * wz.l;
-          if (fr.end) sL.r += AEm2.r * w2_2[ip];
+          sL.l += lW ? ae2m * wz2m : 0.0;
+          sL.l += lE ? AEm2.l * wz.r : 0.0;
+          sL.r += rW ? AEm2.l * wz.l : 0.0;
+          sL.r += rE ? AEm2.r * wz2p : 0.0;
           const D2 v22{wz.l - oD2.l * sL.l, wz.r - oD2.r * sL.r};
           st2(v2_2, tl, v22);
-          const D2 v23 = ld2(v2_3, tl);
-          const D2 AEm3 = ld2(ae3, tl);
           D2 sU{AN3.l * v22.l, AN3.r * v22.r};
-          if (!fl.end) sU.l += AEm3.l * v23.r;
-          if (fl.w0) sU.l += ae3[im] * v2_3[im];
-          if (!fr.end) sU.r += AEm3.r * v2_3[ip];
-          if (fr.w0) sU.r += AEm3.l * v23.l;
+          sU.l += lE ? 0.0 : AEm3.l * v23.r;
+          sU.l += lW0 ? ae3m * v23m : 0.0;
+          sU.r += rE ? 0.0 : AEm3.r * v23p;
+          sU.r += rW0 ? AEm3.l * v23.l : 0.0;
           u2_3 = {c2 * (v23.l - oD3.l * sU.l), c2 * (v23.r - oD3.r * sU.r)};
         } else {
           u2_3 = ld2(w2_3, tl);
         }
         st2(u2_3r, tl, u2_3);
+        if (jl - 3 >= j0 && jl - 3 < j1) {
+          if (outL) acc_g += rn3.l * u2_3.l;                  // gamma = r.z
+          if (outR) acc_g += rn3.r * u2_3.r;
+        }
         {
-          const int row3 = jl - 3;
-          if (row3 >= j0 && row3 < j1) {
-            if (fl.out) acc_g += rn3.l * u2_3.l;              // gamma = r.z
-            if (fr.out) acc_g += rn3.r * u2_3.r;
-          }
-          const D2 AEm4 = ld2(ae4, tl);
+          const D2 AP4 = ld2(c4, tl);
+          const D2 AEm4 = ld2(c4 + NL, tl);
+          const double ae4m = c4[NL + im];
+          const D2 AN4 = ld2(c4 + 2 * NL, tl);
+          const D2 AN5 = ld2(c5 + 2 * NL, tl);
+          const double u24m = u2_4r[im], u24p = u2_4r[ip];
           D2 wv{AP4.l * u2_4.l, AP4.r * u2_4.r};
-          wv.l += ae4[im] * u2_4r[im];
+          wv.l += ae4m * u24m;
           wv.l += AEm4.l * u2_4.r;
           wv.r += AEm4.l * u2_4.l;
-          wv.r += AEm4.r * u2_4r[ip];
+          wv.r += AEm4.r * u24p;
           wv.l += AN5.l * u2_5.l + AN4.l * u2_3.l;
           wv.r += AN5.r * u2_5.r + AN4.r * u2_3.r;
-          const int row4 = jl - 4;
-          if (row4 >= j0 && row4 < j1) {
-            if (fl.out) acc_d += u2_4.l * wv.l;               // delta = z.Az
-            if (fr.out) acc_d += u2_4.r * wv.r;
+          if (jl - 4 >= j0 && jl - 4 < j1) {
+            if (outL) acc_d += u2_4.l * wv.l;                 // delta = z.Az
+            if (outR) acc_d += u2_4.r * wv.r;
           }
         }
+        __syncwarp();
+        if ((tid & 31) == 0 && blk + u >= 5)
+          mbar_arrive(&empty_c[(u + 3) & 7]);                 // coefficient row jl-5 released
         // rotate the histories (register renaming across the unrolled steps)
         u2_5 = u2_4; u2_4 = u2_3;
         rn3 = rn2;
@@ -413,14 +448,12 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, int odd_iter, unsign
         pdo2 = pdo1;
         r2 = r1; r1 = r0;
         oD3 = oD2; oD2 = oD1; oD1 = oD0;
-        AP4 = AP3; AP3 = AP2; AP2 = AP1; AP1 = AP0;
-        AN5 = AN4; AN4 = AN3; AN3 = AN2; AN2 = AN1; AN1 = AN0;
       }
     }
   }
 
   // ---- per-CTA partials and the scalar stage (last CTA, fixed order)
-  double* red = ringAE;   // rings are dead now
+  double* red = ringW;   // rings are dead now
   double v[4] = {acc_rr, acc_g, acc_d, acc_s};
   block_sum<4>(v, red);
   const int ncta = t.n_tiles;
@@ -539,9 +572,9 @@ static int sr_threads(const TileCfg& t) { return ((sr_pairs(t) + 31) & ~31) + 32
 
 template <typename KernelT>
 static cudaError_t sr_launch(KernelT kern, const GridParams& g, const DevPtrs& d, const TileCfg& t, int K,
-                             int parity, int odd, unsigned long long h, int use, cudaStream_t s) {
+                             int parity, unsigned long long h, int use, cudaStream_t s) {
   const int threads = sr_threads(t);
-  kern<<<dim3(t.n_tiles * K), threads, sr_smem_bytes(2 * sr_pairs(t)), s>>>(g, d, t, K, parity, odd, h, use);
+  kern<<<dim3(t.n_tiles * K), threads, sr_smem_bytes(2 * sr_pairs(t)), s>>>(g, d, t, K, parity, h, use);
   return cudaGetLastError();
 }
 
@@ -549,22 +582,27 @@ cudaError_t launch_sr_init(const GridParams& g, const DevPtrs& d, const TileCfg&
                            bool warm, unsigned long long h, cudaStream_t s) {
   const int use = h != 0ull;
   if (warm) {
-    if (precond == SPC_ASSOR2) return sr_launch(k_sr<SPC_ASSOR2, SR_INIT_WARM>, g, d, t, K, 1, 0, h, use, s);
-    if (precond == SPC_JACOBI) return sr_launch(k_sr<SPC_JACOBI, SR_INIT_WARM>, g, d, t, K, 1, 0, h, use, s);
-    return sr_launch(k_sr<SPC_NONE, SR_INIT_WARM>, g, d, t, K, 1, 0, h, use, s);
+    if (precond == SPC_ASSOR2) return sr_launch(k_sr<SPC_ASSOR2, SR_INIT_WARM>, g, d, t, K, 1, h, use, s);
+    if (precond == SPC_JACOBI) return sr_launch(k_sr<SPC_JACOBI, SR_INIT_WARM>, g, d, t, K, 1, h, use, s);
+    return sr_launch(k_sr<SPC_NONE, SR_INIT_WARM>, g, d, t, K, 1, h, use, s);
   }
-  if (precond == SPC_ASSOR2) return sr_launch(k_sr<SPC_ASSOR2, SR_INIT_COLD>, g, d, t, K, 1, 0, h, use, s);
-  if (precond == SPC_JACOBI) return sr_launch(k_sr<SPC_JACOBI, SR_INIT_COLD>, g, d, t, K, 1, 0, h, use, s);
-  return sr_launch(k_sr<SPC_NONE, SR_INIT_COLD>, g, d, t, K, 1, 0, h, use, s);
+  if (precond == SPC_ASSOR2) return sr_launch(k_sr<SPC_ASSOR2, SR_INIT_COLD>, g, d, t, K, 1, h, use, s);
+  if (precond == SPC_JACOBI) return sr_launch(k_sr<SPC_JACOBI, SR_INIT_COLD>, g, d, t, K, 1, h, use, s);
+  return sr_launch(k_sr<SPC_NONE, SR_INIT_COLD>, g, d, t, K, 1, h, use, s);
 }
 
+// iteration i = 2m + parity: odd iterations also apply the pending x update
 cudaError_t launch_sr_iter(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,
                            int parity, unsigned long long h, cudaStream_t s) {
   const int use = h != 0ull;
-  const int odd = parity & 1;   // iteration i = 2m + parity
-  if (precond == SPC_ASSOR2) return sr_launch(k_sr<SPC_ASSOR2, SR_ITER>, g, d, t, K, parity, odd, h, use, s);
-  if (precond == SPC_JACOBI) return sr_launch(k_sr<SPC_JACOBI, SR_ITER>, g, d, t, K, parity, odd, h, use, s);
-  return sr_launch(k_sr<SPC_NONE, SR_ITER>, g, d, t, K, parity, odd, h, use, s);
+  if (parity & 1) {
+    if (precond == SPC_ASSOR2) return sr_launch(k_sr<SPC_ASSOR2, SR_ITER_ODD>, g, d, t, K, parity, h, use, s);
+    if (precond == SPC_JACOBI) return sr_launch(k_sr<SPC_JACOBI, SR_ITER_ODD>, g, d, t, K, parity, h, use, s);
+    return sr_launch(k_sr<SPC_NONE, SR_ITER_ODD>, g, d, t, K, parity, h, use, s);
+  }
+  if (precond == SPC_ASSOR2) return sr_launch(k_sr<SPC_ASSOR2, SR_ITER_EVEN>, g, d, t, K, parity, h, use, s);
+  if (precond == SPC_JACOBI) return sr_launch(k_sr<SPC_JACOBI, SR_ITER_EVEN>, g, d, t, K, parity, h, use, s);
+  return sr_launch(k_sr<SPC_NONE, SR_ITER_EVEN>, g, d, t, K, parity, h, use, s);
 }
 
 cudaError_t launch_sr_fixup(const GridParams& g, const DevPtrs& d, int K, cudaStream_t s) {
@@ -584,7 +622,10 @@ cudaError_t configure_sr_kernels(const TileCfg& t) {
   const int bytes = (int)sr_smem_bytes(2 * sr_pairs(t));
   cudaError_t e = cudaSuccess;
 #define GMAF_SR_SET(...) if (e == cudaSuccess) e = sr_set(__VA_ARGS__, bytes)
-  GMAF_SR_SET(k_sr<SPC_ASSOR2, SR_ITER>); GMAF_SR_SET(k_sr<SPC_JACOBI, SR_ITER>); GMAF_SR_SET(k_sr<SPC_NONE, SR_ITER>);
+  GMAF_SR_SET(k_sr<SPC_ASSOR2, SR_ITER_EVEN>); GMAF_SR_SET(k_sr<SPC_JACOBI, SR_ITER_EVEN>);
+  GMAF_SR_SET(k_sr<SPC_NONE, SR_ITER_EVEN>);
+  GMAF_SR_SET(k_sr<SPC_ASSOR2, SR_ITER_ODD>); GMAF_SR_SET(k_sr<SPC_JACOBI, SR_ITER_ODD>);
+  GMAF_SR_SET(k_sr<SPC_NONE, SR_ITER_ODD>);
   GMAF_SR_SET(k_sr<SPC_ASSOR2, SR_INIT_COLD>); GMAF_SR_SET(k_sr<SPC_JACOBI, SR_INIT_COLD>);
   GMAF_SR_SET(k_sr<SPC_NONE, SR_INIT_COLD>);
   GMAF_SR_SET(k_sr<SPC_ASSOR2, SR_INIT_WARM>); GMAF_SR_SET(k_sr<SPC_JACOBI, SR_INIT_WARM>);
@@ -596,7 +637,7 @@ cudaError_t configure_sr_kernels(const TileCfg& t) {
 int sr_ctas_per_sm(const TileCfg& t) {
   int n = 0;
   const int threads = sr_threads(t);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_sr<SPC_ASSOR2, SR_ITER>, threads,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_sr<SPC_ASSOR2, SR_ITER_ODD>, threads,
                                                     sr_smem_bytes(2 * sr_pairs(t))) != cudaSuccess)
     return 1;
   return n;

@@ -29,7 +29,7 @@ int quad_ctas_per_condition(const GridParams& g, int K);
 cudaError_t configure_pcg_kernels(const TileCfg& t, int K);
 int pcg_ctas_per_sm(const TileCfg& t, int K);
 }
-static_assert(gmaf::SR_HALO_COLS == 6, "sr.cu halo");
+static_assert(gmaf::SR_HALO_COLS == 4, "sr.cu halo");
 
 using namespace gmaf;
 
@@ -62,9 +62,9 @@ size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 // One wave: as many (strip, chunk, condition) tiles as the GPU holds resident CTAs
 // (slots = SMs x CTAs/SM from the occupancy calculator), each CTA marching a long chunk.
-TileCfg make_tiles(int nt, int ny, int K, int slots) {
+TileCfg make_tiles(int nt, int ny, int K, int slots, int tw) {
   TileCfg t{};
-  t.tw = (nt >= 1024) ? 256 : 128;
+  t.tw = tw;
   t.n_strips = (nt + t.tw - 1) / t.tw;
   int chunks = slots / (t.n_strips * K);
   if (chunks < 1) chunks = 1;
@@ -78,6 +78,12 @@ TileCfg make_tiles(int nt, int ny, int K, int slots) {
 }
 
 constexpr int kMaxTilesPerCondition = 148 * 16;
+
+// strip widths: two-phase kernels 256/128 columns; the single-pass kernel keeps the seam
+// inside a strip, so its strips may not be wider than the ring (and need >= 12 columns)
+int tw_table1(int nt) { return nt >= 1024 ? 256 : 128; }
+int tw_single(int nt) { int w = nt < 256 ? nt : 256; return w & ~1; }
+bool single_ok(int nt) { return nt % 2 == 0 && nt >= 12; }
 constexpr int kConstRowLen = 1024;   // >= the widest TMA row segment (tw + 2*halo)
 
 int check_grid(const gmaf_grid* g) {
@@ -457,20 +463,20 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
     if (cudaGetDevice(&dev) != cudaSuccess ||
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
       return cleanup_fail(GMAF_E_CUDA);
-    TileCfg probe = make_tiles(grid->n_theta, grid->n_y, K, 1);
+    TileCfg probe = make_tiles(grid->n_theta, grid->n_y, K, 1, tw_table1(grid->n_theta));
     if (configure_pcg_kernels(probe, K) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
     const int occ = pcg_ctas_per_sm(probe, K);
-    ctx->tiles = make_tiles(grid->n_theta, grid->n_y, K, sms * (occ > 0 ? occ : 1));
+    ctx->tiles = make_tiles(grid->n_theta, grid->n_y, K, sms * (occ > 0 ? occ : 1), tw_table1(grid->n_theta));
     if (ctx->tiles.n_tiles > kMaxTilesPerCondition) return cleanup_fail(GMAF_E_INVALID_MESH);
     if (configure_pcg_kernels(ctx->tiles, K) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
     // single-pass kernel: its own tiles (wider halo, TMA ring) and occupancy
-    TileCfg sprobe = make_tiles(grid->n_theta, grid->n_y, K, 1);
+    TileCfg sprobe = make_tiles(grid->n_theta, grid->n_y, K, 1, tw_single(grid->n_theta));
     if (configure_sr_kernels(sprobe) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
     const int socc = sr_ctas_per_sm(sprobe);
-    ctx->tiles_sr = make_tiles(grid->n_theta, grid->n_y, K, sms * (socc > 0 ? socc : 1));
+    ctx->tiles_sr = make_tiles(grid->n_theta, grid->n_y, K, sms * (socc > 0 ? socc : 1), tw_single(grid->n_theta));
     if (ctx->tiles_sr.n_tiles > kMaxTilesPerCondition) return cleanup_fail(GMAF_E_INVALID_MESH);
     // the single-pass kernel streams rows with 16-byte TMA copies: needs an even n_theta
-    ctx->schedule = (grid->n_theta % 2 == 0) ? GMAF_SCHEDULE_SINGLE : GMAF_SCHEDULE_TABLE1;
+    ctx->schedule = single_ok(grid->n_theta) ? GMAF_SCHEDULE_SINGLE : GMAF_SCHEDULE_TABLE1;
     const char* sch = std::getenv("GMAF_SCHEDULE");
     if (sch && std::strcmp(sch, "table1") == 0) ctx->schedule = GMAF_SCHEDULE_TABLE1;
   }
@@ -657,7 +663,7 @@ gmaf_status gmaf_reset_kernel_times(gmaf_ctx* ctx) {
 gmaf_status gmaf_set_schedule(gmaf_ctx* ctx, int32_t schedule) {
   if (!ctx) return GMAF_E_INVALID_ARG;
   if (schedule == GMAF_SCHEDULE_TABLE1) { ctx->schedule = schedule; return GMAF_OK; }
-  if (schedule == GMAF_SCHEDULE_SINGLE && ctx->grid.n_theta % 2 == 0) { ctx->schedule = schedule; return GMAF_OK; }
+  if (schedule == GMAF_SCHEDULE_SINGLE && single_ok(ctx->grid.n_theta)) { ctx->schedule = schedule; return GMAF_OK; }
   return fail(ctx, GMAF_E_INVALID_ARG, "set_schedule: %d not available (n_theta %d)", schedule, ctx->grid.n_theta);
 }
 

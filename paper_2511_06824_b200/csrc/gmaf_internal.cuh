@@ -117,7 +117,7 @@ cudaError_t launch_residual_init(const GridParams& g, const DevPtrs& d, const Ti
                                  cudaStream_t s);
 
 // ---- launchers (sr.cu): single-pass schedule, one kernel + one reduction per iteration ----
-constexpr int SR_HALO_COLS = 6;
+constexpr int SR_HALO_COLS = 4;
 cudaError_t launch_sr_init(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,
                            bool warm, unsigned long long cond_handle, cudaStream_t s);
 cudaError_t launch_sr_iter(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,

@@ -18,14 +18,17 @@
 // other iteration) = 40 B, plus the 3 coefficient bands of the DISTINCT matrices (shared
 // through L2 by the conditions with equal e).
 //
-// Tiling.  A CTA owns TW output columns (+ HALO = 6 on each side: the dependency radius
-// of z_{i+1} and A z_{i+1} on r_i including the ASSOR seam) of one condition, one thread
-// per column PAIR, and marches over a chunk of rows.  Input rows are streamed by the TMA
-// engine (cp.async.bulk) into a 4-stage shared ring signalled by mbarriers (3 rows in
-// flight).  Derived rows (w, v1, pd, w2, v2, z2) live in 2-slot shared rings for the
-// theta-neighbour reads; coefficient rows in an 8-slot ring; own-column history in
-// registers.  The row loop is unrolled by 8 so every ring slot is a compile-time index.
-// Two barriers per row.  Stage lags (rows behind the load row jl):
+// Tiling.  Strip s of a condition owns output columns [s*TW - TW/2, (s+1)*TW - TW/2) (mod
+// n_theta: the periodic seam lies in the MIDDLE of strip 0, so no strip edge is within 6
+// columns of it and a halo of HALO = 4 columns -- the dependency radius of A M^-1 A M^-1
+// away from the seam -- suffices), one thread per column PAIR, marching over a chunk of
+// rows.  Rows are streamed by the TMA engine (cp.async.bulk) from a dedicated producer
+// warp: r, pd, x into a 4-slot ring (consumed in one step), A_P, A_E, A_N into an 8-slot
+// ring (alive for 6 steps), one full mbarrier per step, empty mbarriers per ring.  Derived
+// rows (w, v1, pd, w2, v2, z2) live in 2-slot shared rings for theta-neighbour reads;
+// own-column history in registers.  The row loop is unrolled by 8 so every ring slot is a
+// compile-time index.  Two compute-warp barriers per row.  Stage lags (rows behind the
+// load row jl):
 //   A(0) load, D^-1, w      B(0) v1 = (I - wD^-1L) w        C(1) z, pd
 //   D(2) s = A pd, r, x, w2 E(2) v2                         F(3) z2, gamma
 //   G(4) A z2, delta
@@ -35,17 +38,13 @@
 
 namespace gmaf {
 
-constexpr int SR_HALO = 6;      // theta halo (columns) on each side
+constexpr int SR_HALO = 4;      // theta halo (columns) on each side (seam kept mid-strip)
 constexpr int SR_YLO = 4;       // rows loaded below the chunk
 constexpr int SR_YHI = 4;       // rows loaded above the chunk
 constexpr int SR_LAG = 4;       // the delta stage trails the load by 4 rows
 constexpr int SR_VSLOTS = 4;    // TMA ring of vector rows (r, pd, x), consumed in one step
 constexpr int SR_CSLOTS = 8;    // TMA ring of coefficient rows (AP, AE, AN), alive 6 steps
 constexpr int SR_UNROLL = 8;    // row-loop unroll = coefficient-ring period
-enum { SA_R = 0, SA_PD = 1, SA_X = 2, SA_AP = 3, SA_AE = 4, SA_AN = 5 };
-// row lag of each streamed array in the stage of step jl: pd_{i-1} is consumed at jl-1,
-// x (or S in a warm init) at jl-2; the others at jl.
-__host__ __device__ constexpr int arr_lag(int a) { return a == SA_PD ? 1 : (a == SA_X ? 2 : 0); }
 
 enum { SR_ITER_EVEN = 0, SR_ITER_ODD = 3, SR_INIT_COLD = 1, SR_INIT_WARM = 2 };
 enum { SPC_NONE = 0, SPC_JACOBI = 1, SPC_ASSOR2 = 2 };
@@ -54,38 +53,44 @@ enum { SPC_NONE = 0, SPC_JACOBI = 1, SPC_ASSOR2 = 2 };
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
 __device__ __forceinline__ void mbar_fence_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
-               : "memory");
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
-      "LAB_WAIT:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@P1 bra DONE;\n"
-      "bra LAB_WAIT;\n"
-      "DONE:\n"
-      "}\n" ::"r"(smem_addr(bar)),
-      "r"(parity)
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
       : "memory");
+  return ok != 0;
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
+// consumers: spin on try_wait (the data is normally already there)
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) {
+  }
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+// producer: back off so a waiting producer does not steal issue slots from the compute warps
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) __nanosleep(128);
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
 }
 // named barrier 1 over the compute warps only (the producer warp never joins it)
 __device__ __forceinline__ void compute_bar(int nthreads) {
@@ -110,15 +115,15 @@ __device__ __forceinline__ D2 ld2(const double* base, int t) {
 __device__ __forceinline__ void st2(double* base, int t, D2 v) {
   reinterpret_cast<double2*>(base)[t] = make_double2(v.l, v.r);
 }
-
-__host__ __device__ inline size_t sr_smem_bytes(int nl) {
-  // vector slots + coefficient slots + 6 derived rings (2 each) + full/empty mbarriers
-  return (size_t)(SR_VSLOTS * 3 + SR_CSLOTS * 3 + 12) * nl * sizeof(double) +
-         2 * (SR_VSLOTS + SR_CSLOTS) * sizeof(uint64_t) + 64;
+__device__ __forceinline__ void stg2(double* p, D2 v) {   // 16-byte global store (pairs are aligned)
+  *reinterpret_cast<double2*>(p) = make_double2(v.l, v.r);
 }
 
-// Per-column flags of the ASSOR split on the periodic ring (DESIGN.md R-A12).
-struct ColFlags { bool hasW, w0, end, out; };
+__host__ __device__ inline size_t sr_smem_bytes(int nl) {
+  // vector slots + coefficient slots + 6 derived rings (2 each) + mbarriers
+  return (size_t)(SR_VSLOTS * 3 + SR_CSLOTS * 3 + 12) * nl * sizeof(double) +
+         (SR_CSLOTS + SR_VSLOTS + SR_CSLOTS) * sizeof(uint64_t) + 64;
+}
 
 template <int PC, int MODE>
 __global__ void __launch_bounds__(192, 2)
@@ -140,25 +145,25 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
   const int tid = threadIdx.x;
   const bool is_producer = tid >= NCT;
   const int tl = min(tid, NTC - 1);
-  const bool active = tid < NTC;
   const int k = blockIdx.x % K;
   const int tile = blockIdx.x / K;
   const int strip = tile % t.n_strips, chunk = tile / t.n_strips;
-  const int i0 = strip * t.tw;
-  const int j0 = chunk * t.th, j1 = min(j0 + t.th, g.ny);
   const int nt = g.nt, ny = g.ny;
-  const int cl = 2 * tl, cr = 2 * tl + 1;
+  const int i0 = strip * t.tw - t.tw / 2;           // first output column (may be negative: mod nt)
+  const int j0 = chunk * t.th, j1 = min(j0 + t.th, ny);
+  const int cl = 2 * tl;
   int gl = (i0 - SR_HALO + cl) % nt;
   if (gl < 0) gl += nt;
-  const int gr = (gl + 1 == nt) ? 0 : gl + 1;
-  // ASSOR split flags on the periodic ring (R-A12): W term in L unless the W-wrap (col 0);
-  // E term in U unless the E-wrap (col nt-1)
-  const bool lW = gl >= 1, lW0 = gl == 0, lE = gl == nt - 1;
-  const bool rW = gr >= 1, rW0 = gr == 0, rE = gr == nt - 1;
-  const bool outL = active && (cl >= SR_HALO) && (cl < SR_HALO + t.tw) && (i0 + cl - SR_HALO < nt);
-  const bool outR = active && (cr >= SR_HALO) && (cr < SR_HALO + t.tw) && (i0 + cr - SR_HALO < nt);
-  const int im = max(cl - 1, 0);           // scalar index of the left neighbour of cl
-  const int ip = min(cr + 1, NL - 1);      // scalar index of the right neighbour of cr
+  const int gr = gl + 1;                   // gl is even and nt is even: the pair never wraps
+  // output pair: inside [HALO, HALO + TW) and, for the last (ragged) strip, before column
+  // tw/2 + n_strips*tw - tw/2 ... i.e. its global output index i0 + cl - HALO < nt - tw/2
+  const int o = i0 + cl - SR_HALO + t.tw / 2;       // output index counted from strip 0's start
+  const bool out = (tid < NTC) && (cl >= SR_HALO) && (cl < SR_HALO + t.tw) && (o < nt);
+  // ASSOR split on the periodic ring (R-A12): only a pair holding column 0 on its left or
+  // column nt-1 on its right sees the wraps; every other pair uses the plain formulas.
+  const bool seamL = (gl == 0), seamR = (gr == nt - 1);
+  const int im = max(cl - 1, 0);           // scalar index of the left neighbour of the pair
+  const int ip = min(cl + 2, NL - 1);      // scalar index of the right neighbour of the pair
 
   double* vstage = smem_raw;                                 // [4][3][NL]  r, pd, x rows
   double* cring = vstage + SR_VSLOTS * 3 * NL;               // [8][3][NL]  AP, AE, AN rows
@@ -168,10 +173,10 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
   double* ringW2 = ringP + 2 * NL;
   double* ringV2 = ringW2 + 2 * NL;
   double* ringU2 = ringV2 + 2 * NL;
-  uint64_t* full_v = reinterpret_cast<uint64_t*>(ringU2 + 2 * NL);
-  uint64_t* empty_v = full_v + SR_VSLOTS;
-  uint64_t* full_c = empty_v + SR_VSLOTS;
-  uint64_t* empty_c = full_c + SR_CSLOTS;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ringU2 + 2 * NL);
+  const uint32_t full0 = smem_addr(bars);                     // [8] one per step mod 8
+  const uint32_t emptyv0 = full0 + 8 * SR_CSLOTS;             // [4]
+  const uint32_t emptyc0 = emptyv0 + 8 * SR_VSLOTS;           // [8]
 
   const long long n = (long long)nt * ny;
   const int m = d.cp[k].mat;
@@ -197,8 +202,9 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
   const int nsteps = ((j1 + SR_LAG - jbase) + SR_UNROLL - 1) & ~(SR_UNROLL - 1);
 
   if (tid == 0) {
-    for (int s = 0; s < SR_VSLOTS; ++s) { mbar_init(&full_v[s], 1); mbar_init(&empty_v[s], NCT / 32); }
-    for (int s = 0; s < SR_CSLOTS; ++s) { mbar_init(&full_c[s], 1); mbar_init(&empty_c[s], NCT / 32); }
+    for (int s = 0; s < SR_CSLOTS; ++s) mbar_init(full0 + 8 * s, 1);
+    for (int s = 0; s < SR_VSLOTS; ++s) mbar_init(emptyv0 + 8 * s, NCT / 32);
+    for (int s = 0; s < SR_CSLOTS; ++s) mbar_init(emptyc0 + 8 * s, NCT / 32);
     mbar_fence_init();
   }
   for (int q = tid; q < 12 * NL; q += blockDim.x) ringW[q] = 0.0;
@@ -207,11 +213,9 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
   double acc_rr = 0, acc_g = 0, acc_d = 0, acc_s = 0;
   if (is_producer) {
     // ------------------------------------------------------------- TMA producer warp
-    // lanes 0-2 stream r, pd_{i-1}, x (4-slot ring, consumed at one step); lanes 3-5 stream
-    // AP, AE, AN (8-slot ring, alive for 6 steps)
+    // lane a < 6 streams array a: 0 r, 1 pd_{i-1}, 2 x (or S), 3 AP, 4 AE, 5 AN
     const int lane = tid - NCT;
     const bool vec = lane < 3;
-    const int a = vec ? lane : lane - 3;
     const double* srcp = lane == 0 ? rin
                        : lane == 1 ? d.u[1 - parity] + (long long)k * n
                        : lane == 2 ? ((MODE == SR_INIT_WARM) ? d.S + (long long)k * n : x)
@@ -227,28 +231,28 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
     if (lo < 0) lo = 0;
     int g0 = (i0 - SR_HALO) % nt;
     if (g0 < 0) g0 += nt;
-    const uint32_t vbytes = (uint32_t)NL * 8u * (uint32_t)(1 + (USE_PD ? 1 : 0) + (USE_X ? 1 : 0));
-    const uint32_t cbytes = (uint32_t)NL * 8u * 3u;
+    const int len0 = min(NL, nt - g0);                  // first segment (the seam splits a row)
+    const uint32_t bytes = (uint32_t)NL * 8u * (uint32_t)(4 + (USE_PD ? 1 : 0) + (USE_X ? 1 : 0));
+    const uint32_t dst0 = smem_addr(vec ? vstage + lane * NL : cring + (lane - 3) * NL);
+    const uint32_t dstride = (uint32_t)(3 * NL * 8);    // bytes between slots
     for (int step = 0; step < nsteps; ++step) {
       const int sv = step & (SR_VSLOTS - 1), sc = step & (SR_CSLOTS - 1);
-      if (step >= SR_VSLOTS) mbar_wait(&empty_v[sv], (uint32_t)(((step / SR_VSLOTS) - 1) & 1));
-      if (step >= SR_CSLOTS) mbar_wait(&empty_c[sc], (uint32_t)(((step / SR_CSLOTS) - 1) & 1));
-      if (lane == 0) mbar_arrive_expect_tx(&full_v[sv], vbytes);
-      if (lane == 3) mbar_arrive_expect_tx(&full_c[sc], cbytes);
+      if (step >= SR_VSLOTS) mbar_wait_sleep(emptyv0 + 8 * sv, (uint32_t)(((step / SR_VSLOTS) - 1) & 1));
+      if (step >= SR_CSLOTS) mbar_wait_sleep(emptyc0 + 8 * sc, (uint32_t)(((step / SR_CSLOTS) - 1) & 1));
+      const uint32_t bar = full0 + 8 * sc;
+      if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
       __syncwarp();
       if (used) {
         const int row = jbase + step - lag;
-        uint64_t* bar = vec ? &full_v[sv] : &full_c[sc];
-        double* dst = vec ? vstage + (sv * 3 + a) * NL : cring + (sc * 3 + a) * NL;
+        const uint32_t dst = dst0 + (uint32_t)(vec ? sv : sc) * dstride;
         if (row >= lo && row < hi) {
           const double* rowp = srcp + (long long)row * nt;
-          int gg = g0, done = 0;
-          while (done < NL) {
-            int len = nt - gg;
-            if (len > NL - done) len = NL - done;
-            bulk_g2s(dst + done, rowp + gg, (uint32_t)len * 8u, bar);
+          bulk_g2s(dst, rowp + g0, (uint32_t)len0 * 8u, bar);
+          int done = len0;
+          while (done < NL) {                              // wrapped remainder (small n_theta loops)
+            const int len = min(NL - done, nt);
+            bulk_g2s(dst + (uint32_t)done * 8u, rowp, (uint32_t)len * 8u, bar);
             done += len;
-            gg = 0;
           }
         } else {
           bulk_g2s(dst, constrow, (uint32_t)NL * 8u, bar);
@@ -261,8 +265,9 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
     // coefficient rows are read from the 8-slot ring at their lag
     D2 oD1{0, 0}, oD2{0, 0}, oD3{0, 0};
     D2 r1{0, 0}, r2{0, 0}, pdo2{0, 0}, pd2{0, 0}, pd3{0, 0}, rn3{0, 0}, u2_4{0, 0}, u2_5{0, 0};
+    const bool lane0 = (tid & 31) == 0;
     for (int blk = 0; blk < nsteps; blk += SR_UNROLL) {
-      const uint32_t cpar = (uint32_t)((blk / SR_UNROLL) & 1);       // phase parity of the 8-slot ring
+      const uint32_t cpar = (uint32_t)((blk / SR_UNROLL) & 1);       // phase of the per-step barriers
 #pragma unroll
       for (int u = 0; u < SR_UNROLL; ++u) {
         const int jl = jbase + blk + u;
@@ -287,20 +292,18 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
         double* u2_3r = ringU2 + ((u + 1) & 1) * NL;
         const double* u2_4r = ringU2 + (u & 1) * NL;
 
-        // ---- batch 1: this row's streamed data and ring values completed before barrier 2
-        mbar_wait(&full_v[sv], (uint32_t)((u >> 2) & 1));
-        mbar_wait(&full_c[u], cpar);
+        // ---- (A) row jl: streamed data, D^-1, w = D^-1 r
+        mbar_wait(full0 + 8 * u, cpar);
         const double* vs = vstage + sv * 3 * NL;
         const D2 r0 = ld2(vs, tl);
         const D2 pdo1 = USE_PD ? ld2(vs + NL, tl) : D2{0, 0};
         const D2 x2 = USE_X ? ld2(vs + 2 * NL, tl) : D2{0, 0};
         __syncwarp();
-        if ((tid & 31) == 0) mbar_arrive(&empty_v[sv]);     // this warp is done with vector slot sv
+        if (lane0) mbar_arrive(emptyv0 + 8 * sv);            // this warp is done with vector slot sv
         const D2 AP0 = ld2(c0, tl);
         const D2 AE0 = ld2(c0 + NL, tl);
         const D2 AN1 = ld2(c1 + 2 * NL, tl);
         const D2 w1 = ld2(w_1, tl);
-        // (A) row jl: D^-1, w = D^-1 r
         const D2 iD0{fast_rcp(AP0.l), fast_rcp(AP0.r)};
         const D2 oD0{omega * iD0.l, omega * iD0.r};
         D2 w0;
@@ -308,77 +311,50 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
         st2(w_0, tl, w0);
         compute_bar(NCT);                                     // barrier 1: w(jl) complete
 
-        // (B) v1(jl) = w - (omega/D) sum_L A w   (Eq. 3.5)      (C) z(jl-1), pd(jl-1)
+        // ---- (B) v1(jl) = w - (omega/D) sum_L A w  (Eq. 3.5);  (C) z(jl-1), pd(jl-1)
         D2 z1;
         if constexpr (PC == SPC_ASSOR2) {
-          const double w0m = w_0[im], w0p = w_0[ip], ae0m = c0[NL + im];
+          const double w0m = w_0[im], ae0m = c0[NL + im];
           const D2 v11 = ld2(v_1, tl);
-          const double v1m = v_1[im], v1p = v_1[ip];
+          const double v1p = v_1[ip];
           const D2 AEm1 = ld2(c1 + NL, tl);
-          const double ae1m = c1[NL + im];
-          D2 sL{AN1.l * w1.l, AN1.r * w1.r};
-          sL.l += lW ? ae0m * w0m : 0.0;
-          sL.l += lE ? AE0.l * w0.r : 0.0;
-          sL.r += rW ? AE0.l * w0.l : 0.0;
-          sL.r += rE ? AE0.r * w0p : 0.0;
+          // plain pair: L = {W, S}, U = {E, N}
+          D2 sL{AN1.l * w1.l + ae0m * w0m, AN1.r * w1.r + AE0.l * w0.l};
+          if (seamL) sL.l -= ae0m * w0m;                          // column 0: W is the wrap (in U)
+          if (seamR) sL.r += AE0.r * w_0[ip];                     // column nt-1: E-wrap is in L
           const D2 v10{w0.l - oD0.l * sL.l, w0.r - oD0.r * sL.r};
           st2(v_0, tl, v10);
-          D2 sU{AN1.l * v10.l, AN1.r * v10.r};
-          sU.l += lE ? 0.0 : AEm1.l * v11.r;
-          sU.l += lW0 ? ae1m * v1m : 0.0;
-          sU.r += rE ? 0.0 : AEm1.r * v1p;
-          sU.r += rW0 ? AEm1.l * v11.l : 0.0;
+          D2 sU{AN1.l * v10.l + AEm1.l * v11.r, AN1.r * v10.r + AEm1.r * v1p};
+          if (seamL) sU.l += c1[NL + im] * v_1[im];               // column 0: W-wrap
+          if (seamR) sU.r -= AEm1.r * v1p;                        // column nt-1: no E in U
           z1 = {c2 * (v11.l - oD1.l * sU.l), c2 * (v11.r - oD1.r * sU.r)};
         } else {
           z1 = w1;                                            // D^-1 r (Jacobi) or r (none)
         }
         const D2 pd1 = USE_PD ? D2{z1.l + beta * pdo1.l, z1.r + beta * pdo1.r} : z1;   // step 9
         st2(p_1, tl, pd1);
-        {
-          const int row1 = jl - 1;
-          if (row1 >= j0 && row1 < j1) {
-            double* q = pdout + (long long)row1 * nt;
-            if (outL) q[gl] = ITER ? pd1.l : 0.0;             // INIT stores pd_{-1} = 0
-            if (outR) q[gr] = ITER ? pd1.r : 0.0;
-          }
-        }
-        // (D) s(jl-2) = A pd, r_{i+1} = r_i - alpha s, x, w2 = D^-1 r_{i+1}
+        if (out && jl - 1 >= j0 && jl - 1 < j1)
+          stg2(pdout + (long long)(jl - 1) * nt + gl, ITER ? pd1 : D2{0, 0});   // INIT: pd_{-1} = 0
+        // ---- (D) s(jl-2) = A pd, r_{i+1} = r_i - alpha s, x, w2 = D^-1 r_{i+1}
         D2 rn2;
         {
           const D2 AP2 = ld2(c2r, tl);
           const D2 AEm2 = ld2(c2r + NL, tl);
-          const double ae2m = c2r[NL + im];
           const D2 AN2 = ld2(c2r + 2 * NL, tl);
           const D2 AN3 = ld2(c3 + 2 * NL, tl);
-          const double p2m = p_2[im], p2p = p_2[ip];
-          D2 sv{AP2.l * pd2.l, AP2.r * pd2.r};
-          sv.l += ae2m * p2m;
-          sv.l += AEm2.l * pd2.r;
-          sv.r += AEm2.l * pd2.l;
-          sv.r += AEm2.r * p2p;
-          sv.l += AN3.l * pd3.l + AN2.l * pd1.l;
-          sv.r += AN3.r * pd3.r + AN2.r * pd1.r;
+          D2 sv{AP2.l * pd2.l + c2r[NL + im] * p_2[im], AP2.r * pd2.r + AEm2.l * pd2.l};
+          sv.l += AEm2.l * pd2.r + AN3.l * pd3.l + AN2.l * pd1.l;
+          sv.r += AEm2.r * p_2[ip] + AN3.r * pd3.r + AN2.r * pd1.r;
           rn2 = {r2.l - alpha * sv.l, r2.r - alpha * sv.r};  // step 5 (INIT: alpha = 0)
         }
-        {
-          const int row2 = jl - 2;
-          if (row2 >= j0 && row2 < j1) {
-            const long long qb = (long long)row2 * nt;
-            if (outL) {
-              rout[qb + gl] = rn2.l;
-              acc_rr += rn2.l * rn2.l;
-              if (XUPD) x[qb + gl] = x2.l + (alpha_prev * pdo2.l + alpha * pd2.l);   // step 4
-              if (MODE == SR_INIT_COLD) { x[qb + gl] = 0.0; acc_s += r2.l * r2.l; }
-              if (MODE == SR_INIT_WARM) acc_s += x2.l * x2.l;   // x2 holds S here
-            }
-            if (outR) {
-              rout[qb + gr] = rn2.r;
-              acc_rr += rn2.r * rn2.r;
-              if (XUPD) x[qb + gr] = x2.r + (alpha_prev * pdo2.r + alpha * pd2.r);
-              if (MODE == SR_INIT_COLD) { x[qb + gr] = 0.0; acc_s += r2.r * r2.r; }
-              if (MODE == SR_INIT_WARM) acc_s += x2.r * x2.r;
-            }
-          }
+        if (out && jl - 2 >= j0 && jl - 2 < j1) {
+          const long long q2 = (long long)(jl - 2) * nt + gl;
+          stg2(rout + q2, rn2);
+          acc_rr += rn2.l * rn2.l + rn2.r * rn2.r;
+          if (XUPD) stg2(x + q2, D2{x2.l + (alpha_prev * pdo2.l + alpha * pd2.l),      // step 4
+                                    x2.r + (alpha_prev * pdo2.r + alpha * pd2.r)});
+          if (MODE == SR_INIT_COLD) { stg2(x + q2, D2{0, 0}); acc_s += r2.l * r2.l + r2.r * r2.r; }
+          if (MODE == SR_INIT_WARM) acc_s += x2.l * x2.l + x2.r * x2.r;   // x2 holds S here
         }
         D2 wz;
         if constexpr (PC == SPC_NONE) wz = rn2;
@@ -386,61 +362,43 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
         st2(w2_2, tl, wz);
         compute_bar(NCT);                                     // barrier 2: w2(jl-2) complete
 
-        // (E) v2(jl-2)   (F) z2(jl-3), gamma   (G) A z2 at jl-4, delta
+        // ---- (E) v2(jl-2)   (F) z2(jl-3), gamma   (G) A z2 at jl-4, delta
         D2 u2_3;
         const D2 AN3 = ld2(c3 + 2 * NL, tl);
         if constexpr (PC == SPC_ASSOR2) {
           const D2 AEm2 = ld2(c2r + NL, tl);
           const double ae2m = c2r[NL + im];
           const D2 w23 = ld2(w2_3, tl);
-          const double wz2m = w2_2[im], wz2p = w2_2[ip];
+          const double wz2m = w2_2[im];
           const D2 v23 = ld2(v2_3, tl);
-          const double v23m = v2_3[im], v23p = v2_3[ip];
+          const double v23p = v2_3[ip];
           const D2 AEm3 = ld2(c3 + NL, tl);
-          const double ae3m = c3[NL + im];
-          D2 sL{AN3.l * w23.l, AN3.r * w23.r};
-          sL.l += lW ? ae2m * wz2m : 0.0;
-          sL.l += lE ? AEm2.l * wz.r : 0.0;
-          sL.r += rW ? AEm2.l * wz.l : 0.0;
-          sL.r += rE ? AEm2.r * wz2p : 0.0;
+          D2 sL{AN3.l * w23.l + ae2m * wz2m, AN3.r * w23.r + AEm2.l * wz.l};
+          if (seamL) sL.l -= ae2m * wz2m;
+          if (seamR) sL.r += AEm2.r * w2_2[ip];
           const D2 v22{wz.l - oD2.l * sL.l, wz.r - oD2.r * sL.r};
           st2(v2_2, tl, v22);
-          D2 sU{AN3.l * v22.l, AN3.r * v22.r};
-          sU.l += lE ? 0.0 : AEm3.l * v23.r;
-          sU.l += lW0 ? ae3m * v23m : 0.0;
-          sU.r += rE ? 0.0 : AEm3.r * v23p;
-          sU.r += rW0 ? AEm3.l * v23.l : 0.0;
+          D2 sU{AN3.l * v22.l + AEm3.l * v23.r, AN3.r * v22.r + AEm3.r * v23p};
+          if (seamL) sU.l += c3[NL + im] * v2_3[im];
+          if (seamR) sU.r -= AEm3.r * v23p;
           u2_3 = {c2 * (v23.l - oD3.l * sU.l), c2 * (v23.r - oD3.r * sU.r)};
         } else {
           u2_3 = ld2(w2_3, tl);
         }
         st2(u2_3r, tl, u2_3);
-        if (jl - 3 >= j0 && jl - 3 < j1) {
-          if (outL) acc_g += rn3.l * u2_3.l;                  // gamma = r.z
-          if (outR) acc_g += rn3.r * u2_3.r;
-        }
+        if (out && jl - 3 >= j0 && jl - 3 < j1) acc_g += rn3.l * u2_3.l + rn3.r * u2_3.r;   // gamma
         {
           const D2 AP4 = ld2(c4, tl);
           const D2 AEm4 = ld2(c4 + NL, tl);
-          const double ae4m = c4[NL + im];
           const D2 AN4 = ld2(c4 + 2 * NL, tl);
           const D2 AN5 = ld2(c5 + 2 * NL, tl);
-          const double u24m = u2_4r[im], u24p = u2_4r[ip];
-          D2 wv{AP4.l * u2_4.l, AP4.r * u2_4.r};
-          wv.l += ae4m * u24m;
-          wv.l += AEm4.l * u2_4.r;
-          wv.r += AEm4.l * u2_4.l;
-          wv.r += AEm4.r * u24p;
-          wv.l += AN5.l * u2_5.l + AN4.l * u2_3.l;
-          wv.r += AN5.r * u2_5.r + AN4.r * u2_3.r;
-          if (jl - 4 >= j0 && jl - 4 < j1) {
-            if (outL) acc_d += u2_4.l * wv.l;                 // delta = z.Az
-            if (outR) acc_d += u2_4.r * wv.r;
-          }
+          D2 wv{AP4.l * u2_4.l + c4[NL + im] * u2_4r[im], AP4.r * u2_4.r + AEm4.l * u2_4.l};
+          wv.l += AEm4.l * u2_4.r + AN5.l * u2_5.l + AN4.l * u2_3.l;
+          wv.r += AEm4.r * u2_4r[ip] + AN5.r * u2_5.r + AN4.r * u2_3.r;
+          if (out && jl - 4 >= j0 && jl - 4 < j1) acc_d += u2_4.l * wv.l + u2_4.r * wv.r;  // delta
         }
         __syncwarp();
-        if ((tid & 31) == 0 && blk + u >= 5)
-          mbar_arrive(&empty_c[(u + 3) & 7]);                 // coefficient row jl-5 released
+        if (lane0 && blk + u >= 5) mbar_arrive(emptyc0 + 8 * ((u + 3) & 7));   // coefficient row jl-5 done
         // rotate the histories (register renaming across the unrolled steps)
         u2_5 = u2_4; u2_4 = u2_3;
         rn3 = rn2;

@@ -115,6 +115,12 @@ __device__ __forceinline__ D2 ld2(const double* base, int t) {
 __device__ __forceinline__ void st2(double* base, int t, D2 v) {
   reinterpret_cast<double2*>(base)[t] = make_double2(v.l, v.r);
 }
+// Derived rings use a split layout [even columns | odd columns] (NTC doubles each) so that
+// the theta neighbours of a pair are contiguous across lanes (2 wavefronts, no conflicts).
+__device__ __forceinline__ void rst(double* base, int t, int ntc, D2 v) { base[t] = v.l; base[ntc + t] = v.r; }
+__device__ __forceinline__ D2 rld(const double* base, int t, int ntc) { return {base[t], base[ntc + t]}; }
+__device__ __forceinline__ double rleft(const double* base, int t, int ntc) { return base[ntc + t - 1]; }
+__device__ __forceinline__ double rright(const double* base, int t) { return base[t + 1]; }
 __device__ __forceinline__ void stg2(double* p, D2 v) {   // 16-byte global store (pairs are aligned)
   *reinterpret_cast<double2*>(p) = make_double2(v.l, v.r);
 }
@@ -303,48 +309,49 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
         const D2 AP0 = ld2(c0, tl);
         const D2 AE0 = ld2(c0 + NL, tl);
         const D2 AN1 = ld2(c1 + 2 * NL, tl);
-        const D2 w1 = ld2(w_1, tl);
+        const D2 w1 = rld(w_1, tl, NTC);
         const D2 iD0{fast_rcp(AP0.l), fast_rcp(AP0.r)};
         const D2 oD0{omega * iD0.l, omega * iD0.r};
         D2 w0;
         if constexpr (PC == SPC_NONE) w0 = r0; else w0 = {r0.l * iD0.l, r0.r * iD0.r};
-        st2(w_0, tl, w0);
+        rst(w_0, tl, NTC, w0);
         compute_bar(NCT);                                     // barrier 1: w(jl) complete
 
         // ---- (B) v1(jl) = w - (omega/D) sum_L A w  (Eq. 3.5);  (C) z(jl-1), pd(jl-1)
         D2 z1;
         if constexpr (PC == SPC_ASSOR2) {
-          const double w0m = w_0[im], ae0m = c0[NL + im];
-          const D2 v11 = ld2(v_1, tl);
-          const double v1p = v_1[ip];
+          const double w0m = rleft(w_0, tl, NTC), ae0m = c0[NL + im];
+          const D2 v11 = rld(v_1, tl, NTC);
+          const double v1p = rright(v_1, tl);
           const D2 AEm1 = ld2(c1 + NL, tl);
           // plain pair: L = {W, S}, U = {E, N}
           D2 sL{AN1.l * w1.l + ae0m * w0m, AN1.r * w1.r + AE0.l * w0.l};
           if (seamL) sL.l -= ae0m * w0m;                          // column 0: W is the wrap (in U)
-          if (seamR) sL.r += AE0.r * w_0[ip];                     // column nt-1: E-wrap is in L
+          if (seamR) sL.r += AE0.r * rright(w_0, tl);             // column nt-1: E-wrap is in L
           const D2 v10{w0.l - oD0.l * sL.l, w0.r - oD0.r * sL.r};
-          st2(v_0, tl, v10);
+          rst(v_0, tl, NTC, v10);
           D2 sU{AN1.l * v10.l + AEm1.l * v11.r, AN1.r * v10.r + AEm1.r * v1p};
-          if (seamL) sU.l += c1[NL + im] * v_1[im];               // column 0: W-wrap
+          if (seamL) sU.l += c1[NL + im] * rleft(v_1, tl, NTC);   // column 0: W-wrap
           if (seamR) sU.r -= AEm1.r * v1p;                        // column nt-1: no E in U
           z1 = {c2 * (v11.l - oD1.l * sU.l), c2 * (v11.r - oD1.r * sU.r)};
         } else {
           z1 = w1;                                            // D^-1 r (Jacobi) or r (none)
         }
         const D2 pd1 = USE_PD ? D2{z1.l + beta * pdo1.l, z1.r + beta * pdo1.r} : z1;   // step 9
-        st2(p_1, tl, pd1);
+        rst(p_1, tl, NTC, pd1);
         if (out && jl - 1 >= j0 && jl - 1 < j1)
           stg2(pdout + (long long)(jl - 1) * nt + gl, ITER ? pd1 : D2{0, 0});   // INIT: pd_{-1} = 0
         // ---- (D) s(jl-2) = A pd, r_{i+1} = r_i - alpha s, x, w2 = D^-1 r_{i+1}
         D2 rn2;
+        const D2 AEm2 = ld2(c2r + NL, tl);
+        const D2 AN3 = ld2(c3 + 2 * NL, tl);
+        const double ae2m = c2r[NL + im];
         {
           const D2 AP2 = ld2(c2r, tl);
-          const D2 AEm2 = ld2(c2r + NL, tl);
           const D2 AN2 = ld2(c2r + 2 * NL, tl);
-          const D2 AN3 = ld2(c3 + 2 * NL, tl);
-          D2 sv{AP2.l * pd2.l + c2r[NL + im] * p_2[im], AP2.r * pd2.r + AEm2.l * pd2.l};
+          D2 sv{AP2.l * pd2.l + ae2m * rleft(p_2, tl, NTC), AP2.r * pd2.r + AEm2.l * pd2.l};
           sv.l += AEm2.l * pd2.r + AN3.l * pd3.l + AN2.l * pd1.l;
-          sv.r += AEm2.r * p_2[ip] + AN3.r * pd3.r + AN2.r * pd1.r;
+          sv.r += AEm2.r * rright(p_2, tl) + AN3.r * pd3.r + AN2.r * pd1.r;
           rn2 = {r2.l - alpha * sv.l, r2.r - alpha * sv.r};  // step 5 (INIT: alpha = 0)
         }
         if (out && jl - 2 >= j0 && jl - 2 < j1) {
@@ -359,42 +366,39 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
         D2 wz;
         if constexpr (PC == SPC_NONE) wz = rn2;
         else wz = {(rn2.l * oD2.l) * romega, (rn2.r * oD2.r) * romega};
-        st2(w2_2, tl, wz);
+        rst(w2_2, tl, NTC, wz);
         compute_bar(NCT);                                     // barrier 2: w2(jl-2) complete
 
         // ---- (E) v2(jl-2)   (F) z2(jl-3), gamma   (G) A z2 at jl-4, delta
         D2 u2_3;
-        const D2 AN3 = ld2(c3 + 2 * NL, tl);
         if constexpr (PC == SPC_ASSOR2) {
-          const D2 AEm2 = ld2(c2r + NL, tl);
-          const double ae2m = c2r[NL + im];
-          const D2 w23 = ld2(w2_3, tl);
-          const double wz2m = w2_2[im];
-          const D2 v23 = ld2(v2_3, tl);
-          const double v23p = v2_3[ip];
+          const D2 w23 = rld(w2_3, tl, NTC);
+          const double wz2m = rleft(w2_2, tl, NTC);
+          const D2 v23 = rld(v2_3, tl, NTC);
+          const double v23p = rright(v2_3, tl);
           const D2 AEm3 = ld2(c3 + NL, tl);
           D2 sL{AN3.l * w23.l + ae2m * wz2m, AN3.r * w23.r + AEm2.l * wz.l};
           if (seamL) sL.l -= ae2m * wz2m;
-          if (seamR) sL.r += AEm2.r * w2_2[ip];
+          if (seamR) sL.r += AEm2.r * rright(w2_2, tl);
           const D2 v22{wz.l - oD2.l * sL.l, wz.r - oD2.r * sL.r};
-          st2(v2_2, tl, v22);
+          rst(v2_2, tl, NTC, v22);
           D2 sU{AN3.l * v22.l + AEm3.l * v23.r, AN3.r * v22.r + AEm3.r * v23p};
-          if (seamL) sU.l += c3[NL + im] * v2_3[im];
+          if (seamL) sU.l += c3[NL + im] * rleft(v2_3, tl, NTC);
           if (seamR) sU.r -= AEm3.r * v23p;
           u2_3 = {c2 * (v23.l - oD3.l * sU.l), c2 * (v23.r - oD3.r * sU.r)};
         } else {
-          u2_3 = ld2(w2_3, tl);
+          u2_3 = rld(w2_3, tl, NTC);
         }
-        st2(u2_3r, tl, u2_3);
+        rst(u2_3r, tl, NTC, u2_3);
         if (out && jl - 3 >= j0 && jl - 3 < j1) acc_g += rn3.l * u2_3.l + rn3.r * u2_3.r;   // gamma
         {
           const D2 AP4 = ld2(c4, tl);
           const D2 AEm4 = ld2(c4 + NL, tl);
           const D2 AN4 = ld2(c4 + 2 * NL, tl);
           const D2 AN5 = ld2(c5 + 2 * NL, tl);
-          D2 wv{AP4.l * u2_4.l + c4[NL + im] * u2_4r[im], AP4.r * u2_4.r + AEm4.l * u2_4.l};
+          D2 wv{AP4.l * u2_4.l + c4[NL + im] * rleft(u2_4r, tl, NTC), AP4.r * u2_4.r + AEm4.l * u2_4.l};
           wv.l += AEm4.l * u2_4.r + AN5.l * u2_5.l + AN4.l * u2_3.l;
-          wv.r += AEm4.r * u2_4r[ip] + AN5.r * u2_5.r + AN4.r * u2_3.r;
+          wv.r += AEm4.r * rright(u2_4r, tl) + AN5.r * u2_5.r + AN4.r * u2_3.r;
           if (out && jl - 4 >= j0 && jl - 4 < j1) acc_d += u2_4.l * wv.l + u2_4.r * wv.r;  // delta
         }
         __syncwarp();

@@ -1,0 +1,62 @@
+"""Host-side multi-process plumbing (torch.distributed; NCCL on GPUs, gloo on CPU tests).
+
+Round-1 multi-GPU mode: every rank analyses its own operating point --
+an independent K-condition joint system (Eq. 3.7) of one Picard step -- so the
+units shard with no data-path collective ("weak" scaling).  The only collectives are
+outside the timed data path: a barrier before/after the timed region and one all-gather
+of (device ms, wall ms, DOF*iterations) to take the max time over ranks.
+
+The synchronized convergence of a condition-sharded joint system (Eq. 3.9 across ranks)
+needs one small allreduce of the packed (gamma, delta, r.r) partials per iteration; the
+partition helpers below are what that path will use.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+def shard_range(n_units: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous block [lo, hi) of n_units for this rank; the first n_units % world ranks
+    get one extra unit.  Blocks tile [0, n_units) exactly, in rank order."""
+    if world < 1 or not 0 <= rank < world or n_units < 0:
+        raise ValueError("bad shard arguments")
+    base, extra = divmod(n_units, world)
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return lo, hi
+
+
+def operating_point_of(rank: int, base_phi_deg: float = 90.0) -> float:
+    """Shaft angle analysed by `rank` in the weak-scaling bench: rank r takes phi + r deg."""
+    return base_phi_deg + float(rank)
+
+
+@dataclass
+class Aggregate:
+    device_ms_max: float
+    wall_ms_max: float
+    dof_iters_total: float
+    per_rank: list
+
+    def rate(self) -> float:
+        """Whole-job DOF*iter/s: all ranks' work / the slowest rank's device time."""
+        return self.dof_iters_total / (self.device_ms_max * 1e-3)
+
+    def e2e_rate(self) -> float:
+        return self.dof_iters_total / (self.wall_ms_max * 1e-3)
+
+
+def aggregate(device_ms: float, wall_ms: float, dof_iters: float, group=None, device=None) -> Aggregate:
+    """All-gather the per-rank timings (max over ranks) and work (sum over ranks).
+    Works for world = 1 without an initialised process group."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([device_ms, wall_ms, dof_iters], dtype=torch.float64,
+                     device=device if device is not None else "cpu")
+    if dist.is_available() and dist.is_initialized():
+        parts = [torch.zeros_like(t) for _ in range(dist.get_world_size(group))]
+        dist.all_gather(parts, t, group=group)
+        rows = [p.cpu().tolist() for p in parts]
+    else:
+        rows = [t.cpu().tolist()]
+    return Aggregate(max(r[0] for r in rows), max(r[1] for r in rows), sum(r[2] for r in rows), rows)

@@ -168,7 +168,8 @@ def _config_obj(cfg, args):
             "texture": "short 60x10" if g.get("tex_n_theta") else "smooth",
             "dof": cfg.dof, "l2_policy": "inputs larger than L2 (151 MB per field at C3)",
             "parallelism": "1 GPU" if args.gpus == 1 else
-            f"{args.gpus} GPUs, one independent K-condition joint solve per rank (weak)"}
+            f"{args.gpus} GPUs: one joint system of {cfg.K}x{args.gpus} conditions, condition-sharded "
+            f"({cfg.K} per GPU), one NCCL allgather per PCG iteration (weak)"}
 
 
 def run_gmaf(args, cfg):
@@ -183,10 +184,25 @@ def run_gmaf(args, cfg):
     import paper_2511_06824_b200 as P
     P.lib()
     K, n = cfg.K, cfg.grid["n_theta"] * cfg.grid["n_y"]
-    # weak scaling: rank r analyses its own operating point (shaft angle shifted by r degrees)
+    # N GPUs (weak scaling, C5-style): ONE joint system of 9*N conditions -- operating point r
+    # (shaft angle 90 + r deg) and its 8 FD perturbations on rank r -- condition-sharded with one
+    # NCCL allgather of the packed dot products per iteration (synchronized convergence, Eq. 3.9)
     from paper_2511_06824_b200.dist import aggregate, operating_point_of
-    conds = cfg.conds if rank == 0 else gi.fd_conditions(gi.condition(phi_deg=operating_point_of(rank)))
-    S = P.JointSolver(cfg.grid, K, device=local)
+    if world > 1 or args.shard:
+        conds_all = np.concatenate([cfg.conds if r == 0 else
+                                    gi.fd_conditions(gi.condition(phi_deg=operating_point_of(r)))
+                                    for r in range(world)])
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            uid.copy_(torch.frombuffer(bytearray(P.gmaf_nccl_unique_id()), dtype=torch.uint8))
+        if dist:
+            dist.broadcast(uid, 0)
+        S = P.JointSolver(cfg.grid, K * world, device=local, rank=rank, world=world,
+                          nccl_uid=bytes(uid.cpu().numpy().tobytes()))
+        conds = conds_all
+    else:
+        conds = cfg.conds
+        S = P.JointSolver(cfg.grid, K, device=local)
     stream = S.stream
 
     def one_step():
@@ -218,7 +234,7 @@ def run_gmaf(args, cfg):
     kt = S.kernel_times()
     if dist:
         dist.barrier()
-    agg = aggregate(dev_ms, wall_ms, float(K * n * sum(iters)), device="cuda")
+    agg = aggregate(dev_ms, wall_ms, float(K * n * sum(iters)), device="cuda")   # K local conditions
     dev_max_ms, wall_max_ms, total_dof_iters = agg.device_ms_max, agg.wall_ms_max, agg.dof_iters_total
     value = agg.rate()
     e2e_value = agg.e2e_rate()
@@ -280,6 +296,8 @@ def main():
     ap.add_argument("--impl", default="gmaf", choices=["gmaf", "reference"])
     ap.add_argument("--ref-iters", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="use the condition-sharded NCCL path even on one GPU (1-rank communicator)")
     args = ap.parse_args()
     cfg = gi.config(args.config)
     if args.impl == "reference":

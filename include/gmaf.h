@@ -87,9 +87,16 @@ typedef struct {
   double p_in, p_out;            /* Dirichlet pressures at y = 0 and y = L_F, Pa */
 } gmaf_condition;
 
-/* Multi-GPU description.  world == 1 needs no NCCL.  world > 1: conditions are
- * sharded in contiguous blocks over ranks; nccl_unique_id points at the 128-byte
- * ncclUniqueId broadcast by the caller (e.g. over torch.distributed). */
+/* Multi-GPU description (condition sharding).  dist == NULL, or world == 1
+ * with nccl_unique_id == NULL: a single-rank context that needs no NCCL at all.  Otherwise
+ * the K conditions are sharded over the ranks in contiguous blocks (the first K % world ranks
+ * own one more); every rank calls every entry point with the same arguments (all K
+ * conditions to gmaf_thickness), and each solve iteration performs ONE ncclAllGather of the
+ * packed per-condition sums so that Eq. 3.9 and alpha/beta are evaluated identically on all
+ * ranks.  nccl_unique_id points at the 128-byte ncclUniqueId made by gmaf_nccl_unique_id on
+ * rank 0 and broadcast by the caller (e.g. over torch.distributed); gmaf_create is then a
+ * collective call.  Requires world <= K and the single-pass schedule (even n_theta >= 12).
+ * gmaf_get / gmaf_field_ptr accept only this rank's conditions; gmaf_integrate returns all K. */
 typedef struct {
   int32_t rank, world;
   const void* nccl_unique_id;
@@ -176,6 +183,9 @@ gmaf_status gmaf_solve_fixed(gmaf_ctx* ctx, double omega, int32_t precond, int32
 /* Choose the iteration schedule for subsequent solves (GMAF_SCHEDULE_*).  SINGLE with an
  * odd n_theta returns INVALID_ARG. */
 gmaf_status gmaf_set_schedule(gmaf_ctx* ctx, int32_t schedule);
+
+/* Make a new ncclUniqueId (128 bytes) into out (NCCL is loaded at run time).  Errors: NCCL. */
+gmaf_status gmaf_nccl_unique_id(void* out);
 
 const char* gmaf_last_error(const gmaf_ctx* ctx);
 const char* gmaf_version(void);

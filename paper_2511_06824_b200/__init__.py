@@ -95,12 +95,14 @@ def lib() -> C.CDLL:
         L.gmaf_kernel_times.argtypes = [P, C.POINTER(gmaf_kernel_timing), C.c_int32, C.POINTER(C.c_int32)]
         L.gmaf_reset_kernel_times.argtypes = [P]
         L.gmaf_set_schedule.argtypes = [P, C.c_int32]
+        L.gmaf_nccl_unique_id.argtypes = [P]
         L.gmaf_last_error.restype = C.c_char_p
         L.gmaf_last_error.argtypes = [P]
         L.gmaf_version.restype = C.c_char_p
         for name in ("gmaf_create", "gmaf_destroy", "gmaf_thickness", "gmaf_assemble", "gmaf_solve",
                      "gmaf_solve_fixed", "gmaf_integrate", "gmaf_get", "gmaf_field_ptr",
-                     "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_set_schedule"):
+                     "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_set_schedule",
+                     "gmaf_nccl_unique_id"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -108,8 +110,8 @@ def lib() -> C.CDLL:
 
 ABI_SYMBOLS = ("gmaf_workspace_bytes", "gmaf_create", "gmaf_destroy", "gmaf_thickness", "gmaf_assemble",
                "gmaf_solve", "gmaf_solve_fixed", "gmaf_integrate", "gmaf_get", "gmaf_field_ptr",
-               "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_set_schedule", "gmaf_last_error",
-               "gmaf_version")
+               "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_set_schedule", "gmaf_nccl_unique_id",
+               "gmaf_last_error", "gmaf_version")
 SCHEDULE = {"table1": 0, "single": 1}
 
 
@@ -138,14 +140,29 @@ def _check(ctx, code: int):
 
 # ---- ABI-named thin wrappers ------------------------------------------------------------
 
-def gmaf_workspace_bytes(grid: gmaf_grid, K: int) -> int:
-    return int(lib().gmaf_workspace_bytes(C.byref(grid), int(K), None))
+def gmaf_nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (make it on rank 0, broadcast it to the others)."""
+    buf = (C.c_char * 128)()
+    _check(None, lib().gmaf_nccl_unique_id(buf))
+    return bytes(buf)
 
 
-def gmaf_create(grid: gmaf_grid, K: int, d_workspace: int, ws_bytes: int, stream: int) -> C.c_void_p:
+def make_dist(rank: int, world: int, uid: bytes | None):
+    if uid is None:
+        return None, None
+    keep = C.create_string_buffer(uid, 128)
+    return gmaf_dist(int(rank), int(world), C.cast(keep, C.c_void_p), 0), keep
+
+
+def gmaf_workspace_bytes(grid: gmaf_grid, K: int, dist: gmaf_dist | None = None) -> int:
+    return int(lib().gmaf_workspace_bytes(C.byref(grid), int(K), C.byref(dist) if dist else None))
+
+
+def gmaf_create(grid: gmaf_grid, K: int, d_workspace: int, ws_bytes: int, stream: int,
+                dist: gmaf_dist | None = None) -> C.c_void_p:
     ctx = C.c_void_p()
-    _check(None, lib().gmaf_create(C.byref(grid), int(K), None, C.c_void_p(d_workspace), ws_bytes,
-                                   C.c_void_p(stream), C.byref(ctx)))
+    _check(None, lib().gmaf_create(C.byref(grid), int(K), C.byref(dist) if dist else None,
+                                   C.c_void_p(d_workspace), ws_bytes, C.c_void_p(stream), C.byref(ctx)))
     return ctx
 
 
@@ -190,7 +207,10 @@ class SolveStats:
 class JointSolver:
     """One context: K working conditions on one mesh (Eq. 3.7 joint system)."""
 
-    def __init__(self, grid: dict, K: int, device: int | str = 0, stream=None):
+    def __init__(self, grid: dict, K: int, device: int | str = 0, stream=None, rank: int = 0,
+                 world: int = 1, nccl_uid: bytes | None = None):
+        """K = total conditions.  With nccl_uid the K conditions are sharded over `world` ranks
+        (condition sharding with one allgather per iteration, include/gmaf.h gmaf_dist)."""
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("JointSolver needs a CUDA device (no CPU fallback)")
@@ -200,14 +220,16 @@ class JointSolver:
         self.grid = make_grid(grid)
         self.K = int(K)
         self.n_theta, self.n_y = int(grid["n_theta"]), int(grid["n_y"])
-        nbytes = gmaf_workspace_bytes(self.grid, self.K)
+        self.dist, self._uid_buf = make_dist(rank, world, nccl_uid)
+        nbytes = gmaf_workspace_bytes(self.grid, self.K, self.dist)
         if nbytes == 0:
             raise GmafError(-1, "invalid grid for workspace sizing")
         with torch.cuda.device(self.device):
             self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
             # 256-byte alignment: torch's caching allocator returns >= 512-byte aligned blocks
             self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
-        self.ctx = gmaf_create(self.grid, self.K, self.workspace.data_ptr(), nbytes, self.stream.cuda_stream)
+        self.ctx = gmaf_create(self.grid, self.K, self.workspace.data_ptr(), nbytes, self.stream.cuda_stream,
+                               self.dist)
 
     def close(self):
         if getattr(self, "ctx", None):

@@ -6,6 +6,8 @@
 // residual kernel; the convergence decision is taken on the device (Eq. 3.9) and the host
 // reads the statistics once, after the graph.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>   // types only: NCCL is resolved at run time (world == 1 needs no NCCL)
 
 #include <cmath>
 #include <cstdarg>
@@ -35,6 +37,44 @@ using namespace gmaf;
 
 namespace {
 
+// NCCL, loaded on demand (normally the libnccl.so.2 that torch already mapped).
+struct NcclApi {
+  bool ok = false;
+  std::string err;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) { a.err = dlerror(); return a; }
+    a.getUniqueId = reinterpret_cast<decltype(a.getUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    a.commInitRank = reinterpret_cast<decltype(a.commInitRank)>(dlsym(h, "ncclCommInitRank"));
+    a.allGather = reinterpret_cast<decltype(a.allGather)>(dlsym(h, "ncclAllGather"));
+    a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(dlsym(h, "ncclCommDestroy"));
+    a.getErrorString = reinterpret_cast<decltype(a.getErrorString)>(dlsym(h, "ncclGetErrorString"));
+    a.ok = a.getUniqueId && a.commInitRank && a.allGather && a.commDestroy && a.getErrorString;
+    if (!a.ok) a.err = "libnccl.so.2 lacks a required symbol";
+    return a;
+  }();
+  return api;
+}
+
+// Contiguous condition blocks: rank r owns [lo, hi); the first K % world ranks one more.
+void shard(int K, int world, int rank, int* lo, int* hi) {
+  const int base = K / world, extra = K % world;
+  *lo = rank * base + (rank < extra ? rank : extra);
+  *hi = *lo + base + (rank < extra ? 1 : 0);
+}
+
+bool dist_mode(const gmaf_dist* dist) { return dist && (dist->world > 1 || dist->nccl_unique_id != nullptr); }
+
 constexpr int kUnroll = 4;          // (A, B) pairs per WHILE-body execution (must be even)
 static_assert(kUnroll % 2 == 0, "ping-pong parity");
 constexpr size_t kAlign = 256;
@@ -55,7 +95,7 @@ struct Layout {
   size_t off_ct, off_st, off_cth, off_sth, off_cp, off_AP, off_AE, off_AN, off_S, off_p, off_r, off_r2,
       off_u, off_u2,
       off_scratch, off_constrows, off_part, off_wpart, off_wrench, off_state, off_cs, off_counters, off_timing,
-      off_guard, off_matrep, total;
+      off_guard, off_matrep, off_plocal, off_pall, off_wall, total;
 };
 
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
@@ -100,7 +140,7 @@ int check_grid(const gmaf_grid* g) {
   return GMAF_OK;
 }
 
-Layout make_layout(const gmaf_grid* g, int K) {
+Layout make_layout(const gmaf_grid* g, int K, int world = 0, int kmax = 0) {
   Layout L{};
   const size_t nt = (size_t)g->n_theta, ny = (size_t)g->n_y, n = nt * ny;
   size_t o = 0;
@@ -115,7 +155,10 @@ Layout make_layout(const gmaf_grid* g, int K) {
   L.off_constrows = take((size_t)2 * kConstRowLen * 8);   // a zero row and a one row (TMA sources)
   L.off_part = take((size_t)4 * K * kMaxTilesPerCondition * 8);
   L.off_wpart = take((size_t)(148 * 8 + K) * 12 * 8);
-  L.off_wrench = take((size_t)K * 12 * 8);
+  L.off_wrench = take((size_t)(K > kmax ? K : kmax) * 12 * 8);
+  L.off_plocal = take((size_t)4 * (kmax > 0 ? kmax : 1) * 8);
+  L.off_pall = take((size_t)4 * (world > 0 ? world : 1) * (kmax > 0 ? kmax : 1) * 8);
+  L.off_wall = take((size_t)12 * (world > 0 ? world : 1) * (kmax > 0 ? kmax : 1) * 8);
   L.off_state = take(sizeof(SolverState));
   L.off_cs = take((size_t)7 * K * 8);
   L.off_counters = take(16 * sizeof(unsigned int));
@@ -158,6 +201,14 @@ struct gmaf_ctx {
   int quad_ctas = 0;
   int r_parity = 0;   // which ping-pong buffer holds the latest residual
   bool stream_mode = false;  // GMAF_LAUNCH_MODE=stream: no CUDA graph (for ncu)
+  // multi-rank (condition sharding): this rank owns global conditions [kofs, kofs + K)
+  bool distm = false;
+  int world = 1, rank = 0, kofs = 0, Kglob = 0, kmax = 0;
+  ncclComm_t comm = nullptr;
+  double* h_packed = nullptr;   // [world][4][kmax]
+  double* h_wall = nullptr;     // [world][kmax][12]
+  cudaEvent_t evb[2] = {nullptr, nullptr};
+  int* h_done = nullptr;        // [2]
 };
 
 namespace {
@@ -296,6 +347,87 @@ gmaf_status build_graph(gmaf_ctx* ctx, const GraphKey& key, cudaGraphExec_t* out
   return GMAF_OK;
 }
 
+#define NC(call)                                                                              \
+  do {                                                                                        \
+    ncclResult_t r_ = (call);                                                                 \
+    if (r_ != ncclSuccess)                                                                    \
+      return fail(ctx, GMAF_E_NCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call,                \
+                  nccl_api().getErrorString(r_));                                             \
+  } while (0)
+
+// Multi-rank solve (condition sharding): every iteration = the single-pass
+// kernel on the local conditions, ONE allgather of the packed per-condition sums
+// (gamma_k, delta_k, r.r_k, S.S_k; 4 x kmax doubles per rank), and a one-CTA scalar kernel
+// that evaluates Eq. 3.9 and alpha/beta in global condition order -- bitwise the same on
+// every rank.  Iterations are enqueued in batches with one batch in flight; the host reads
+// the device done flag of the previous batch (kernels after convergence are no-ops).
+gmaf_status run_solve_dist(gmaf_ctx* ctx, int precond, int warm, gmaf_solve_stats* out, double* cond_rel) {
+  NcclApi& N = nccl_api();
+  const int K = ctx->K, km = ctx->kmax, W = ctx->world;
+  const DevPtrs& d = ctx->d;
+  cudaStream_t s = ctx->stream;
+  SolverState* hs = ctx->h_state;
+  CU(cudaMemcpyAsync(d.st_, hs, sizeof(SolverState), cudaMemcpyHostToDevice, s));
+  CU(cudaEventRecord(ctx->ev0, s));
+  if (warm) CU(launch_residual_init(ctx->gp, d, ctx->tiles, K, 1, s));
+  CU(launch_sr_init(ctx->gp, d, ctx->tiles_sr, K, precond, warm != 0, 0ull, s));
+  NC(N.allGather(d.dist.packed_local, d.dist.packed_all, (size_t)4 * km, ncclDouble, ctx->comm, s));
+  CU(launch_sr_scalar(d, true, ctx->Kglob, K, ctx->kofs, W, s));
+  double* h_init = ctx->h_packed + (size_t)4 * km * W;   // S.S_k of every condition (init sums)
+  CU(cudaMemcpyAsync(h_init, d.dist.packed_all, (size_t)4 * km * W * 8, cudaMemcpyDeviceToHost, s));
+  constexpr int kBatch = 8;   // even: iteration parity = position in the batch
+  for (int b = 0;; ++b) {
+    for (int u = 0; u < kBatch; ++u) {
+      CU(launch_sr_iter(ctx->gp, d, ctx->tiles_sr, K, precond, u & 1, 0ull, s));
+      NC(N.allGather(d.dist.packed_local, d.dist.packed_all, (size_t)4 * km, ncclDouble, ctx->comm, s));
+      CU(launch_sr_scalar(d, false, ctx->Kglob, K, ctx->kofs, W, s));
+    }
+    CU(cudaMemcpyAsync(&ctx->h_done[b & 1], &d.st_->done, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CU(cudaEventRecord(ctx->evb[b & 1], s));
+    if (b >= 1) {
+      CU(cudaEventSynchronize(ctx->evb[(b - 1) & 1]));
+      if (ctx->h_done[(b - 1) & 1]) break;
+    }
+  }
+  CU(cudaMemcpyAsync(ctx->h_packed, d.dist.packed_all, (size_t)4 * km * W * 8, cudaMemcpyDeviceToHost, s));
+  CU(launch_sr_fixup(ctx->gp, d, K, s));
+  CU(launch_true_residual(ctx->gp, d, ctx->tiles, K, s));
+  NC(N.allGather(d.dist.packed_local, d.dist.packed_all, (size_t)km, ncclDouble, ctx->comm, s));
+  CU(launch_true_scalar(d, W, s));
+  CU(cudaEventRecord(ctx->ev1, s));
+  CU(cudaMemcpyAsync(hs, d.st_, sizeof(SolverState), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+  if (hs->zero_p) {
+    CU(cudaMemsetAsync(d.p, 0, (size_t)K * ctx->grid.n_theta * ctx->grid.n_y * 8, s));
+    CU(cudaStreamSynchronize(s));
+  }
+  if (cond_rel) {
+    for (int r = 0; r < W; ++r) {
+      int lo, hi;
+      shard(ctx->Kglob, W, r, &lo, &hi);
+      for (int kl = 0; kl < hi - lo; ++kl) {
+        const double rr = ctx->h_packed[(size_t)r * 4 * km + kl], ss = h_init[(size_t)r * 4 * km + 3 * km + kl];
+        cond_rel[lo + kl] = ss > 0.0 ? std::sqrt(rr) / std::sqrt(ss) : 0.0;
+      }
+    }
+  }
+  if (out) {
+    out->iterations = hs->iter; out->converged = hs->converged; out->status = hs->status;
+    out->precond = precond; out->schedule = GMAF_SCHEDULE_SINGLE; out->rel_residual = hs->rel;
+    out->true_rel_residual = hs->true_rel; out->solve_ms = ms;
+  }
+  ctx->r_parity = hs->iter & 1;
+  ctx->state = ST_SOLVED;
+  if (hs->status == GMAF_E_BREAKDOWN)
+    return fail(ctx, GMAF_E_BREAKDOWN, "solve: breakdown at iteration %d", hs->iter);
+  if (hs->status == GMAF_E_NO_CONVERGENCE)
+    return fail(ctx, GMAF_E_NO_CONVERGENCE, "solve: no convergence after %d iterations (rel %.3e)", hs->iter,
+                hs->rel);
+  return GMAF_OK;
+}
+
 gmaf_status run_solve(gmaf_ctx* ctx, double tol, double omega, int precond, int coupling, int max_iter,
                       int warm, int fixed_iters, gmaf_solve_stats* out, double* cond_rel) {
   SolverState* hs = ctx->h_state;
@@ -305,6 +437,7 @@ gmaf_status run_solve(gmaf_ctx* ctx, double tol, double omega, int precond, int 
   hs->coupling = coupling;
   hs->max_iter = max_iter;
   hs->fixed_iters = fixed_iters;
+  if (ctx->distm) return run_solve_dist(ctx, precond, warm, out, cond_rel);
   const GraphKey key{ctx->schedule, precond, warm ? 1 : 0, fixed_iters > 0 ? 1 : 0};
   CU(cudaMemcpyAsync(ctx->d.st_, hs, sizeof(SolverState), cudaMemcpyHostToDevice, ctx->stream));
   if (ctx->stream_mode) {
@@ -372,6 +505,12 @@ const char* gmaf_version(void) { return "gmaf-b200 0.1 (sm_100a)"; }
 size_t gmaf_workspace_bytes(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist) {
   if (check_grid(grid) != GMAF_OK || K < 1) return 0;
   if (dist && (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)) return 0;
+  if (dist_mode(dist)) {
+    if (dist->world > K) return 0;
+    int lo, hi;
+    shard(K, dist->world, dist->rank, &lo, &hi);
+    return make_layout(grid, hi - lo, dist->world, (K + dist->world - 1) / dist->world).total;
+  }
   return make_layout(grid, K).total;
 }
 
@@ -382,14 +521,32 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
   int rc = check_grid(grid);
   if (rc != GMAF_OK) return (gmaf_status)rc;
   if (K < 1) return GMAF_E_INVALID_ARG;
-  if (dist && dist->world != 1) return GMAF_E_INVALID_ARG;  // multi-rank: see gmaf_dist in DESIGN.md
-  const Layout L = make_layout(grid, K);
+  if (dist && (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)) return GMAF_E_INVALID_ARG;
+  const bool dm = dist_mode(dist);
+  int klo = 0, khi = K, world = 1, kmax = 0;
+  if (dm) {
+    // condition sharding needs the single-pass schedule, >= 1 condition per rank and an id
+    if (!dist->nccl_unique_id || dist->world > K || grid->n_theta % 2 != 0 || grid->n_theta < 12)
+      return GMAF_E_INVALID_ARG;
+    world = dist->world;
+    shard(K, world, dist->rank, &klo, &khi);
+    kmax = (K + world - 1) / world;
+  }
+  const int Kglob = K;
+  K = khi - klo;   // from here on: the local conditions
+  const Layout L = dm ? make_layout(grid, K, world, kmax) : make_layout(grid, K);
   if (!d_workspace || ws_bytes < L.total || (reinterpret_cast<uintptr_t>(d_workspace) % kAlign) != 0)
     return GMAF_E_WORKSPACE;
   gmaf_ctx* ctx = new (std::nothrow) gmaf_ctx();
   if (!ctx) return GMAF_E_INVALID_ARG;
   ctx->grid = *grid;
   ctx->K = K;
+  ctx->Kglob = Kglob;
+  ctx->distm = dm;
+  ctx->world = world;
+  ctx->rank = dm ? dist->rank : 0;
+  ctx->kofs = klo;
+  ctx->kmax = kmax;
   ctx->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
   ctx->ws = reinterpret_cast<char*>(d_workspace);
   ctx->ws_bytes = ws_bytes;
@@ -423,6 +580,12 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
   d.timing = at<Timing>(ctx, L.off_timing);
   d.guard = at<unsigned long long>(ctx, L.off_guard);
   d.mat_rep = at<int32_t>(ctx, L.off_matrep);
+  d.dist.world = dm ? world : 0;
+  d.dist.rank = ctx->rank;
+  d.dist.kofs = klo;
+  d.dist.kmax_local = kmax;
+  d.dist.packed_local = at<double>(ctx, L.off_plocal);
+  d.dist.packed_all = at<double>(ctx, L.off_pall);
 
   auto cleanup_fail = [&](gmaf_status s) { gmaf_destroy(ctx); return s; };
   if (cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -482,6 +645,22 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
   }
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
   ctx->quad_ctas = quad_ctas_per_condition(gp, K);
+  if (dm) {
+    NcclApi& N = nccl_api();
+    if (!N.ok) { gmaf_status e = fail(ctx, GMAF_E_NCCL, "NCCL unavailable: %s", N.err.c_str()); gmaf_destroy(ctx); return e; }
+    if (cudaMallocHost((void**)&ctx->h_packed, (size_t)2 * 4 * kmax * world * 8) != cudaSuccess ||
+        cudaMallocHost((void**)&ctx->h_wall, (size_t)12 * kmax * world * 8) != cudaSuccess ||
+        cudaMallocHost((void**)&ctx->h_done, 2 * sizeof(int)) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->evb[0], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->evb[1], cudaEventDisableTiming) != cudaSuccess)
+      return cleanup_fail(GMAF_E_CUDA);
+    ncclUniqueId uid;
+    std::memcpy(&uid, dist->nccl_unique_id, sizeof(uid));
+    if (N.commInitRank(&ctx->comm, world, uid, ctx->rank) != ncclSuccess) {
+      ctx->comm = nullptr;
+      return cleanup_fail(GMAF_E_NCCL);
+    }
+  }
   const char* lm = std::getenv("GMAF_LAUNCH_MODE");
   ctx->stream_mode = lm && std::strcmp(lm, "stream") == 0;
   *out = ctx;
@@ -490,6 +669,11 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
 
 gmaf_status gmaf_destroy(gmaf_ctx* ctx) {
   if (!ctx) return GMAF_E_INVALID_ARG;
+  if (ctx->comm) nccl_api().commDestroy(ctx->comm);
+  if (ctx->h_packed) cudaFreeHost(ctx->h_packed);
+  if (ctx->h_wall) cudaFreeHost(ctx->h_wall);
+  if (ctx->h_done) cudaFreeHost(ctx->h_done);
+  for (int q = 0; q < 2; ++q) if (ctx->evb[q]) cudaEventDestroy(ctx->evb[q]);
   for (auto& kv : ctx->graphs) {
     if (kv.second.second) cudaGraphExecDestroy(kv.second.second);
     if (kv.second.first) cudaGraphDestroy(kv.second.first);
@@ -507,8 +691,9 @@ gmaf_status gmaf_destroy(gmaf_ctx* ctx) {
   return GMAF_OK;
 }
 
-gmaf_status gmaf_thickness(gmaf_ctx* ctx, const gmaf_condition* conds) {
-  if (!ctx || !conds) return GMAF_E_INVALID_ARG;
+gmaf_status gmaf_thickness(gmaf_ctx* ctx, const gmaf_condition* conds_all) {
+  if (!ctx || !conds_all) return GMAF_E_INVALID_ARG;
+  const gmaf_condition* conds = conds_all + ctx->kofs;   // this rank's block (all K on every rank)
   const int K = ctx->K;
   ctx->mat_of.assign(K, 0);
   ctx->mat_rep.clear();
@@ -575,14 +760,29 @@ gmaf_status gmaf_integrate(gmaf_ctx* ctx, double* wrench) {
   if (!ctx || !wrench) return GMAF_E_INVALID_ARG;
   if (ctx->state < ST_SOLVED) return fail(ctx, GMAF_E_STATE, "integrate before solve");
   CU(launch_quadrature(ctx->gp, ctx->d, ctx->K, ctx->stream, nullptr));
+  if (ctx->distm) {   // every rank returns all K wrenches (allgather of the padded blocks)
+    const int km = ctx->kmax;
+    double* wall = reinterpret_cast<double*>(ctx->ws + ctx->L.off_wall);
+    NC(nccl_api().allGather(ctx->d.wrench, wall, (size_t)12 * km, ncclDouble, ctx->comm, ctx->stream));
+    CU(cudaMemcpyAsync(ctx->h_wall, wall, (size_t)12 * km * ctx->world * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (int r = 0; r < ctx->world; ++r) {
+      int lo, hi;
+      shard(ctx->Kglob, ctx->world, r, &lo, &hi);
+      std::memcpy(wrench + (size_t)lo * 12, ctx->h_wall + (size_t)r * 12 * km, (size_t)(hi - lo) * 12 * 8);
+    }
+    return GMAF_OK;
+  }
   CU(cudaMemcpyAsync(ctx->h_wrench, ctx->d.wrench, (size_t)ctx->K * 12 * 8, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   std::memcpy(wrench, ctx->h_wrench, (size_t)ctx->K * 12 * 8);
   return GMAF_OK;
 }
 
-gmaf_status gmaf_field_ptr(gmaf_ctx* ctx, int32_t field, int32_t k, void** dptr) {
-  if (!ctx || !dptr || k < 0 || k >= ctx->K) return GMAF_E_INVALID_ARG;
+gmaf_status gmaf_field_ptr(gmaf_ctx* ctx, int32_t field, int32_t kglob, void** dptr) {
+  if (!ctx || !dptr) return GMAF_E_INVALID_ARG;
+  const int32_t k = kglob - ctx->kofs;   // fields of this rank's conditions only
+  if (k < 0 || k >= ctx->K) return fail(ctx, GMAF_E_INVALID_ARG, "condition %d is not on this rank", kglob);
   const size_t n = (size_t)ctx->grid.n_theta * ctx->grid.n_y;
   const size_t m = ctx->mat_of.empty() ? 0 : (size_t)ctx->mat_of[k];
   switch (field) {
@@ -597,8 +797,10 @@ gmaf_status gmaf_field_ptr(gmaf_ctx* ctx, int32_t field, int32_t k, void** dptr)
   return GMAF_OK;
 }
 
-gmaf_status gmaf_get(gmaf_ctx* ctx, int32_t field, int32_t k, double* host_out) {
-  if (!ctx || !host_out || k < 0 || k >= ctx->K) return GMAF_E_INVALID_ARG;
+gmaf_status gmaf_get(gmaf_ctx* ctx, int32_t field, int32_t kglob, double* host_out) {
+  if (!ctx || !host_out) return GMAF_E_INVALID_ARG;
+  const int32_t k = kglob - ctx->kofs;
+  if (k < 0 || k >= ctx->K) return fail(ctx, GMAF_E_INVALID_ARG, "condition %d is not on this rank", kglob);
   const size_t n = (size_t)ctx->grid.n_theta * ctx->grid.n_y;
   if (field == GMAF_FIELD_H || field == GMAF_FIELD_HDOT) {
     if (ctx->state < ST_THICK) return fail(ctx, GMAF_E_STATE, "get H before thickness");
@@ -612,7 +814,7 @@ gmaf_status gmaf_get(gmaf_ctx* ctx, int32_t field, int32_t k, double* host_out) 
       ctx->state < ST_ASSEMBLED)
     return fail(ctx, GMAF_E_STATE, "get bands before assemble");
   void* src = nullptr;
-  gmaf_status s = gmaf_field_ptr(ctx, field, k, &src);
+  gmaf_status s = gmaf_field_ptr(ctx, field, kglob, &src);
   if (s != GMAF_OK) return s;
   CU(cudaMemcpyAsync(host_out, src, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
@@ -662,9 +864,21 @@ gmaf_status gmaf_reset_kernel_times(gmaf_ctx* ctx) {
 
 gmaf_status gmaf_set_schedule(gmaf_ctx* ctx, int32_t schedule) {
   if (!ctx) return GMAF_E_INVALID_ARG;
+  if (ctx->distm && schedule != GMAF_SCHEDULE_SINGLE)
+    return fail(ctx, GMAF_E_INVALID_ARG, "set_schedule: multi-rank contexts run the single-pass schedule");
   if (schedule == GMAF_SCHEDULE_TABLE1) { ctx->schedule = schedule; return GMAF_OK; }
   if (schedule == GMAF_SCHEDULE_SINGLE && single_ok(ctx->grid.n_theta)) { ctx->schedule = schedule; return GMAF_OK; }
   return fail(ctx, GMAF_E_INVALID_ARG, "set_schedule: %d not available (n_theta %d)", schedule, ctx->grid.n_theta);
+}
+
+gmaf_status gmaf_nccl_unique_id(void* out) {
+  if (!out) return GMAF_E_INVALID_ARG;
+  NcclApi& N = nccl_api();
+  if (!N.ok) return GMAF_E_NCCL;
+  ncclUniqueId uid;
+  if (N.getUniqueId(&uid) != ncclSuccess) return GMAF_E_NCCL;
+  std::memcpy(out, &uid, sizeof(uid));
+  return GMAF_OK;
 }
 
 const char* gmaf_last_error(const gmaf_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }

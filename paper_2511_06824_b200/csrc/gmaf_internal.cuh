@@ -64,6 +64,13 @@ struct CondScalars {
   double* ttk;     // [K] true residual^2
 };
 
+// Multi-rank state (world > 0 only when the context was created with an NCCL communicator).
+struct DistPtrs {
+  int32_t world, rank, kofs, kmax_local;   // ranks own contiguous condition blocks
+  double* packed_local;                    // [4][kmax_local] this rank's per-condition sums
+  double* packed_all;                      // [world][4][kmax_local] after the allgather
+};
+
 struct DevPtrs {
   const double* ct; const double* st;      // cos/sin(i dtheta)
   const double* cth; const double* sth;    // cos/sin((i+1/2) dtheta)
@@ -82,6 +89,7 @@ struct DevPtrs {
   Timing* timing;
   unsigned long long* guard;               // [4]: flag, k, i|j, h bits
   int32_t* mat_rep;                        // [M] representative condition of each matrix
+  DistPtrs dist;
 };
 
 // Marching-tile configuration of the PCG kernels.
@@ -116,6 +124,8 @@ cudaError_t launch_true_residual(const GridParams& g, const DevPtrs& d, const Ti
 cudaError_t launch_residual_init(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int out_parity,
                                  cudaStream_t s);
 
+cudaError_t launch_true_scalar(const DevPtrs& d, int world, cudaStream_t s);
+
 // ---- launchers (sr.cu): single-pass schedule, one kernel + one reduction per iteration ----
 constexpr int SR_HALO_COLS = 4;
 cudaError_t launch_sr_init(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,
@@ -123,6 +133,9 @@ cudaError_t launch_sr_init(const GridParams& g, const DevPtrs& d, const TileCfg&
 cudaError_t launch_sr_iter(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,
                            int parity, unsigned long long cond_handle, cudaStream_t s);
 cudaError_t launch_sr_fixup(const GridParams& g, const DevPtrs& d, int K, cudaStream_t s);
+// multi-rank: scalars from the gathered per-condition sums (one CTA)
+cudaError_t launch_sr_scalar(const DevPtrs& d, bool init, int Kglob, int Klocal, int kofs, int world,
+                             cudaStream_t s);
 cudaError_t configure_sr_kernels(const TileCfg& t);
 int sr_ctas_per_sm(const TileCfg& t);
 

@@ -317,6 +317,8 @@ k_phase_b(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long l
       if (TRUE_RES) {
         for (int k = 0; k < K; ++k) d.cs.ttk[k] = rrk[k];
         st->true_rel = (st->nS > 0.0) ? sqrt(rr) / st->nS : 0.0;
+        if (d.dist.world > 0)   // multi-rank: publish ||S_k - A_k p_k||^2; k_true_scalar sums all ranks
+          for (int k = 0; k < d.dist.kmax_local; ++k) d.dist.packed_local[k] = k < K ? rrk[k] : 0.0;
       } else if (INIT) {
         double SS = 0.0, dd = 0.0;
         for (int k = 0; k < K; ++k) {
@@ -456,6 +458,21 @@ cudaError_t launch_residual_init(const GridParams& g, const DevPtrs& d, const Ti
 cudaError_t launch_true_residual(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K,
                                  cudaStream_t s) {
   return launch_tiles(k_phase_b<PC_NONE, MODE_TRUERES>, g, d, t, K, 0, 0ull, 0, s);
+}
+
+// Multi-rank true residual: sum of every rank's ||S_k - A_k p_k||^2 in condition order.
+__global__ void k_true_scalar(DevPtrs d, int world) {
+  if (threadIdx.x != 0) return;
+  const int km = d.dist.kmax_local;
+  double rr = 0.0;
+  for (int r = 0; r < world; ++r)
+    for (int k = 0; k < km; ++k) rr += d.dist.packed_all[(long long)r * km + k];
+  d.st_->true_rel = (d.st_->nS > 0.0) ? sqrt(rr) / d.st_->nS : 0.0;
+}
+
+cudaError_t launch_true_scalar(const DevPtrs& d, int world, cudaStream_t s) {
+  k_true_scalar<<<1, 32, 0, s>>>(d, world);
+  return cudaGetLastError();
 }
 
 // Resident CTAs per SM of the dominant iteration kernel (phase B, ASSOR-II).

@@ -131,6 +131,97 @@ __host__ __device__ inline size_t sr_smem_bytes(int nl) {
          (SR_CSLOTS + SR_VSLOTS + SR_CSLOTS) * sizeof(uint64_t) + 64;
 }
 
+// Table-1 scalars from the per-condition sums (fixed k order): convergence test (Eq. 3.9),
+// alpha/beta of the single-reduction recurrence (coupled: global; lockstep: per condition).
+// red = [rr | gamma | delta | S.S] x Kall.  Local conditions kofs .. kofs+Klocal-1 receive their
+// alpha/beta in d.cs (indexed locally).  One thread.
+template <bool INIT>
+__device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, int Klocal, int kofs,
+                                int use_cond, unsigned long long hcond) {
+  SolverState* st = d.st_;
+  const double* rrk = red;
+  const double* gk = red + Kall;
+  const double* dk = red + 2 * Kall;
+  const double* ssk = red + 3 * Kall;
+  double rr = 0.0;
+  for (int kk = 0; kk < Kall; ++kk) rr += rrk[kk];
+  for (int kl = 0; kl < Klocal; ++kl) d.cs.rrk[kl] = rrk[kofs + kl];
+  bool bad = false;
+  if (INIT) {
+    double SS = 0.0;
+    for (int kk = 0; kk < Kall; ++kk) SS += ssk[kk];
+    for (int kl = 0; kl < Klocal; ++kl) d.cs.Sk[kl] = ssk[kofs + kl];
+    st->nS = sqrt(SS);
+    st->iter = 0; st->status = 0; st->converged = 0; st->done = 0; st->zero_p = 0;
+    if (st->nS == 0.0) {
+      st->rel = 0.0; st->done = 1; st->converged = 1; st->zero_p = 1;
+    } else {
+      st->rel = sqrt(rr) / st->nS;
+      if (st->fixed_iters == 0 && st->rel <= st->tol) { st->done = 1; st->converged = 1; }
+      else if (st->max_iter <= 0) { st->done = 1; st->status = -6; }
+    }
+    if (!st->done) {
+      if (st->coupling == 0) {
+        double gg = 0.0, dd = 0.0;
+        for (int kk = 0; kk < Kall; ++kk) { gg += gk[kk]; dd += dk[kk]; }
+        if (!(dd > 0.0)) bad = true;
+        const double a0 = gg / dd;
+        for (int kl = 0; kl < Klocal; ++kl) { d.cs.alpha[kl] = a0; d.cs.beta[kl] = 0.0; d.cs.uvk[kl] = 0.0; }
+        st->d = gg;
+      } else {
+        for (int kk = 0; kk < Kall; ++kk)
+          if (gk[kk] != 0.0 && !(dk[kk] > 0.0)) bad = true;
+        for (int kl = 0; kl < Klocal; ++kl) {
+          const int kk = kofs + kl;
+          d.cs.alpha[kl] = gk[kk] != 0.0 ? gk[kk] / dk[kk] : 0.0;
+          d.cs.beta[kl] = 0.0; d.cs.uvk[kl] = 0.0; d.cs.dk[kl] = gk[kk];
+        }
+      }
+      if (bad) { st->done = 1; st->status = -5; }
+    }
+  } else {
+    st->iter += 1;
+    st->rel = sqrt(rr) / st->nS;
+    for (int kl = 0; kl < Klocal; ++kl) d.cs.uvk[kl] = d.cs.alpha[kl];   // alpha used this iteration
+    if (st->fixed_iters > 0) {
+      if (st->iter >= st->fixed_iters) st->done = 1;
+    } else if (st->rel <= st->tol) {
+      st->done = 1; st->converged = 1;
+    } else if (st->iter >= st->max_iter) {
+      st->done = 1; st->status = -6;
+    }
+    if (!st->done || st->fixed_iters > 0) {
+      if (st->coupling == 0) {
+        double g2 = 0.0, d2 = 0.0;
+        for (int kk = 0; kk < Kall; ++kk) { g2 += gk[kk]; d2 += dk[kk]; }
+        const double aold = d.cs.alpha[0];
+        const double b = g2 / st->d;
+        const double den = d2 - b * g2 / aold;
+        if (!(g2 > 0.0) || !(den > 0.0)) bad = true;
+        const double a = g2 / den;
+        for (int kl = 0; kl < Klocal; ++kl) { d.cs.alpha[kl] = a; d.cs.beta[kl] = b; }
+        st->d = g2;
+      } else {
+        for (int kk = 0; kk < Kall; ++kk)
+          if (gk[kk] < 0.0) bad = true;
+        for (int kl = 0; kl < Klocal; ++kl) {
+          const int kk = kofs + kl;
+          const double aold = d.cs.alpha[kl], gold = d.cs.dk[kl];
+          double a = 0.0, b = 0.0;
+          if (gold != 0.0 && aold != 0.0) {
+            b = gk[kk] / gold;
+            const double den = dk[kk] - b * gk[kk] / aold;
+            a = (gk[kk] == 0.0) ? 0.0 : gk[kk] / den;
+          }
+          d.cs.alpha[kl] = a; d.cs.beta[kl] = b; d.cs.dk[kl] = gk[kk];
+        }
+      }
+      if (bad && !st->done) { st->done = 1; st->status = -5; }
+    }
+  }
+  if (use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, st->done ? 0u : 1u);
+}
+
 template <int PC, int MODE>
 __global__ void __launch_bounds__(192, 2)
 k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long hcond, int use_cond) {
@@ -414,7 +505,7 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
     }
   }
 
-  // ---- per-CTA partials and the scalar stage (last CTA, fixed order)
+  // ---- per-CTA partials, then the scalar stage (last CTA, fixed order)
   double* red = ringW;   // rings are dead now
   double v[4] = {acc_rr, acc_g, acc_d, acc_s};
   block_sum<4>(v, red);
@@ -425,6 +516,7 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
     for (int q = 0; q < 4; ++q) d.partials[(long long)(q * K + k) * ncta + cta] = v[q];
   }
   if (last_cta_arrive(&d.counters[ITER ? KK_SR_ITER : KK_SR_INIT], gridDim.x)) {
+    // per-condition sums in CTA order: [rr | gamma | delta | S.S] x K
     for (int q = tid; q < 4 * K; q += blockDim.x) {
       const double* srcp = d.partials + (long long)q * ncta;
       double sum = 0.0;
@@ -433,89 +525,43 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
     }
     __syncthreads();
     if (tid == 0) {
-      const double* rrk = red;
-      const double* gk = red + K;
-      const double* dk = red + 2 * K;
-      const double* ssk = red + 3 * K;
-      double rr = 0.0;
-      for (int kk = 0; kk < K; ++kk) { rr += rrk[kk]; d.cs.rrk[kk] = rrk[kk]; }
-      bool bad = false;
-      if (INIT) {
-        double SS = 0.0;
-        for (int kk = 0; kk < K; ++kk) { d.cs.Sk[kk] = ssk[kk]; SS += ssk[kk]; }
-        st->nS = sqrt(SS);
-        st->iter = 0; st->status = 0; st->converged = 0; st->done = 0; st->zero_p = 0;
-        if (st->nS == 0.0) {
-          st->rel = 0.0; st->done = 1; st->converged = 1; st->zero_p = 1;
-        } else {
-          st->rel = sqrt(rr) / st->nS;
-          if (st->fixed_iters == 0 && st->rel <= st->tol) { st->done = 1; st->converged = 1; }
-          else if (st->max_iter <= 0) { st->done = 1; st->status = -6; }
-        }
-        if (!st->done) {
-          if (st->coupling == 0) {
-            double gg = 0.0, dd = 0.0;
-            for (int kk = 0; kk < K; ++kk) { gg += gk[kk]; dd += dk[kk]; }
-            if (!(dd > 0.0)) bad = true;
-            const double a0 = gg / dd;
-            for (int kk = 0; kk < K; ++kk) { d.cs.alpha[kk] = a0; d.cs.beta[kk] = 0.0; d.cs.uvk[kk] = 0.0; }
-            st->d = gg;
-          } else {
-            for (int kk = 0; kk < K; ++kk) {
-              double a0 = 0.0;
-              if (gk[kk] != 0.0) { if (!(dk[kk] > 0.0)) bad = true; a0 = gk[kk] / dk[kk]; }
-              d.cs.alpha[kk] = a0; d.cs.beta[kk] = 0.0; d.cs.uvk[kk] = 0.0; d.cs.dk[kk] = gk[kk];
-            }
-          }
-          if (bad) { st->done = 1; st->status = -5; }
-        }
+      if (d.dist.world > 0) {
+        // multi-rank: publish this rank's per-condition sums; the allgather + k_sr_scalar
+        // that follow on the stream evaluate the scalars identically on every rank
+        const int km = d.dist.kmax_local;
+        for (int q = 0; q < 4; ++q)
+          for (int kk = 0; kk < km; ++kk) d.dist.packed_local[q * km + kk] = kk < K ? red[q * K + kk] : 0.0;
       } else {
-        st->iter += 1;
-        st->rel = sqrt(rr) / st->nS;
-        for (int kk = 0; kk < K; ++kk) d.cs.uvk[kk] = d.cs.alpha[kk];   // alpha used this iteration
-        if (st->fixed_iters > 0) {
-          if (st->iter >= st->fixed_iters) st->done = 1;
-        } else if (st->rel <= st->tol) {
-          st->done = 1; st->converged = 1;
-        } else if (st->iter >= st->max_iter) {
-          st->done = 1; st->status = -6;
-        }
-        if (!st->done || st->fixed_iters > 0) {
-          if (st->coupling == 0) {
-            double g2 = 0.0, d2 = 0.0;
-            for (int kk = 0; kk < K; ++kk) { g2 += gk[kk]; d2 += dk[kk]; }
-            const double aold = d.cs.alpha[0];
-            const double b = g2 / st->d;
-            const double den = d2 - b * g2 / aold;
-            if (!(g2 > 0.0) || !(den > 0.0)) bad = true;
-            const double a = g2 / den;
-            for (int kk = 0; kk < K; ++kk) { d.cs.alpha[kk] = a; d.cs.beta[kk] = b; }
-            st->d = g2;
-          } else {
-            for (int kk = 0; kk < K; ++kk) {
-              const double aold = d.cs.alpha[kk], gold = d.cs.dk[kk];
-              double a = 0.0, b = 0.0;
-              if (gold != 0.0 && aold != 0.0) {
-                if (gk[kk] < 0.0) bad = true;
-                b = gk[kk] / gold;
-                const double den = dk[kk] - b * gk[kk] / aold;
-                a = (gk[kk] == 0.0) ? 0.0 : gk[kk] / den;
-              }
-              d.cs.alpha[kk] = a; d.cs.beta[kk] = b; d.cs.dk[kk] = gk[kk];
-            }
-          }
-          if (bad && !st->done) { st->done = 1; st->status = -5; }
-        }
+        sr_scalar_stage<INIT>(d, red, K, K, 0, use_cond, hcond);
       }
-      if (use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, st->done ? 0u : 1u);
       timing_end(d.timing, ITER ? KK_SR_ITER : KK_SR_INIT);
     }
   }
 }
 
+// Multi-rank scalar stage: one CTA, after the allgather of every rank's packed sums
+// (rank-major = condition-major since ranks own contiguous condition blocks).
+template <bool INIT>
+__global__ void k_sr_scalar(DevPtrs d, int Kglob, int Klocal, int kofs, int world) {
+  if (!INIT && d.st_->done) return;
+  extern __shared__ double sh[];       // [4][Kglob]
+  const int km = d.dist.kmax_local;
+  for (int kg = threadIdx.x; kg < Kglob; kg += blockDim.x) {
+    // rank and local index of global condition kg (blocks: first Kglob % world ranks get one more)
+    const int base = Kglob / world, extra = Kglob % world;
+    int r, kl;
+    if (kg < extra * (base + 1)) { r = kg / (base + 1); kl = kg % (base + 1); }
+    else { r = extra + (kg - extra * (base + 1)) / base; kl = (kg - extra * (base + 1)) % base; }
+    const double* src = d.dist.packed_all + (long long)r * 4 * km;
+    for (int q = 0; q < 4; ++q) sh[q * Kglob + kg] = src[q * km + kl];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) sr_scalar_stage<INIT>(d, sh, Kglob, Klocal, kofs, 0, 0ull);
+}
+
 // x += alpha_{it-1} pd_{it-1} when the iteration count is odd (the last x update of the
 // two-at-a-time scheme is still pending).  Elementwise, reads the device iteration count.
-__global__ void k_sr_fixup(GridParams g, DevPtrs d, int K) {
+__global__ void k_sr_fixup(GridParams g, DevPtrs d, int K) {   // K = local conditions
   const int it = d.st_->iter;
   if ((it & 1) == 0) return;
   const long long n = (long long)g.nt * g.ny;
@@ -572,6 +618,14 @@ cudaError_t launch_sr_fixup(const GridParams& g, const DevPtrs& d, int K, cudaSt
   long long blocks = (work + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   k_sr_fixup<<<(int)blocks, 256, 0, s>>>(g, d, K);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sr_scalar(const DevPtrs& d, bool init, int Kglob, int Klocal, int kofs, int world,
+                             cudaStream_t s) {
+  const size_t sm = (size_t)4 * Kglob * sizeof(double);
+  if (init) k_sr_scalar<true><<<1, 128, sm, s>>>(d, Kglob, Klocal, kofs, world);
+  else k_sr_scalar<false><<<1, 128, sm, s>>>(d, Kglob, Klocal, kofs, world);
   return cudaGetLastError();
 }
 

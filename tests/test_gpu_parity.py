@@ -216,3 +216,30 @@ def test_c3_full_size(P, orc, gi):
         wo = orc.wrench(cfg.grid, cfg.conds[k], S.get("p", k))
         assert wrench_err(W[k], wo, cfg.conds[k][8]) <= 1e-6
     S.close()
+
+
+def test_nccl_condition_sharding_world1(P, orc, gi):
+    """The multi-rank path (condition sharding: local kernels + one NCCL allgather of the packed
+    per-condition sums + the scalar kernel, per iteration) on a 1-rank communicator reproduces
+    the single-rank solve bit for bit (same sums in the same condition order)."""
+    cfg = gi.config("C2")
+    g = dict(cfg.grid, n_theta=256, n_y=128)
+    conds = cfg.conds
+    uid = P.gmaf_nccl_unique_id()
+    Sd = P.JointSolver(g, 9, rank=0, world=1, nccl_uid=uid)
+    std, Wd = Sd.step(conds, omega=1.8)
+    S = P.JointSolver(g, 9)
+    st, W = S.step(conds, omega=1.8)
+    assert std.iterations == st.iterations and std.converged
+    assert std.rel_residual == st.rel_residual and std.true_rel_residual == st.true_rel_residual
+    for k in (0, 4, 8):
+        assert np.array_equal(Sd.get("p", k), S.get("p", k))
+    assert np.array_equal(Wd, W)
+    assert np.array_equal(std.cond_rel, st.cond_rel)
+    # fixed-budget iterates too
+    a = Sd.solve(tol=1e-30, omega=1.8, max_iter=7, raise_on_error=False)
+    b = S.solve(tol=1e-30, omega=1.8, max_iter=7, raise_on_error=False)
+    assert a.iterations == b.iterations == 7
+    assert np.array_equal(Sd.get("p", 3), S.get("p", 3))
+    Sd.close()
+    S.close()

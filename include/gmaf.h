@@ -56,7 +56,10 @@ typedef enum {
 
 enum { GMAF_PRECOND_NONE = 0, GMAF_PRECOND_JACOBI = 1, GMAF_PRECOND_ASSOR2 = 2 };
 enum { GMAF_COUPLED = 0,   /* one Krylov process on A_G: global alpha, beta (Eq. 3.9) */
-       GMAF_LOCKSTEP = 1   /* per-condition alpha_k, beta_k, same global stop test (R-A11) */ };
+       GMAF_LOCKSTEP = 1,  /* per-condition alpha_k, beta_k, same global stop test (R-A11) */
+       GMAF_ASYNC = 2      /* asynchronous strategy (Eq. 3.10): per-condition processes, each
+                              frozen once ||r_k||/||S_k|| <= tol (its CTAs stop loading); single-pass
+                              schedule, one rank */ };
 enum { GMAF_FIELD_P = 0, GMAF_FIELD_H = 1, GMAF_FIELD_HDOT = 2, GMAF_FIELD_AP = 3,
        GMAF_FIELD_AE = 4, GMAF_FIELD_AN = 5, GMAF_FIELD_S = 6, GMAF_FIELD_R = 7 };
 enum { GMAF_SHARD_CONDITIONS = 0 };
@@ -183,6 +186,10 @@ gmaf_status gmaf_solve_fixed(gmaf_ctx* ctx, double omega, int32_t precond, int32
 /* Choose the iteration schedule for subsequent solves (GMAF_SCHEDULE_*).  SINGLE with an
  * odd n_theta returns INVALID_ARG. */
 gmaf_status gmaf_set_schedule(gmaf_ctx* ctx, int32_t schedule);
+
+/* Per-condition iteration counts of the last solve (host int32[K]): the freeze iteration of
+ * each condition under GMAF_ASYNC, the common count otherwise. */
+gmaf_status gmaf_cond_iterations(gmaf_ctx* ctx, int32_t* out);
 
 /* Make a new ncclUniqueId (128 bytes) into out (NCCL is loaded at run time).  Errors: NCCL. */
 gmaf_status gmaf_nccl_unique_id(void* out);

@@ -25,7 +25,7 @@ STATUS = {0: "OK", -1: "INVALID_ARG", -2: "INVALID_MESH", -3: "MESH_TOO_COARSE",
           -4: "NONPOSITIVE_THICKNESS", -5: "BREAKDOWN", -6: "NO_CONVERGENCE", -7: "STATE",
           -8: "WORKSPACE", -9: "CUDA", -10: "NCCL"}
 PRECOND = {"none": 0, "jacobi": 1, "assor2": 2}
-COUPLING = {"coupled": 0, "lockstep": 1}
+COUPLING = {"coupled": 0, "lockstep": 1, "async": 2}
 FIELD = {"p": 0, "h": 1, "hdot": 2, "AP": 3, "AE": 4, "AN": 5, "S": 6, "r": 7}
 
 
@@ -96,13 +96,14 @@ def lib() -> C.CDLL:
         L.gmaf_reset_kernel_times.argtypes = [P]
         L.gmaf_set_schedule.argtypes = [P, C.c_int32]
         L.gmaf_nccl_unique_id.argtypes = [P]
+        L.gmaf_cond_iterations.argtypes = [P, C.POINTER(C.c_int32)]
         L.gmaf_last_error.restype = C.c_char_p
         L.gmaf_last_error.argtypes = [P]
         L.gmaf_version.restype = C.c_char_p
         for name in ("gmaf_create", "gmaf_destroy", "gmaf_thickness", "gmaf_assemble", "gmaf_solve",
                      "gmaf_solve_fixed", "gmaf_integrate", "gmaf_get", "gmaf_field_ptr",
                      "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_set_schedule",
-                     "gmaf_nccl_unique_id"):
+                     "gmaf_nccl_unique_id", "gmaf_cond_iterations"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -111,6 +112,7 @@ def lib() -> C.CDLL:
 ABI_SYMBOLS = ("gmaf_workspace_bytes", "gmaf_create", "gmaf_destroy", "gmaf_thickness", "gmaf_assemble",
                "gmaf_solve", "gmaf_solve_fixed", "gmaf_integrate", "gmaf_get", "gmaf_field_ptr",
                "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_set_schedule", "gmaf_nccl_unique_id",
+               "gmaf_cond_iterations",
                "gmaf_last_error", "gmaf_version")
 SCHEDULE = {"table1": 0, "single": 1}
 
@@ -267,6 +269,12 @@ class JointSolver:
                                                  C.byref(st)))
         return SolveStats(_SCHED_NAME[st.schedule], st.iterations, bool(st.converged), st.status,
                           st.rel_residual, st.true_rel_residual, st.solve_ms, np.zeros(self.K))
+
+    def cond_iterations(self) -> np.ndarray:
+        """Per-condition iteration counts of the last solve (the freeze iteration under 'async')."""
+        out = (C.c_int32 * self.K)()
+        _check(self.ctx, lib().gmaf_cond_iterations(self.ctx, out))
+        return np.array(list(out))
 
     def set_schedule(self, schedule: str) -> None:
         """'single' (one kernel + one reduction per iteration, default) or 'table1'."""

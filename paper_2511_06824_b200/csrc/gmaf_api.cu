@@ -160,7 +160,7 @@ Layout make_layout(const gmaf_grid* g, int K, int world = 0, int kmax = 0) {
   L.off_pall = take((size_t)4 * (world > 0 ? world : 1) * (kmax > 0 ? kmax : 1) * 8);
   L.off_wall = take((size_t)12 * (world > 0 ? world : 1) * (kmax > 0 ? kmax : 1) * 8);
   L.off_state = take(sizeof(SolverState));
-  L.off_cs = take((size_t)7 * K * 8);
+  L.off_cs = take((size_t)9 * K * 8);   // 7 double arrays + 2 int arrays
   L.off_counters = take(16 * sizeof(unsigned int));
   L.off_timing = take(sizeof(Timing));
   L.off_guard = take(4 * sizeof(unsigned long long));
@@ -200,6 +200,7 @@ struct gmaf_ctx {
   Timing* h_timing = nullptr;
   int quad_ctas = 0;
   int r_parity = 0;   // which ping-pong buffer holds the latest residual
+  int last_coupling = 0;
   bool stream_mode = false;  // GMAF_LAUNCH_MODE=stream: no CUDA graph (for ncu)
   // multi-rank (condition sharding): this rank owns global conditions [kofs, kofs + K)
   bool distm = false;
@@ -437,6 +438,7 @@ gmaf_status run_solve(gmaf_ctx* ctx, double tol, double omega, int precond, int 
   hs->coupling = coupling;
   hs->max_iter = max_iter;
   hs->fixed_iters = fixed_iters;
+  ctx->last_coupling = coupling;
   if (ctx->distm) return run_solve_dist(ctx, precond, warm, out, cond_rel);
   const GraphKey key{ctx->schedule, precond, warm ? 1 : 0, fixed_iters > 0 ? 1 : 0};
   CU(cudaMemcpyAsync(ctx->d.st_, hs, sizeof(SolverState), cudaMemcpyHostToDevice, ctx->stream));
@@ -576,6 +578,7 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
   double* cs = at<double>(ctx, L.off_cs);
   d.cs.alpha = cs; d.cs.beta = cs + K; d.cs.dk = cs + 2 * K; d.cs.Sk = cs + 3 * K; d.cs.rrk = cs + 4 * K;
   d.cs.uvk = cs + 5 * K; d.cs.ttk = cs + 6 * K;
+  d.cs.itk = reinterpret_cast<int32_t*>(cs + 7 * K); d.cs.frz = d.cs.itk + K;
   d.counters = at<unsigned int>(ctx, L.off_counters);
   d.timing = at<Timing>(ctx, L.off_timing);
   d.guard = at<unsigned long long>(ctx, L.off_guard);
@@ -741,8 +744,10 @@ gmaf_status gmaf_solve(gmaf_ctx* ctx, double tol, double omega, int32_t precond,
                        int32_t max_iter, int32_t warm_start, gmaf_solve_stats* out, double* cond_rel) {
   if (!ctx) return GMAF_E_INVALID_ARG;
   if (ctx->state < ST_ASSEMBLED) return fail(ctx, GMAF_E_STATE, "solve before assemble");
+  if (coupling == GMAF_ASYNC && (ctx->schedule != GMAF_SCHEDULE_SINGLE || ctx->distm))
+    return fail(ctx, GMAF_E_INVALID_ARG, "solve: the asynchronous strategy runs on the single-pass schedule, one rank");
   if (!(tol >= 0.0) || !(omega > 0.0 && omega < 2.0) || precond < 0 || precond > 2 || coupling < 0 ||
-      coupling > 1 || max_iter < 0)
+      coupling > 2 || max_iter < 0)
     return fail(ctx, GMAF_E_INVALID_ARG, "solve: invalid tol/omega/precond/coupling/max_iter");
   return run_solve(ctx, tol, omega, precond, coupling, max_iter, warm_start, 0, out, cond_rel);
 }
@@ -869,6 +874,16 @@ gmaf_status gmaf_set_schedule(gmaf_ctx* ctx, int32_t schedule) {
   if (schedule == GMAF_SCHEDULE_TABLE1) { ctx->schedule = schedule; return GMAF_OK; }
   if (schedule == GMAF_SCHEDULE_SINGLE && single_ok(ctx->grid.n_theta)) { ctx->schedule = schedule; return GMAF_OK; }
   return fail(ctx, GMAF_E_INVALID_ARG, "set_schedule: %d not available (n_theta %d)", schedule, ctx->grid.n_theta);
+}
+
+gmaf_status gmaf_cond_iterations(gmaf_ctx* ctx, int32_t* out) {
+  if (!ctx || !out) return GMAF_E_INVALID_ARG;
+  if (ctx->state < ST_SOLVED) return fail(ctx, GMAF_E_STATE, "cond_iterations before solve");
+  std::vector<int32_t> tmp((size_t)ctx->K);
+  CU(cudaMemcpyAsync(tmp.data(), ctx->d.cs.itk, (size_t)ctx->K * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  for (int k = 0; k < ctx->K; ++k) out[k] = ctx->last_coupling == GMAF_ASYNC ? tmp[k] : ctx->h_state->iter;
+  return GMAF_OK;
 }
 
 gmaf_status gmaf_nccl_unique_id(void* out) {

@@ -62,6 +62,8 @@ struct CondScalars {
   double* rrk;     // [K] r_k.r_k
   double* uvk;     // [K]
   double* ttk;     // [K] true residual^2
+  int32_t* itk;    // [K] iterations of condition k (asynchronous strategy, Eq. 3.10)
+  int32_t* frz;    // [K] 1 once condition k met its own test (asynchronous strategy)
 };
 
 // Multi-rank state (world > 0 only when the context was created with an NCCL communicator).

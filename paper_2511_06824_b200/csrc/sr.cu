@@ -135,10 +135,69 @@ __host__ __device__ inline size_t sr_smem_bytes(int nl) {
 // alpha/beta of the single-reduction recurrence (coupled: global; lockstep: per condition).
 // red = [rr | gamma | delta | S.S] x Kall.  Local conditions kofs .. kofs+Klocal-1 receive their
 // alpha/beta in d.cs (indexed locally).  One thread.
+// Asynchronous strategy (Eq. 3.10): every condition is its own Krylov process
+// (per-condition alpha_k, beta_k) frozen at its own test ||r_k||/||S_k|| <= tol; the solve ends
+// when all are frozen.  A frozen condition's CTAs no longer stream or compute (device mask, no
+// host round trip -- the cost the paper's implementation paid).  One rank (Kall == Klocal).
+template <bool INIT>
+__device__ void sr_scalar_async(const DevPtrs& d, const double* red, int K) {
+  SolverState* st = d.st_;
+  const double* rrk = red;
+  const double* gk = red + K;
+  const double* dk = red + 2 * K;
+  const double* ssk = red + 3 * K;
+  bool bad = false;
+  if (INIT) {
+    double SS = 0.0;
+    for (int k = 0; k < K; ++k) SS += ssk[k];
+    st->nS = sqrt(SS);
+    st->iter = 0; st->status = 0; st->converged = 0; st->done = 0; st->zero_p = (st->nS == 0.0);
+    for (int k = 0; k < K; ++k) {
+      d.cs.Sk[k] = ssk[k]; d.cs.rrk[k] = rrk[k]; d.cs.itk[k] = 0;
+      const double relk = ssk[k] > 0.0 ? sqrt(rrk[k]) / sqrt(ssk[k]) : 0.0;
+      d.cs.frz[k] = (ssk[k] == 0.0 || relk <= st->tol) ? 1 : 0;
+      double a0 = 0.0;
+      if (!d.cs.frz[k] && gk[k] != 0.0) { if (!(dk[k] > 0.0)) bad = true; a0 = gk[k] / dk[k]; }
+      d.cs.alpha[k] = a0; d.cs.beta[k] = 0.0; d.cs.uvk[k] = 0.0; d.cs.dk[k] = gk[k];
+    }
+  } else {
+    st->iter += 1;
+    for (int k = 0; k < K; ++k) {
+      if (d.cs.frz[k]) continue;
+      d.cs.itk[k] += 1;
+      d.cs.rrk[k] = rrk[k];
+      d.cs.uvk[k] = d.cs.alpha[k];                       // alpha used this iteration
+      const double relk = d.cs.Sk[k] > 0.0 ? sqrt(rrk[k]) / sqrt(d.cs.Sk[k]) : 0.0;
+      if (relk <= st->tol) { d.cs.frz[k] = 1; continue; }
+      const double aold = d.cs.alpha[k], gold = d.cs.dk[k];
+      double a = 0.0, b = 0.0;
+      if (gold != 0.0 && aold != 0.0) {
+        if (gk[k] < 0.0) bad = true;
+        b = gk[k] / gold;
+        const double den = dk[k] - b * gk[k] / aold;
+        a = (gk[k] == 0.0) ? 0.0 : gk[k] / den;
+      }
+      d.cs.alpha[k] = a; d.cs.beta[k] = b; d.cs.dk[k] = gk[k];
+    }
+  }
+  double rr = 0.0;
+  int live = 0;
+  for (int k = 0; k < K; ++k) { rr += d.cs.rrk[k]; live += d.cs.frz[k] ? 0 : 1; }
+  st->rel = st->nS > 0.0 ? sqrt(rr) / st->nS : 0.0;
+  if (live == 0) { st->done = 1; st->converged = 1; }
+  else if (st->iter >= st->max_iter) { st->done = 1; st->status = -6; }
+  if (bad && !st->done) { st->done = 1; st->status = -5; }
+}
+
 template <bool INIT>
 __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, int Klocal, int kofs,
                                 int use_cond, unsigned long long hcond) {
   SolverState* st = d.st_;
+  if (st->coupling == 2) {
+    sr_scalar_async<INIT>(d, red, Kall);
+    if (use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, st->done ? 0u : 1u);
+    return;
+  }
   const double* rrk = red;
   const double* gk = red + Kall;
   const double* dk = red + 2 * Kall;
@@ -308,7 +367,10 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
   __syncthreads();
 
   double acc_rr = 0, acc_g = 0, acc_d = 0, acc_s = 0;
-  if (is_producer) {
+  // asynchronous strategy: a frozen condition's CTAs only join the reduction
+  const bool frozen = ITER && st->coupling == 2 && d.cs.frz[k] != 0;
+  if (frozen) {
+  } else if (is_producer) {
     // ------------------------------------------------------------- TMA producer warp
     // lane a < 6 streams array a: 0 r, 1 pd_{i-1}, 2 x (or S), 3 AP, 4 AE, 5 AN
     const int lane = tid - NCT;
@@ -562,14 +624,15 @@ __global__ void k_sr_scalar(DevPtrs d, int Kglob, int Klocal, int kofs, int worl
 // x += alpha_{it-1} pd_{it-1} when the iteration count is odd (the last x update of the
 // two-at-a-time scheme is still pending).  Elementwise, reads the device iteration count.
 __global__ void k_sr_fixup(GridParams g, DevPtrs d, int K) {   // K = local conditions
-  const int it = d.st_->iter;
-  if ((it & 1) == 0) return;
+  const bool async = d.st_->coupling == 2;     // asynchronous: each condition has its own count
+  if (!async && (d.st_->iter & 1) == 0) return;
   const long long n = (long long)g.nt * g.ny;
   const double* pd = d.u[0];   // pd_{it-1}, it-1 even -> parity 0
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n * K;
        q += (long long)gridDim.x * blockDim.x) {
     const int kk = (int)(q / n);
-    d.p[q] = d.p[q] + d.cs.uvk[kk] * pd[q];
+    const int it = async ? d.cs.itk[kk] : d.st_->iter;
+    if (it & 1) d.p[q] = d.p[q] + d.cs.uvk[kk] * pd[q];
   }
 }
 

@@ -243,3 +243,32 @@ def test_nccl_condition_sharding_world1(P, orc, gi):
     assert np.array_equal(Sd.get("p", 3), S.get("p", 3))
     Sd.close()
     S.close()
+
+
+def test_async_strategy_matches_independent_solves(P, orc, gi):
+    """Asynchronous strategy (Eq. 3.10): every condition is its own PCG process, frozen at its own
+    test.  Each block equals an independent PCG solve of that condition (oracle orc_pcg_async),
+    and equals the sequential GPU acceleration (SGA) result -- K=1 contexts one after the
+    other -- to the solve tolerance."""
+    g = gi.grid(200, 48, "short", tex_n_theta=10, tex_n_y=3, tex_band_rows=12)
+    conds = gi.random_conditions(21, 4)
+    S = P.JointSolver(g, 4)
+    st, W = S.step(conds, tol=1e-10, omega=1.6, coupling="async")
+    its = S.cond_iterations()
+    AP, AE, AN, SS = orc.assemble_joint(g, conds)
+    pa, iters_ref, rc = orc.pcg_async(AP, AE, AN, SS, tol=1e-10, omega=1.6)
+    assert st.converged and rc == 0
+    assert np.all(np.abs(its - iters_ref) <= np.maximum(3, 0.02 * iters_ref)), (its, iters_ref)
+    assert st.iterations == its.max()
+    for k in range(4):
+        assert st.cond_rel[k] <= 1e-10
+        pk = S.get("p", k)
+        assert rel(pk, pa[k]) <= 1e-8, (k, rel(pk, pa[k]))
+        # SGA: the same condition alone
+        S1 = P.JointSolver(g, 1)
+        st1, W1 = S1.step(conds[k][None], tol=1e-10, omega=1.6)
+        assert abs(st1.iterations - its[k]) <= 1
+        assert rel(S1.get("p", 0), pk) <= 1e-8
+        assert wrench_err(W1[0], W[k], conds[k][8]) <= 1e-6
+        S1.close()
+    S.close()

@@ -318,6 +318,8 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
   // ASSOR split on the periodic ring (R-A12): only a pair holding column 0 on its left or
   // column nt-1 on its right sees the wraps; every other pair uses the plain formulas.
   const bool seamL = (gl == 0), seamR = (gr == nt - 1);
+  // warp-uniform guard: only the warp holding a seam pair runs the wrap corrections
+  const bool seamWarp = __any_sync(0xffffffffu, (seamL || seamR) && tid < NCT);
   const int im = max(cl - 1, 0);           // scalar index of the left neighbour of the pair
   const int ip = min(cl + 2, NL - 1);      // scalar index of the right neighbour of the pair
 
@@ -479,13 +481,17 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
           const D2 AEm1 = ld2(c1 + NL, tl);
           // plain pair: L = {W, S}, U = {E, N}
           D2 sL{AN1.l * w1.l + ae0m * w0m, AN1.r * w1.r + AE0.l * w0.l};
-          if (seamL) sL.l -= ae0m * w0m;                          // column 0: W is the wrap (in U)
-          if (seamR) sL.r += AE0.r * rright(w_0, tl);             // column nt-1: E-wrap is in L
+          if (seamWarp) {
+            if (seamL) sL.l -= ae0m * w0m;                        // column 0: W is the wrap (in U)
+            if (seamR) sL.r += AE0.r * rright(w_0, tl);           // column nt-1: E-wrap is in L
+          }
           const D2 v10{w0.l - oD0.l * sL.l, w0.r - oD0.r * sL.r};
           rst(v_0, tl, NTC, v10);
           D2 sU{AN1.l * v10.l + AEm1.l * v11.r, AN1.r * v10.r + AEm1.r * v1p};
-          if (seamL) sU.l += c1[NL + im] * rleft(v_1, tl, NTC);   // column 0: W-wrap
-          if (seamR) sU.r -= AEm1.r * v1p;                        // column nt-1: no E in U
+          if (seamWarp) {
+            if (seamL) sU.l += c1[NL + im] * rleft(v_1, tl, NTC); // column 0: W-wrap
+            if (seamR) sU.r -= AEm1.r * v1p;                      // column nt-1: no E in U
+          }
           z1 = {c2 * (v11.l - oD1.l * sU.l), c2 * (v11.r - oD1.r * sU.r)};
         } else {
           z1 = w1;                                            // D^-1 r (Jacobi) or r (none)
@@ -531,13 +537,17 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
           const double v23p = rright(v2_3, tl);
           const D2 AEm3 = ld2(c3 + NL, tl);
           D2 sL{AN3.l * w23.l + ae2m * wz2m, AN3.r * w23.r + AEm2.l * wz.l};
-          if (seamL) sL.l -= ae2m * wz2m;
-          if (seamR) sL.r += AEm2.r * rright(w2_2, tl);
+          if (seamWarp) {
+            if (seamL) sL.l -= ae2m * wz2m;
+            if (seamR) sL.r += AEm2.r * rright(w2_2, tl);
+          }
           const D2 v22{wz.l - oD2.l * sL.l, wz.r - oD2.r * sL.r};
           rst(v2_2, tl, NTC, v22);
           D2 sU{AN3.l * v22.l + AEm3.l * v23.r, AN3.r * v22.r + AEm3.r * v23p};
-          if (seamL) sU.l += c3[NL + im] * rleft(v2_3, tl, NTC);
-          if (seamR) sU.r -= AEm3.r * v23p;
+          if (seamWarp) {
+            if (seamL) sU.l += c3[NL + im] * rleft(v2_3, tl, NTC);
+            if (seamR) sU.r -= AEm3.r * v23p;
+          }
           u2_3 = {c2 * (v23.l - oD3.l * sU.l), c2 * (v23.r - oD3.r * sU.r)};
         } else {
           u2_3 = rld(w2_3, tl, NTC);

@@ -616,6 +616,7 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
       cudaMemcpyAsync((void*)d.sth, tab.data() + 3 * nt, nt * 8, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
       cudaMemsetAsync(d.counters, 0, 16 * sizeof(unsigned int), ctx->stream) != cudaSuccess ||
       cudaMemsetAsync(d.st_, 0, sizeof(SolverState), ctx->stream) != cudaSuccess ||
+      cudaMemsetAsync((void*)d.cs.alpha, 0, (size_t)9 * K * 8, ctx->stream) != cudaSuccess ||
       cudaMemsetAsync(d.p, 0, (size_t)K * gp.nt * gp.ny * 8, ctx->stream) != cudaSuccess ||
       cudaMemsetAsync((void*)d.zero_row, 0, kConstRowLen * 8, ctx->stream) != cudaSuccess ||
       cudaMemcpyAsync((void*)d.one_row, ones.data(), kConstRowLen * 8, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess)

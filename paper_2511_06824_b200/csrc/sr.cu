@@ -24,14 +24,14 @@
 // away from the seam -- suffices), one thread per column PAIR, marching over a chunk of
 // rows.  Rows are streamed by the TMA engine (cp.async.bulk) from a dedicated producer
 // warp: r, pd, x into a 4-slot ring (consumed in one step), A_P, A_E, A_N into an 8-slot
-// ring (alive for 6 steps), one full mbarrier per step, empty mbarriers per ring.  Derived
+// ring (alive for 5 steps), one full mbarrier per step, empty mbarriers per ring.  Derived
 // rows (w, v1, pd, w2, v2, z2) live in 2-slot shared rings for theta-neighbour reads;
 // own-column history in registers.  The row loop is unrolled by 8 so every ring slot is a
 // compile-time index.  Two compute-warp barriers per row.  Stage lags (rows behind the
 // load row jl):
 //   A(0) load, D^-1, w      B(0) v1 = (I - wD^-1L) w        C(1) z, pd
 //   D(2) s = A pd, r, x, w2 E(2) v2                         F(3) z2, gamma
-//   G(4) A z2, delta
+//   G(4) delta = z2' A z2 (quadratic form)
 #include <cstdint>
 #include "device_common.cuh"
 #include "gmaf_internal.cuh"
@@ -43,7 +43,7 @@ constexpr int SR_YLO = 4;       // rows loaded below the chunk
 constexpr int SR_YHI = 4;       // rows loaded above the chunk
 constexpr int SR_LAG = 4;       // the delta stage trails the load by 4 rows
 constexpr int SR_VSLOTS = 4;    // TMA ring of vector rows (r, pd, x), consumed in one step
-constexpr int SR_CSLOTS = 8;    // TMA ring of coefficient rows (AP, AE, AN), alive 6 steps
+constexpr int SR_CSLOTS = 8;    // TMA ring of coefficient rows (AP, AE, AN), alive 5 steps
 constexpr int SR_UNROLL = 8;    // row-loop unroll = coefficient-ring period
 
 enum { SR_ITER_EVEN = 0, SR_ITER_ODD = 3, SR_INIT_COLD = 1, SR_INIT_WARM = 2 };
@@ -425,7 +425,7 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
     // own-column history in registers (suffix = lag in rows behind the load row);
     // coefficient rows are read from the 8-slot ring at their lag
     D2 oD1{0, 0}, oD2{0, 0}, oD3{0, 0};
-    D2 r1{0, 0}, r2{0, 0}, pdo2{0, 0}, pd2{0, 0}, pd3{0, 0}, rn3{0, 0}, u2_4{0, 0}, u2_5{0, 0};
+    D2 r1{0, 0}, r2{0, 0}, pdo2{0, 0}, pd2{0, 0}, pd3{0, 0}, rn3{0, 0}, u2_4{0, 0};
     const bool lane0 = (tid & 31) == 0;
     for (int blk = 0; blk < nsteps; blk += SR_UNROLL) {
       const uint32_t cpar = (uint32_t)((blk / SR_UNROLL) & 1);       // phase of the per-step barriers
@@ -439,7 +439,6 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
         const double* c2r = cring + (((u + 6) & 7) * 3) * NL;
         const double* c3 = cring + (((u + 5) & 7) * 3) * NL;
         const double* c4 = cring + (((u + 4) & 7) * 3) * NL;
-        const double* c5 = cring + (((u + 3) & 7) * 3) * NL;
         double* w_0 = ringW + (u & 1) * NL;
         const double* w_1 = ringW + ((u + 1) & 1) * NL;
         double* v_0 = ringV + (u & 1) * NL;
@@ -555,19 +554,22 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
         rst(u2_3r, tl, NTC, u2_3);
         if (out && jl - 3 >= j0 && jl - 3 < j1) acc_g += rn3.l * u2_3.l + rn3.r * u2_3.r;   // gamma
         {
+          // delta = z2' A z2 as the quadratic form (A symmetric): each owned row j adds its
+          // diagonal term and its east and north couplings, i.e. every edge once, at its
+          // west / south end -- no w = A z2 vector, one coefficient row (lag 4)
           const D2 AP4 = ld2(c4, tl);
           const D2 AEm4 = ld2(c4 + NL, tl);
           const D2 AN4 = ld2(c4 + 2 * NL, tl);
-          const D2 AN5 = ld2(c5 + 2 * NL, tl);
-          D2 wv{AP4.l * u2_4.l + c4[NL + im] * rleft(u2_4r, tl, NTC), AP4.r * u2_4.r + AEm4.l * u2_4.l};
-          wv.l += AEm4.l * u2_4.r + AN5.l * u2_5.l + AN4.l * u2_3.l;
-          wv.r += AEm4.r * rright(u2_4r, tl) + AN5.r * u2_5.r + AN4.r * u2_3.r;
-          if (out && jl - 4 >= j0 && jl - 4 < j1) acc_d += u2_4.l * wv.l + u2_4.r * wv.r;  // delta
+          if (out && jl - 4 >= j0 && jl - 4 < j1) {
+            const double ql = AP4.l * u2_4.l + 2.0 * (AEm4.l * u2_4.r + AN4.l * u2_3.l);
+            const double qr = AP4.r * u2_4.r + 2.0 * (AEm4.r * rright(u2_4r, tl) + AN4.r * u2_3.r);
+            acc_d += u2_4.l * ql + u2_4.r * qr;
+          }
         }
         __syncwarp();
-        if (lane0 && blk + u >= 5) mbar_arrive(emptyc0 + 8 * ((u + 3) & 7));   // coefficient row jl-5 done
+        if (lane0 && blk + u >= 4) mbar_arrive(emptyc0 + 8 * ((u + 4) & 7));   // coefficient row jl-4 done
         // rotate the histories (register renaming across the unrolled steps)
-        u2_5 = u2_4; u2_4 = u2_3;
+        u2_4 = u2_3;
         rn3 = rn2;
         pd3 = pd2; pd2 = pd1;
         pdo2 = pdo1;

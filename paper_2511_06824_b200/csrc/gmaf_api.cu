@@ -122,7 +122,13 @@ constexpr int kMaxTilesPerCondition = 148 * 16;
 // strip widths: two-phase kernels 256/128 columns; the single-pass kernel keeps the seam
 // inside a strip, so its strips may not be wider than the ring (and need >= 12 columns)
 int tw_table1(int nt) { return nt >= 1024 ? 256 : 128; }
-int tw_single(int nt) { int w = nt < 256 ? nt : 256; return w & ~1; }
+int tw_single(int nt) {
+  int cap = 256;
+  if (const char* e = std::getenv("GMAF_SR_TW")) cap = std::atoi(e);   // A/B experiments
+  if (cap < 12 || cap > 1000) cap = 256;
+  int w = nt < cap ? nt : cap;
+  return w & ~1;
+}
 bool single_ok(int nt) { return nt % 2 == 0 && nt >= 12; }
 constexpr int kConstRowLen = 1024;   // >= the widest TMA row segment (tw + 2*halo)
 
@@ -642,6 +648,10 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
     const int socc = sr_ctas_per_sm(sprobe);
     ctx->tiles_sr = make_tiles(grid->n_theta, grid->n_y, K, sms * (socc > 0 ? socc : 1), tw_single(grid->n_theta));
     if (ctx->tiles_sr.n_tiles > kMaxTilesPerCondition) return cleanup_fail(GMAF_E_INVALID_MESH);
+    if (std::getenv("GMAF_DEBUG"))
+      std::fprintf(stderr, "gmaf: sms %d | two-phase occ %d tiles %dx%d tw %d th %d | single occ %d tiles %dx%d tw %d th %d\n",
+                   sms, occ, ctx->tiles.n_strips, ctx->tiles.n_chunks, ctx->tiles.tw, ctx->tiles.th, socc,
+                   ctx->tiles_sr.n_strips, ctx->tiles_sr.n_chunks, ctx->tiles_sr.tw, ctx->tiles_sr.th);
     // the single-pass kernel streams rows with 16-byte TMA copies: needs an even n_theta
     ctx->schedule = single_ok(grid->n_theta) ? GMAF_SCHEDULE_SINGLE : GMAF_SCHEDULE_TABLE1;
     const char* sch = std::getenv("GMAF_SCHEDULE");

@@ -282,7 +282,7 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
 }
 
 template <int PC, int MODE>
-__global__ void __launch_bounds__(192, 2)
+__global__ void __maxnreg__(168)
 k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long hcond, int use_cond) {
   extern __shared__ __align__(128) double smem_raw[];
   constexpr bool ITER = (MODE == SR_ITER_EVEN || MODE == SR_ITER_ODD);

@@ -1,0 +1,278 @@
+// sr_common.cuh -- pieces shared by the two single-reduction PCG-ASSOR-II iteration kernels
+// (today sr.cu; kept apart so a second iteration kernel can share them):
+// PTX wrappers (mbarrier, TMA bulk copy, named barrier), column-pair helpers, the Table-1 /
+// Chronopoulos-Gear scalar stage and the per-launch reduction tail.
+#pragma once
+#include <cstdint>
+#include "device_common.cuh"
+#include "gmaf_internal.cuh"
+
+namespace gmaf {
+
+enum { SR_ITER_EVEN = 0, SR_ITER_ODD = 3, SR_INIT_COLD = 1, SR_INIT_WARM = 2 };
+enum { SPC_NONE = 0, SPC_JACOBI = 1, SPC_ASSOR2 = 2 };
+
+// ------------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// consumers: spin on try_wait (the data is normally already there)
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) {
+  }
+}
+// producer: back off so a waiting producer does not steal issue slots from the compute warps
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  while (!mbar_try(bar, parity)) __nanosleep(128);
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+// named barrier 1 over the compute warps only (the producer warp never joins it)
+__device__ __forceinline__ void compute_bar(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+// 1/a to full double precision without the IEEE-division slow path: rcp.approx (MUFU)
+// + two Newton steps (the solve does not need a correctly rounded D^-1).
+__device__ __forceinline__ double fast_rcp(double a) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+  double e = fma(-a, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-a, r, 1.0);
+  return fma(r, e, r);
+}
+
+struct D2 { double l, r; };
+__device__ __forceinline__ D2 ld2(const double* base, int t) {
+  const double2 v = reinterpret_cast<const double2*>(base)[t];
+  return {v.x, v.y};
+}
+__device__ __forceinline__ void st2(double* base, int t, D2 v) {
+  reinterpret_cast<double2*>(base)[t] = make_double2(v.l, v.r);
+}
+// Derived rings use a split layout [even columns | odd columns] (NTC doubles each) so that
+// the theta neighbours of a pair are contiguous across lanes (2 wavefronts, no conflicts).
+__device__ __forceinline__ void rst(double* base, int t, int ntc, D2 v) { base[t] = v.l; base[ntc + t] = v.r; }
+__device__ __forceinline__ D2 rld(const double* base, int t, int ntc) { return {base[t], base[ntc + t]}; }
+__device__ __forceinline__ double rleft(const double* base, int t, int ntc) { return base[ntc + t - 1]; }
+__device__ __forceinline__ double rright(const double* base, int t) { return base[t + 1]; }
+__device__ __forceinline__ void stg2(double* p, D2 v) {   // 16-byte global store (pairs are aligned)
+  *reinterpret_cast<double2*>(p) = make_double2(v.l, v.r);
+}
+
+// Table-1 scalars from the per-condition sums (fixed k order): convergence test (Eq. 3.9),
+// alpha/beta of the single-reduction recurrence (coupled: global; lockstep: per condition).
+// red = [rr | gamma | delta | S.S] x Kall.  Local conditions kofs .. kofs+Klocal-1 receive their
+// alpha/beta in d.cs (indexed locally).  One thread.
+// Asynchronous strategy (Eq. 3.10): every condition is its own Krylov process
+// (per-condition alpha_k, beta_k) frozen at its own test ||r_k||/||S_k|| <= tol; the solve ends
+// when all are frozen.  A frozen condition's CTAs no longer stream or compute (device mask, no
+// host round trip -- the cost the paper's implementation paid).  One rank (Kall == Klocal).
+template <bool INIT>
+__device__ void sr_scalar_async(const DevPtrs& d, const double* red, int K) {
+  SolverState* st = d.st_;
+  const double* rrk = red;
+  const double* gk = red + K;
+  const double* dk = red + 2 * K;
+  const double* ssk = red + 3 * K;
+  bool bad = false;
+  if (INIT) {
+    double SS = 0.0;
+    for (int k = 0; k < K; ++k) SS += ssk[k];
+    st->nS = sqrt(SS);
+    st->iter = 0; st->status = 0; st->converged = 0; st->done = 0; st->zero_p = (st->nS == 0.0);
+    for (int k = 0; k < K; ++k) {
+      d.cs.Sk[k] = ssk[k]; d.cs.rrk[k] = rrk[k]; d.cs.itk[k] = 0;
+      const double relk = ssk[k] > 0.0 ? sqrt(rrk[k]) / sqrt(ssk[k]) : 0.0;
+      d.cs.frz[k] = (ssk[k] == 0.0 || relk <= st->tol) ? 1 : 0;
+      double a0 = 0.0;
+      if (!d.cs.frz[k] && gk[k] != 0.0) { if (!(dk[k] > 0.0)) bad = true; a0 = gk[k] / dk[k]; }
+      d.cs.alpha[k] = a0; d.cs.beta[k] = 0.0; d.cs.uvk[k] = 0.0; d.cs.dk[k] = gk[k];
+    }
+  } else {
+    st->iter += 1;
+    for (int k = 0; k < K; ++k) {
+      if (d.cs.frz[k]) continue;
+      d.cs.itk[k] += 1;
+      d.cs.rrk[k] = rrk[k];
+      d.cs.uvk[k] = d.cs.alpha[k];                       // alpha used this iteration
+      const double relk = d.cs.Sk[k] > 0.0 ? sqrt(rrk[k]) / sqrt(d.cs.Sk[k]) : 0.0;
+      if (relk <= st->tol) { d.cs.frz[k] = 1; continue; }
+      const double aold = d.cs.alpha[k], gold = d.cs.dk[k];
+      double a = 0.0, b = 0.0;
+      if (gold != 0.0 && aold != 0.0) {
+        if (gk[k] < 0.0) bad = true;
+        b = gk[k] / gold;
+        const double den = dk[k] - b * gk[k] / aold;
+        a = (gk[k] == 0.0) ? 0.0 : gk[k] / den;
+      }
+      d.cs.alpha[k] = a; d.cs.beta[k] = b; d.cs.dk[k] = gk[k];
+    }
+  }
+  double rr = 0.0;
+  int live = 0;
+  for (int k = 0; k < K; ++k) { rr += d.cs.rrk[k]; live += d.cs.frz[k] ? 0 : 1; }
+  st->rel = st->nS > 0.0 ? sqrt(rr) / st->nS : 0.0;
+  if (live == 0) { st->done = 1; st->converged = 1; }
+  else if (st->iter >= st->max_iter) { st->done = 1; st->status = -6; }
+  if (bad && !st->done) { st->done = 1; st->status = -5; }
+}
+
+template <bool INIT>
+__device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, int Klocal, int kofs,
+                                int use_cond, unsigned long long hcond) {
+  SolverState* st = d.st_;
+  if (st->coupling == 2) {
+    sr_scalar_async<INIT>(d, red, Kall);
+    if (use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, st->done ? 0u : 1u);
+    return;
+  }
+  const double* rrk = red;
+  const double* gk = red + Kall;
+  const double* dk = red + 2 * Kall;
+  const double* ssk = red + 3 * Kall;
+  double rr = 0.0;
+  for (int kk = 0; kk < Kall; ++kk) rr += rrk[kk];
+  for (int kl = 0; kl < Klocal; ++kl) d.cs.rrk[kl] = rrk[kofs + kl];
+  bool bad = false;
+  if (INIT) {
+    double SS = 0.0;
+    for (int kk = 0; kk < Kall; ++kk) SS += ssk[kk];
+    for (int kl = 0; kl < Klocal; ++kl) d.cs.Sk[kl] = ssk[kofs + kl];
+    st->nS = sqrt(SS);
+    st->iter = 0; st->status = 0; st->converged = 0; st->done = 0; st->zero_p = 0;
+    if (st->nS == 0.0) {
+      st->rel = 0.0; st->done = 1; st->converged = 1; st->zero_p = 1;
+    } else {
+      st->rel = sqrt(rr) / st->nS;
+      if (st->fixed_iters == 0 && st->rel <= st->tol) { st->done = 1; st->converged = 1; }
+      else if (st->max_iter <= 0) { st->done = 1; st->status = -6; }
+    }
+    if (!st->done) {
+      if (st->coupling == 0) {
+        double gg = 0.0, dd = 0.0;
+        for (int kk = 0; kk < Kall; ++kk) { gg += gk[kk]; dd += dk[kk]; }
+        if (!(dd > 0.0)) bad = true;
+        const double a0 = gg / dd;
+        for (int kl = 0; kl < Klocal; ++kl) { d.cs.alpha[kl] = a0; d.cs.beta[kl] = 0.0; d.cs.uvk[kl] = 0.0; }
+        st->d = gg;
+      } else {
+        for (int kk = 0; kk < Kall; ++kk)
+          if (gk[kk] != 0.0 && !(dk[kk] > 0.0)) bad = true;
+        for (int kl = 0; kl < Klocal; ++kl) {
+          const int kk = kofs + kl;
+          d.cs.alpha[kl] = gk[kk] != 0.0 ? gk[kk] / dk[kk] : 0.0;
+          d.cs.beta[kl] = 0.0; d.cs.uvk[kl] = 0.0; d.cs.dk[kl] = gk[kk];
+        }
+      }
+      if (bad) { st->done = 1; st->status = -5; }
+    }
+  } else {
+    st->iter += 1;
+    st->rel = sqrt(rr) / st->nS;
+    for (int kl = 0; kl < Klocal; ++kl) d.cs.uvk[kl] = d.cs.alpha[kl];   // alpha used this iteration
+    if (st->fixed_iters > 0) {
+      if (st->iter >= st->fixed_iters) st->done = 1;
+    } else if (st->rel <= st->tol) {
+      st->done = 1; st->converged = 1;
+    } else if (st->iter >= st->max_iter) {
+      st->done = 1; st->status = -6;
+    }
+    if (!st->done || st->fixed_iters > 0) {
+      if (st->coupling == 0) {
+        double g2 = 0.0, d2 = 0.0;
+        for (int kk = 0; kk < Kall; ++kk) { g2 += gk[kk]; d2 += dk[kk]; }
+        const double aold = d.cs.alpha[0];
+        const double b = g2 / st->d;
+        const double den = d2 - b * g2 / aold;
+        if (!(g2 > 0.0) || !(den > 0.0)) bad = true;
+        const double a = g2 / den;
+        for (int kl = 0; kl < Klocal; ++kl) { d.cs.alpha[kl] = a; d.cs.beta[kl] = b; }
+        st->d = g2;
+      } else {
+        for (int kk = 0; kk < Kall; ++kk)
+          if (gk[kk] < 0.0) bad = true;
+        for (int kl = 0; kl < Klocal; ++kl) {
+          const int kk = kofs + kl;
+          const double aold = d.cs.alpha[kl], gold = d.cs.dk[kl];
+          double a = 0.0, b = 0.0;
+          if (gold != 0.0 && aold != 0.0) {
+            b = gk[kk] / gold;
+            const double den = dk[kk] - b * gk[kk] / aold;
+            a = (gk[kk] == 0.0) ? 0.0 : gk[kk] / den;
+          }
+          d.cs.alpha[kl] = a; d.cs.beta[kl] = b; d.cs.dk[kl] = gk[kk];
+        }
+      }
+      if (bad && !st->done) { st->done = 1; st->status = -5; }
+    }
+  }
+  if (use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, st->done ? 0u : 1u);
+}
+
+
+// Per-CTA partials -> fixed-order per-condition sums in the last CTA -> the scalar stage
+// (multi-rank: the packed sums for the allgather).  Every thread of the CTA calls it; `red`
+// is dead shared memory of >= max(4 * (blockDim + 32), 4 * K) doubles.
+template <bool ITER, bool INIT>
+__device__ void sr_finish(const DevPtrs& d, double (&v)[4], double* red, int K, int k, int ncta, int cta,
+                          unsigned long long hcond, int use_cond) {
+  const int tid = threadIdx.x;
+  block_sum<4>(v, red);
+  if (tid == 0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) d.partials[(long long)(q * K + k) * ncta + cta] = v[q];
+  }
+  if (last_cta_arrive(&d.counters[ITER ? KK_SR_ITER : KK_SR_INIT], gridDim.x)) {
+    // per-condition sums in CTA order: [rr | gamma | delta | S.S] x K
+    for (int q = tid; q < 4 * K; q += blockDim.x) {
+      const double* srcp = d.partials + (long long)q * ncta;
+      double sum = 0.0;
+      for (int b = 0; b < ncta; ++b) sum += __ldcg(srcp + b);
+      red[q] = sum;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (d.dist.world > 0) {
+        // multi-rank: publish this rank's per-condition sums; the allgather + k_sr_scalar
+        // that follow on the stream evaluate the scalars identically on every rank
+        const int km = d.dist.kmax_local;
+        for (int q = 0; q < 4; ++q)
+          for (int kk = 0; kk < km; ++kk) d.dist.packed_local[q * km + kk] = kk < K ? red[q * K + kk] : 0.0;
+      } else {
+        sr_scalar_stage<INIT>(d, red, K, K, 0, use_cond, hcond);
+      }
+      timing_end(d.timing, ITER ? KK_SR_ITER : KK_SR_INIT);
+    }
+  }
+}
+
+}  // namespace gmaf

@@ -92,6 +92,9 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
   const bool seamWarp = __any_sync(0xffffffffu, (seamL || seamR) && tid < NCT);
   const int im = max(cl - 1, 0);           // scalar index of the left neighbour of the pair
   const int ip = min(cl + 2, NL - 1);      // scalar index of the right neighbour of the pair
+  // the left neighbour's A_E comes by shuffle, except in lane 0 and in idle lanes (which must
+  // reproduce the last real pair exactly, since they write the same ring slots)
+  const bool lcoef = (tid & 31) == 0 || tid >= NTC;
 
   double* vstage = smem_raw;                                 // [4][3][NL]  r, pd, x rows
   double* cring = vstage + SR_VSLOTS * 3 * NL;               // [8][3][NL]  AP, AE, AN rows
@@ -244,7 +247,7 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
         // ---- (B) v1(jl) = w - (omega/D) sum_L A w  (Eq. 3.5);  (C) z(jl-1), pd(jl-1)
         D2 z1;
         if constexpr (PC == SPC_ASSOR2) {
-          const double w0m = rleft(w_0, tl, NTC), ae0m = c0[NL + im];
+          const double w0m = rleft(w_0, tl, NTC), ae0m = left_of(AE0.r, c0 + NL, im, lcoef);
           const D2 v11 = rld(v_1, tl, NTC);
           const double v1p = rright(v_1, tl);
           const D2 AEm1 = ld2(c1 + NL, tl);
@@ -273,7 +276,7 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
         D2 rn2;
         const D2 AEm2 = ld2(c2r + NL, tl);
         const D2 AN3 = ld2(c3 + 2 * NL, tl);
-        const double ae2m = c2r[NL + im];
+        const double ae2m = left_of(AEm2.r, c2r + NL, im, lcoef);
         {
           const D2 AP2 = ld2(c2r, tl);
           const D2 AN2 = ld2(c2r + 2 * NL, tl);
@@ -321,7 +324,7 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
         } else {
           u2_3 = rld(w2_3, tl, NTC);
         }
-        rst(u2_3r, tl, NTC, u2_3);
+        u2_3r[tl] = u2_3.l;                                  // only the right-neighbour read (delta) remains
         if (out && jl - 3 >= j0 && jl - 3 < j1) acc_g += rn3.l * u2_3.l + rn3.r * u2_3.r;   // gamma
         {
           // delta = z2' A z2 as the quadratic form (A symmetric): each owned row j adds its

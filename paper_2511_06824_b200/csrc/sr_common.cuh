@@ -84,6 +84,12 @@ __device__ __forceinline__ void rst(double* base, int t, int ntc, D2 v) { base[t
 __device__ __forceinline__ D2 rld(const double* base, int t, int ntc) { return {base[t], base[ntc + t]}; }
 __device__ __forceinline__ double rleft(const double* base, int t, int ntc) { return base[ntc + t - 1]; }
 __device__ __forceinline__ double rright(const double* base, int t) { return base[t + 1]; }
+// value of the pair to the left (its right column) of a coefficient row: a warp shuffle of the
+// register copy, or the shared-memory element where the shuffle cannot supply it
+__device__ __forceinline__ double left_of(double own_r, const double* row, int im, bool from_smem) {
+  const double v = __shfl_up_sync(0xffffffffu, own_r, 1);
+  return from_smem ? row[im] : v;
+}
 __device__ __forceinline__ void stg2(double* p, D2 v) {   // 16-byte global store (pairs are aligned)
   *reinterpret_cast<double2*>(p) = make_double2(v.l, v.r);
 }

@@ -30,6 +30,8 @@ RPM = 600.0
 OMEGA_S = 2.0 * math.pi * RPM / 60.0
 E_BASE = (-0.2e-6, 0.2e-6, 0.2e-6, -0.2e-6)
 EDOT_BASE = (-3.78e-7, 3.78e-7, 3.78e-7, -3.78e-7)
+M_K = 0.128       # piston mass, kg (Table 8)
+M_G = 0.0259      # slipper mass, kg (Table 8)
 DE = 1e-9
 DEDOT = 1e-8
 # readings (R-A8/A20)
@@ -54,6 +56,11 @@ def grid(n_theta: int, n_y: int, texture: str = "smooth", **over) -> dict:
              tex_fill_num=1, tex_fill_den=2, tex_depth=(TEX_DEPTH if div else 0.0))
     g.update(over)
     return g
+
+
+def pump() -> dict:
+    """Table 8 pump constants for the Picard driver (masses, pitch radius, swash angle, speed)."""
+    return dict(m_k=M_K, m_G=M_G, R_b=R_B, beta=BETA, omega_s=OMEGA_S, R_k=R_K)
 
 
 def coupling_length(phi: float) -> float:

@@ -51,7 +51,8 @@ typedef enum {
   GMAF_E_STATE = -7,                 /* call order violated */
   GMAF_E_WORKSPACE = -8,             /* workspace NULL, too small or misaligned (256 B) */
   GMAF_E_CUDA = -9,                  /* a CUDA runtime error; see gmaf_last_error */
-  GMAF_E_NCCL = -10                  /* a collective failed (world > 1) */
+  GMAF_E_NCCL = -10,                 /* a collective failed (world > 1) */
+  GMAF_E_SINGULAR = -11              /* Picard driver: the 4x4 update system is singular */
 } gmaf_status;
 
 enum { GMAF_PRECOND_NONE = 0, GMAF_PRECOND_JACOBI = 1, GMAF_PRECOND_ASSOR2 = 2 };
@@ -190,6 +191,65 @@ gmaf_status gmaf_set_schedule(gmaf_ctx* ctx, int32_t schedule);
 /* Per-condition iteration counts of the last solve (host int32[K]): the freeze iteration of
  * each condition under GMAF_ASYNC, the common count otherwise. */
 gmaf_status gmaf_cond_iterations(gmaf_ctx* ctx, int32_t* out);
+
+/* ---------------------------------------------------------------------------------------
+ * Picard driver (Sec. 2.3, Eqs. 2.10-2.22): the iteration the
+ * 9 working conditions exist for.  The paper defines the iteration, not the loads: the
+ * generalized forces F1..F4 (Eq. 2.11) and the external / inertial load models are
+ * DESIGN.md readings R-A28..R-A31.  Host code around the device path: every pressure solve
+ * and force integral runs in the kernels above.
+ * ------------------------------------------------------------------------------------- */
+enum { GMAF_PICARD_SIMPLIFIED = 0,   /* Eqs. 2.20-2.22: drop dF/de, backward difference for e */
+       GMAF_PICARD_GENERAL = 1 };    /* Eq. 2.12 with both Jacobians + the same backward difference */
+
+typedef struct {
+  double m_k, m_G;    /* piston and slipper mass, kg (Table 8: 0.128, 0.0259) */
+  double R_b;         /* cylinder-block pitch radius, m (Table 8: 4.05e-2) */
+  double beta;        /* swashplate inclination, rad (Table 8: 10 deg) */
+  double omega_s;     /* shaft speed, rad/s (Table 8: 600 rpm) */
+  double R_k;         /* piston radius, m (the bottom face pi R_k^2 carries p_in) */
+} gmaf_pump;
+
+typedef struct {
+  double F[4];                 /* total general force F_E + F_I + F_O at (e, edot) (Eqs. 2.10-2.11), N */
+  double F_oil[4], F_ext[4], F_inertial[4];
+  double J_e[16], J_edot[16];  /* row-major dF_i/de_j (Eq. 2.13) and dF_i/d(edot)_j (Eq. 2.14) */
+  double e_next[4], edot_next[4];   /* the update (scheme) */
+  double wrench[12];           /* oil-film wrench of the base condition (gmaf_integrate layout) */
+  int32_t pcg_iterations;      /* of the joint solve */
+  int32_t pad;
+} gmaf_picard_iterate;
+
+/* Generalized forces of one state (host only, no context): F_oil4 from an oil-film wrench
+ * (gmaf_integrate layout, R-A28: rigid-body virtual work of the two axis points at y = 0 and
+ * y = L_F), F_ext4 the swashplate reaction to p_in on the piston bottom (R-A29) and F_in4 the
+ * inertial load (R-A30) at shaft angle phi (rad).  Any output may be NULL.  Errors: INVALID_ARG. */
+gmaf_status gmaf_general_forces(const gmaf_pump* pump, const gmaf_condition* cond, double phi,
+                                const double* wrench12, double* F_oil4, double* F_ext4, double* F_in4);
+
+/* One Picard iteration on a context created with K = 9 (world 1): the 9 conditions of
+ * Eqs. 2.17-2.19 around `state` (e = e^(k), edot = edot^(k), plus the load case), ONE joint
+ * thickness -> assemble -> solve -> integrate, the 9 general forces, the finite-difference
+ * Jacobians (Eqs. 2.13-2.14, steps de and dedot; Table 8: 1e-9 m, 1e-8 m/s) and the update
+ * for time step dt (R-A31): SIMPLIFIED e' = e - dt J_edot^-1 F, edot' = edot - J_edot^-1 F
+ * (Eqs. 2.21-2.22); GENERAL (dt J_e + J_edot) d = -F, edot' = edot + d, e' = e + dt d.
+ * tol/omega/max_iter/warm_start as gmaf_solve (ASSOR-II, coupled).  Errors: those of the
+ * device calls, SINGULAR, INVALID_ARG (K != 9, dt <= 0, unknown scheme). */
+gmaf_status gmaf_picard_iteration(gmaf_ctx* ctx, const gmaf_pump* pump, const gmaf_condition* state,
+                                  double phi, double dt, int32_t scheme, double de, double dedot,
+                                  double tol, double omega, int32_t max_iter, int32_t warm_start,
+                                  gmaf_picard_iterate* out);
+
+/* One time step t_l -> t_l + dt of the Picard time march (Sec. 2.3): starts from
+ * e = e_l + dt edot_l, edot = edot_l (so e - e_l = dt edot holds at every iterate) and
+ * iterates gmaf_picard_iteration until ||F|| <= eps_dyn * max(||F_E||, 1 N) (R-A31) or
+ * max_picard iterations.  state: in = (e_l, edot_l, load case of t_l + dt), out = the state
+ * whose force met the test (or the last iterate).  n_picard, residual (||F|| / scale) and
+ * pcg_iterations (summed) may be NULL.  Returns NO_CONVERGENCE if max_picard was reached. */
+gmaf_status gmaf_picard_step(gmaf_ctx* ctx, const gmaf_pump* pump, gmaf_condition* state, double phi,
+                             double dt, int32_t scheme, double de, double dedot, double eps_dyn,
+                             int32_t max_picard, double tol, double omega, int32_t max_iter,
+                             int32_t* n_picard, double* residual, int32_t* pcg_iterations);
 
 /* Make a new ncclUniqueId (128 bytes) into out (NCCL is loaded at run time).  Errors: NCCL. */
 gmaf_status gmaf_nccl_unique_id(void* out);

@@ -23,7 +23,7 @@ LIB_PATH = os.path.join(_HERE, "libgmaf.so")
 
 STATUS = {0: "OK", -1: "INVALID_ARG", -2: "INVALID_MESH", -3: "MESH_TOO_COARSE",
           -4: "NONPOSITIVE_THICKNESS", -5: "BREAKDOWN", -6: "NO_CONVERGENCE", -7: "STATE",
-          -8: "WORKSPACE", -9: "CUDA", -10: "NCCL"}
+          -8: "WORKSPACE", -9: "CUDA", -10: "NCCL", -11: "SINGULAR"}
 PRECOND = {"none": 0, "jacobi": 1, "assor2": 2}
 COUPLING = {"coupled": 0, "lockstep": 1, "async": 2}
 FIELD = {"p": 0, "h": 1, "hdot": 2, "AP": 3, "AE": 4, "AN": 5, "S": 6, "r": 7}
@@ -58,6 +58,20 @@ class gmaf_kernel_timing(C.Structure):
     _fields_ = [("name", C.c_char * 24), ("launches", C.c_int64), ("total_ms", C.c_double),
                 ("bytes_per_launch", C.c_double)]
 
+
+class gmaf_pump(C.Structure):
+    _fields_ = [("m_k", C.c_double), ("m_G", C.c_double), ("R_b", C.c_double), ("beta", C.c_double),
+                ("omega_s", C.c_double), ("R_k", C.c_double)]
+
+
+class gmaf_picard_iterate(C.Structure):
+    _fields_ = [("F", C.c_double * 4), ("F_oil", C.c_double * 4), ("F_ext", C.c_double * 4),
+                ("F_inertial", C.c_double * 4), ("J_e", C.c_double * 16), ("J_edot", C.c_double * 16),
+                ("e_next", C.c_double * 4), ("edot_next", C.c_double * 4), ("wrench", C.c_double * 12),
+                ("pcg_iterations", C.c_int32), ("pad", C.c_int32)]
+
+
+PICARD_SCHEME = {"simplified": 0, "general": 1}
 
 _SCHED_NAME = {0: "table1", 1: "single"}
 
@@ -97,13 +111,24 @@ def lib() -> C.CDLL:
         L.gmaf_set_schedule.argtypes = [P, C.c_int32]
         L.gmaf_nccl_unique_id.argtypes = [P]
         L.gmaf_cond_iterations.argtypes = [P, C.POINTER(C.c_int32)]
+        L.gmaf_general_forces.argtypes = [C.POINTER(gmaf_pump), C.POINTER(gmaf_condition), C.c_double,
+                                          C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                          C.POINTER(C.c_double)]
+        L.gmaf_picard_iteration.argtypes = [P, C.POINTER(gmaf_pump), C.POINTER(gmaf_condition), C.c_double,
+                                            C.c_double, C.c_int32, C.c_double, C.c_double, C.c_double,
+                                            C.c_double, C.c_int32, C.c_int32, C.POINTER(gmaf_picard_iterate)]
+        L.gmaf_picard_step.argtypes = [P, C.POINTER(gmaf_pump), C.POINTER(gmaf_condition), C.c_double,
+                                       C.c_double, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_int32,
+                                       C.c_double, C.c_double, C.c_int32, C.POINTER(C.c_int32),
+                                       C.POINTER(C.c_double), C.POINTER(C.c_int32)]
         L.gmaf_last_error.restype = C.c_char_p
         L.gmaf_last_error.argtypes = [P]
         L.gmaf_version.restype = C.c_char_p
         for name in ("gmaf_create", "gmaf_destroy", "gmaf_thickness", "gmaf_assemble", "gmaf_solve",
                      "gmaf_solve_fixed", "gmaf_integrate", "gmaf_get", "gmaf_field_ptr",
                      "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_set_schedule",
-                     "gmaf_nccl_unique_id", "gmaf_cond_iterations"):
+                     "gmaf_nccl_unique_id", "gmaf_cond_iterations", "gmaf_general_forces",
+                     "gmaf_picard_iteration", "gmaf_picard_step"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -112,7 +137,7 @@ def lib() -> C.CDLL:
 ABI_SYMBOLS = ("gmaf_workspace_bytes", "gmaf_create", "gmaf_destroy", "gmaf_thickness", "gmaf_assemble",
                "gmaf_solve", "gmaf_solve_fixed", "gmaf_integrate", "gmaf_get", "gmaf_field_ptr",
                "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_set_schedule", "gmaf_nccl_unique_id",
-               "gmaf_cond_iterations",
+               "gmaf_cond_iterations", "gmaf_general_forces", "gmaf_picard_iteration", "gmaf_picard_step",
                "gmaf_last_error", "gmaf_version")
 SCHEDULE = {"table1": 0, "single": 1}
 
@@ -132,6 +157,25 @@ def make_conditions(conds) -> C.Array:
             arr[k].edot[q] = c[4 + q]
         arr[k].L_F, arr[k].U_theta, arr[k].U_y, arr[k].p_in, arr[k].p_out = (float(x) for x in c[8:13])
     return arr
+
+
+def make_pump(pump: dict) -> gmaf_pump:
+    """gmaf_pump from a dict with m_k, m_G, R_b, beta (rad), omega_s (rad/s), R_k."""
+    return gmaf_pump(pump["m_k"], pump["m_G"], pump["R_b"], pump["beta"], pump["omega_s"], pump["R_k"])
+
+
+def general_forces(pump: dict, cond, phi: float, wrench12=None):
+    """Generalized forces (Eq. 2.11) of one state: (F_oil, F_ext, F_inertial) as numpy 4-vectors
+    (F_oil is None without a wrench).  DESIGN.md R-A28..R-A30; host only."""
+    c = make_conditions(np.asarray(cond, dtype=np.float64).reshape(1, 13))
+    fo, fe, fi = (C.c_double * 4)(), (C.c_double * 4)(), (C.c_double * 4)()
+    w = None
+    if wrench12 is not None:
+        w = (C.c_double * 12)(*np.asarray(wrench12, dtype=np.float64).ravel())
+    code = lib().gmaf_general_forces(C.byref(make_pump(pump)), c, float(phi), w, fo if w is not None else None,
+                                     fe, fi)
+    _check(None, code)
+    return (np.array(fo[:]) if w is not None else None), np.array(fe[:]), np.array(fi[:])
 
 
 def _check(ctx, code: int):
@@ -291,6 +335,40 @@ class JointSolver:
         st = self.solve(tol=tol, omega=omega, precond=precond, coupling=coupling, max_iter=max_iter,
                         warm=warm)
         return st, self.integrate()
+
+    # -- Picard driver (Sec. 2.3; include/gmaf.h) ----------------------------------------
+    def picard_iteration(self, pump: dict, state, phi: float, dt: float, scheme="general", de=1e-9,
+                         dedot=1e-8, tol=1e-10, omega=1.6, max_iter=200000, warm=False) -> dict:
+        """One Picard iteration around `state` (13 numbers: e, edot, L_F, U_theta, U_y, p_in,
+        p_out): the 9 joint solves, general forces, FD Jacobians and the update."""
+        c = make_conditions(np.asarray(state, dtype=np.float64).reshape(1, 13))
+        it = gmaf_picard_iterate()
+        _check(self.ctx, lib().gmaf_picard_iteration(self.ctx, C.byref(make_pump(pump)), c, float(phi),
+                                                     float(dt), PICARD_SCHEME[scheme], float(de), float(dedot),
+                                                     float(tol), float(omega), int(max_iter), int(bool(warm)),
+                                                     C.byref(it)))
+        return dict(F=np.array(it.F[:]), F_oil=np.array(it.F_oil[:]), F_ext=np.array(it.F_ext[:]),
+                    F_inertial=np.array(it.F_inertial[:]), J_e=np.array(it.J_e[:]).reshape(4, 4),
+                    J_edot=np.array(it.J_edot[:]).reshape(4, 4), e_next=np.array(it.e_next[:]),
+                    edot_next=np.array(it.edot_next[:]), wrench=np.array(it.wrench[:]),
+                    pcg_iterations=int(it.pcg_iterations))
+
+    def picard_step(self, pump: dict, state, phi: float, dt: float, scheme="general", de=1e-9, dedot=1e-8,
+                    eps_dyn=1e-3, max_picard=20, tol=1e-10, omega=1.6, max_iter=200000,
+                    raise_on_error=True):
+        """One time step of the Picard march from (e_l, edot_l) with the load case of t_l + dt.
+        Returns (new state (13,), n_picard, residual, pcg_iterations, status)."""
+        c = make_conditions(np.asarray(state, dtype=np.float64).reshape(1, 13))
+        n, res, pcg = C.c_int32(), C.c_double(), C.c_int32()
+        code = lib().gmaf_picard_step(self.ctx, C.byref(make_pump(pump)), c, float(phi), float(dt),
+                                      PICARD_SCHEME[scheme], float(de), float(dedot), float(eps_dyn),
+                                      int(max_picard), float(tol), float(omega), int(max_iter), C.byref(n),
+                                      C.byref(res), C.byref(pcg))
+        if raise_on_error and code != 0:
+            _check(self.ctx, code)
+        new = np.array(list(c[0].e) + list(c[0].edot) + [c[0].L_F, c[0].U_theta, c[0].U_y, c[0].p_in,
+                                                         c[0].p_out])
+        return new, int(n.value), float(res.value), int(pcg.value), code
 
     # -- readback ----------------------------------------------------------------------
     def get(self, field: str, k: int) -> np.ndarray:

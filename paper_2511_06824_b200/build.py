@@ -5,6 +5,7 @@ Translation units:
   pcg.cu                      (two-phase Table-1 PCG-ASSOR kernels; FMA allowed)
   sr.cu                       (single-pass PCG-ASSOR kernel, TMA row streaming)
   gmaf_api.cu                 (host runtime, C ABI of include/gmaf.h)
+  picard.cu                   (host Picard driver: general forces, FD Jacobians, update)
 """
 from __future__ import annotations
 
@@ -22,7 +23,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math",
           "-I" + os.path.join(ROOT, "include"), "-Xptxas", "-v"]
-UNITS = [("geometry.cu", ["--fmad=false"]), ("pcg.cu", []), ("sr.cu", []), ("gmaf_api.cu", [])]
+UNITS = [("geometry.cu", ["--fmad=false"]), ("pcg.cu", []), ("sr.cu", []), ("gmaf_api.cu", []), ("picard.cu", [])]
 
 
 def _deps():

@@ -506,6 +506,14 @@ gmaf_status run_solve(gmaf_ctx* ctx, double tol, double omega, int precond, int 
 
 }  // namespace
 
+// Context accessors for the host-side Picard driver (picard.cu), which otherwise uses only
+// the public ABI.
+namespace gmaf {
+int ctx_conditions(const gmaf_ctx* c) { return c ? c->K : 0; }
+int ctx_world(const gmaf_ctx* c) { return c ? c->world : 0; }
+gmaf_status ctx_fail(gmaf_ctx* c, gmaf_status code, const char* msg) { return fail(c, code, "%s", msg); }
+}  // namespace gmaf
+
 extern "C" {
 
 const char* gmaf_version(void) { return "gmaf-b200 0.1 (sm_100a)"; }

@@ -141,4 +141,10 @@ cudaError_t launch_sr_scalar(const DevPtrs& d, bool init, int Kglob, int Klocal,
 cudaError_t configure_sr_kernels(const TileCfg& t);
 int sr_ctas_per_sm(const TileCfg& t);
 
+// ---- host accessors (gmaf_api.cu) for the Picard driver (picard.cu) ----
+}  // namespace gmaf
+struct gmaf_ctx;
+namespace gmaf {
+int ctx_conditions(const gmaf_ctx* c);
+int ctx_world(const gmaf_ctx* c);
 }  // namespace gmaf

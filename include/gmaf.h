@@ -55,7 +55,10 @@ typedef enum {
   GMAF_E_SINGULAR = -11              /* Picard driver: the 4x4 update system is singular */
 } gmaf_status;
 
-enum { GMAF_PRECOND_NONE = 0, GMAF_PRECOND_JACOBI = 1, GMAF_PRECOND_ASSOR2 = 2 };
+enum { GMAF_PRECOND_NONE = 0,
+       GMAF_PRECOND_JACOBI = 1,   /* D^-1 (Eq. 2.8) */
+       GMAF_PRECOND_ASSOR2 = 2,   /* two-step ASSOR-II (Eqs. 3.4-3.6), the paper's choice */
+       GMAF_PRECOND_ASSOR1 = 3 }; /* diagonal ASSOR-I (Eq. 3.2); single-pass schedule only */
 enum { GMAF_COUPLED = 0,   /* one Krylov process on A_G: global alpha, beta (Eq. 3.9) */
        GMAF_LOCKSTEP = 1,  /* per-condition alpha_k, beta_k, same global stop test (R-A11) */
        GMAF_ASYNC = 2      /* asynchronous strategy (Eq. 3.10): per-condition processes, each

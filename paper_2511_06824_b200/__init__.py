@@ -24,7 +24,7 @@ LIB_PATH = os.path.join(_HERE, "libgmaf.so")
 STATUS = {0: "OK", -1: "INVALID_ARG", -2: "INVALID_MESH", -3: "MESH_TOO_COARSE",
           -4: "NONPOSITIVE_THICKNESS", -5: "BREAKDOWN", -6: "NO_CONVERGENCE", -7: "STATE",
           -8: "WORKSPACE", -9: "CUDA", -10: "NCCL", -11: "SINGULAR"}
-PRECOND = {"none": 0, "jacobi": 1, "assor2": 2}
+PRECOND = {"none": 0, "jacobi": 1, "assor2": 2, "assor1": 3}
 COUPLING = {"coupled": 0, "lockstep": 1, "async": 2}
 FIELD = {"p": 0, "h": 1, "hdot": 2, "AP": 3, "AE": 4, "AN": 5, "S": 6, "r": 7}
 

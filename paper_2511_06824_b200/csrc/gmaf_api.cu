@@ -765,7 +765,9 @@ gmaf_status gmaf_solve(gmaf_ctx* ctx, double tol, double omega, int32_t precond,
   if (ctx->state < ST_ASSEMBLED) return fail(ctx, GMAF_E_STATE, "solve before assemble");
   if (coupling == GMAF_ASYNC && (ctx->schedule != GMAF_SCHEDULE_SINGLE || ctx->distm))
     return fail(ctx, GMAF_E_INVALID_ARG, "solve: the asynchronous strategy runs on the single-pass schedule, one rank");
-  if (!(tol >= 0.0) || !(omega > 0.0 && omega < 2.0) || precond < 0 || precond > 2 || coupling < 0 ||
+  if (precond == GMAF_PRECOND_ASSOR1 && ctx->schedule != GMAF_SCHEDULE_SINGLE)
+    return fail(ctx, GMAF_E_INVALID_ARG, "solve: ASSOR-I runs on the single-pass schedule only");
+  if (!(tol >= 0.0) || !(omega > 0.0 && omega < 2.0) || precond < 0 || precond > 3 || coupling < 0 ||
       coupling > 2 || max_iter < 0)
     return fail(ctx, GMAF_E_INVALID_ARG, "solve: invalid tol/omega/precond/coupling/max_iter");
   return run_solve(ctx, tol, omega, precond, coupling, max_iter, warm_start, 0, out, cond_rel);
@@ -775,7 +777,9 @@ gmaf_status gmaf_solve_fixed(gmaf_ctx* ctx, double omega, int32_t precond, int32
                              gmaf_solve_stats* out) {
   if (!ctx) return GMAF_E_INVALID_ARG;
   if (ctx->state < ST_ASSEMBLED) return fail(ctx, GMAF_E_STATE, "solve before assemble");
-  if (n_iter < 1 || !(omega > 0.0 && omega < 2.0) || precond < 0 || precond > 2)
+  if (precond == GMAF_PRECOND_ASSOR1 && ctx->schedule != GMAF_SCHEDULE_SINGLE)
+    return fail(ctx, GMAF_E_INVALID_ARG, "solve_fixed: ASSOR-I runs on the single-pass schedule only");
+  if (n_iter < 1 || !(omega > 0.0 && omega < 2.0) || precond < 0 || precond > 3)
     return fail(ctx, GMAF_E_INVALID_ARG, "solve_fixed: invalid arguments");
   return run_solve(ctx, 0.0, omega, precond, 0, n_iter, 0, n_iter, out, nullptr);
 }

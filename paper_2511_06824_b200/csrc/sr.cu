@@ -237,7 +237,23 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
         const D2 AE0 = ld2(c0 + NL, tl);
         const D2 AN1 = ld2(c1 + 2 * NL, tl);
         const D2 w1 = rld(w_1, tl, NTC);
-        const D2 iD0{fast_rcp(AP0.l), fast_rcp(AP0.r)};
+        D2 iD0{fast_rcp(AP0.l), fast_rcp(AP0.r)};
+        if constexpr (PC == SPC_ASSOR1) {
+          // ASSOR-I (Eq. 3.2): the preconditioner is the diagonal c / Dt with
+          // Dt_i = D_i + omega^2 sum_{k in L(i)} L_ik^2 / D_k, L = {W, E-wrap at n_theta-1, S}
+          // (R-A12); it enters the pipeline exactly like Jacobi's D^-1
+          const D2 AP1 = ld2(c1, tl);
+          const double apl = left_of(AP0.r, c0, im, lcoef), ael = left_of(AE0.r, c0 + NL, im, lcoef);
+          double sl = (ael * ael) * fast_rcp(apl);
+          double sr = (AE0.l * AE0.l) * iD0.l;
+          if (seamWarp) {
+            if (seamL) sl = 0.0;                                           // column 0: no W in L
+            if (seamR) sr += (AE0.r * AE0.r) * fast_rcp(c0[ip]);           // column nt-1: E-wrap
+          }
+          sl += (AN1.l * AN1.l) * fast_rcp(AP1.l);
+          sr += (AN1.r * AN1.r) * fast_rcp(AP1.r);
+          iD0 = {c2 * fast_rcp(AP0.l + (omega * omega) * sl), c2 * fast_rcp(AP0.r + (omega * omega) * sr)};
+        }
         const D2 oD0{omega * iD0.l, omega * iD0.r};
         D2 w0;
         if constexpr (PC == SPC_NONE) w0 = r0; else w0 = {r0.l * iD0.l, r0.r * iD0.r};
@@ -410,10 +426,12 @@ cudaError_t launch_sr_init(const GridParams& g, const DevPtrs& d, const TileCfg&
   const int use = h != 0ull;
   if (warm) {
     if (precond == SPC_ASSOR2) return sr_launch(k_sr<SPC_ASSOR2, SR_INIT_WARM>, g, d, t, K, 1, h, use, s);
+    if (precond == SPC_ASSOR1) return sr_launch(k_sr<SPC_ASSOR1, SR_INIT_WARM>, g, d, t, K, 1, h, use, s);
     if (precond == SPC_JACOBI) return sr_launch(k_sr<SPC_JACOBI, SR_INIT_WARM>, g, d, t, K, 1, h, use, s);
     return sr_launch(k_sr<SPC_NONE, SR_INIT_WARM>, g, d, t, K, 1, h, use, s);
   }
   if (precond == SPC_ASSOR2) return sr_launch(k_sr<SPC_ASSOR2, SR_INIT_COLD>, g, d, t, K, 1, h, use, s);
+  if (precond == SPC_ASSOR1) return sr_launch(k_sr<SPC_ASSOR1, SR_INIT_COLD>, g, d, t, K, 1, h, use, s);
   if (precond == SPC_JACOBI) return sr_launch(k_sr<SPC_JACOBI, SR_INIT_COLD>, g, d, t, K, 1, h, use, s);
   return sr_launch(k_sr<SPC_NONE, SR_INIT_COLD>, g, d, t, K, 1, h, use, s);
 }
@@ -424,10 +442,12 @@ cudaError_t launch_sr_iter(const GridParams& g, const DevPtrs& d, const TileCfg&
   const int use = h != 0ull;
   if (parity & 1) {
     if (precond == SPC_ASSOR2) return sr_launch(k_sr<SPC_ASSOR2, SR_ITER_ODD>, g, d, t, K, parity, h, use, s);
+    if (precond == SPC_ASSOR1) return sr_launch(k_sr<SPC_ASSOR1, SR_ITER_ODD>, g, d, t, K, parity, h, use, s);
     if (precond == SPC_JACOBI) return sr_launch(k_sr<SPC_JACOBI, SR_ITER_ODD>, g, d, t, K, parity, h, use, s);
     return sr_launch(k_sr<SPC_NONE, SR_ITER_ODD>, g, d, t, K, parity, h, use, s);
   }
   if (precond == SPC_ASSOR2) return sr_launch(k_sr<SPC_ASSOR2, SR_ITER_EVEN>, g, d, t, K, parity, h, use, s);
+  if (precond == SPC_ASSOR1) return sr_launch(k_sr<SPC_ASSOR1, SR_ITER_EVEN>, g, d, t, K, parity, h, use, s);
   if (precond == SPC_JACOBI) return sr_launch(k_sr<SPC_JACOBI, SR_ITER_EVEN>, g, d, t, K, parity, h, use, s);
   return sr_launch(k_sr<SPC_NONE, SR_ITER_EVEN>, g, d, t, K, parity, h, use, s);
 }
@@ -465,6 +485,8 @@ cudaError_t configure_sr_kernels(const TileCfg& t) {
   GMAF_SR_SET(k_sr<SPC_NONE, SR_INIT_COLD>);
   GMAF_SR_SET(k_sr<SPC_ASSOR2, SR_INIT_WARM>); GMAF_SR_SET(k_sr<SPC_JACOBI, SR_INIT_WARM>);
   GMAF_SR_SET(k_sr<SPC_NONE, SR_INIT_WARM>);
+  GMAF_SR_SET(k_sr<SPC_ASSOR1, SR_ITER_EVEN>); GMAF_SR_SET(k_sr<SPC_ASSOR1, SR_ITER_ODD>);
+  GMAF_SR_SET(k_sr<SPC_ASSOR1, SR_INIT_COLD>); GMAF_SR_SET(k_sr<SPC_ASSOR1, SR_INIT_WARM>);
 #undef GMAF_SR_SET
   return e;
 }

@@ -7,6 +7,8 @@
           400x360 and 800x760, tol 1e-6                               -- Tables 4-6
   assor_vs_jacobi: iterations and time of ASSOR-II vs Jacobi (the "36%", Table 2)
   omega: ASSOR-II iterations vs omega = 0.18 i + 0.1 (Fig. 2b)
+  fig2a: none / Jacobi / ASSOR-I / ASSOR-II at 2000x1600 smooth, rtol 1e-12, omega 1.8 (Fig. 2a,
+         P:277-281: 6352 / 6519 / 3738 iterations for Jacobi / ASSOR-I / ASSOR-II)
 Writes one JSON document to stdout.
 """
 import json
@@ -88,9 +90,25 @@ def omega_sweep():
     return out
 
 
+def fig2a():
+    case = gi.table_case(2000, 1600, "smooth", K=1)
+    S = P.JointSolver(case.grid, 1)
+    out = {}
+    for pc in ("none", "jacobi", "assor1", "assor2"):
+        st, dt = timed_step(S, case.conds, reps=1, tol=1e-12, omega=1.8, precond=pc)
+        out[pc] = dict(iterations=st.iterations, seconds=dt, ms_per_iteration=1e3 * dt / max(st.iterations, 1))
+    out["paper"] = dict(jacobi=6352, ssor=6352, assor1=6519, assor2=3738,
+                        seconds=dict(ssor=1680.10, assor1=215.21, assor2=226.57, jacobi=246.41))
+    S.close()
+    return out
+
+
 def main():
+    if len(sys.argv) > 1:   # one study by name
+        print(json.dumps({sys.argv[1]: globals()[sys.argv[1]]()}, indent=1))
+        return
     doc = {"device": torch.cuda.get_device_name(0), "table3": table3(), "table4": table4(),
-           "omega_sweep_800x760_smooth_tol1e-6": omega_sweep()}
+           "omega_sweep_800x760_smooth_tol1e-6": omega_sweep(), "fig2a": fig2a()}
     print(json.dumps(doc, indent=1))
 
 

@@ -166,7 +166,10 @@ def _config_obj(cfg, args):
                         "coupled synchronized convergence (Eq. 3.9)",
             "n_theta": g["n_theta"], "n_y": g["n_y"], "K": cfg.K,
             "texture": "short 60x10" if g.get("tex_n_theta") else "smooth",
-            "dof": cfg.dof, "l2_policy": "inputs larger than L2 (151 MB per field at C3)",
+            "dof": cfg.dof,
+            "l2_policy": (f"inputs larger than L2 ({cfg.dof * 8 / 1e6:.0f} MB per field, 126 MB L2)"
+                          if cfg.dof * 8 > 126e6 else
+                          f"working set L2-resident ({cfg.dof * 8 / 1e6:.1f} MB per field): not an HBM measurement"),
             "parallelism": "1 GPU" if args.gpus == 1 else
             f"{args.gpus} GPUs: one joint system of {cfg.K}x{args.gpus} conditions, condition-sharded "
             f"({cfg.K} per GPU), one NCCL allgather per PCG iteration (weak)"}

@@ -60,14 +60,14 @@ __device__ __forceinline__ void compute_bar(int nthreads) {
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 // 1/a to full double precision without the IEEE-division slow path: rcp.approx (MUFU)
-// + two Newton steps (the solve does not need a correctly rounded D^-1).
+// + one third-order Newton step (the solve does not need a correctly rounded D^-1).
 __device__ __forceinline__ double fast_rcp(double a) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
-  double e = fma(-a, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-a, r, 1.0);
-  return fma(r, e, r);
+  // one third-order Newton step r (1 + e + e^2), e = 1 - a r: the ~2^-22 approximation
+  // becomes ~2^-66 in 3 dependent FMAs (two second-order steps need 4)
+  const double e = fma(-a, r, 1.0);
+  return fma(r, fma(e, e, e), r);
 }
 
 struct D2 { double l, r; };

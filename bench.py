@@ -172,7 +172,9 @@ def _config_obj(cfg, args):
                           f"working set L2-resident ({cfg.dof * 8 / 1e6:.1f} MB per field): not an HBM measurement"),
             "parallelism": "1 GPU" if args.gpus == 1 else
             f"{args.gpus} GPUs: one joint system of {cfg.K}x{args.gpus} conditions, condition-sharded "
-            f"({cfg.K} per GPU), one NCCL allgather per PCG iteration (weak)"}
+            f"({cfg.K} per GPU); per PCG iteration one gather of the per-condition sums "
+            f"({os.environ.get('GMAF_DIST', 'p2p')}: "
+            f"{'NCCL allgather' if os.environ.get('GMAF_DIST', 'p2p') == 'nccl' else 'fused into the iteration kernel over NVLink peer memory'}) (weak)"}
 
 
 def run_gmaf(args, cfg):
@@ -195,13 +197,24 @@ def run_gmaf(args, cfg):
         conds_all = np.concatenate([cfg.conds if r == 0 else
                                     gi.fd_conditions(gi.condition(phi_deg=operating_point_of(r)))
                                     for r in range(world)])
-        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            uid.copy_(torch.frombuffer(bytearray(P.gmaf_nccl_unique_id()), dtype=torch.uint8))
-        if dist:
-            dist.broadcast(uid, 0)
-        S = P.JointSolver(cfg.grid, K * world, device=local, rank=rank, world=world,
-                          nccl_uid=bytes(uid.cpu().numpy().tobytes()))
+        if os.environ.get("GMAF_DIST", "p2p") == "nccl":
+            # NCCL mode: one ncclAllGather + a scalar kernel per iteration, host-polled batches
+            uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+            if rank == 0:
+                uid.copy_(torch.frombuffer(bytearray(P.gmaf_nccl_unique_id()), dtype=torch.uint8))
+            if dist:
+                dist.broadcast(uid, 0)
+            S = P.JointSolver(cfg.grid, K * world, device=local, rank=rank, world=world,
+                              nccl_uid=bytes(uid.cpu().numpy().tobytes()))
+        else:
+            # peer-to-peer mode (default): the per-iteration gather is fused into the iteration
+            # kernel over IPC-mapped peer memory (NVLink); one CUDA graph per solve
+            S = P.JointSolver(cfg.grid, K * world, device=local, rank=rank, world=world, p2p=True)
+            if dist:
+                from paper_2511_06824_b200.dist import connect_p2p
+                connect_p2p(S)
+            else:
+                S.p2p_connect([S.p2p_handle()])
         conds = conds_all
     else:
         conds = cfg.conds

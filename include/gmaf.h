@@ -66,7 +66,8 @@ enum { GMAF_COUPLED = 0,   /* one Krylov process on A_G: global alpha, beta (P:2
                               schedule, one rank */ };
 enum { GMAF_FIELD_P = 0, GMAF_FIELD_H = 1, GMAF_FIELD_HDOT = 2, GMAF_FIELD_AP = 3,
        GMAF_FIELD_AE = 4, GMAF_FIELD_AN = 5, GMAF_FIELD_S = 6, GMAF_FIELD_R = 7 };
-enum { GMAF_SHARD_CONDITIONS = 0 };
+enum { GMAF_SHARD_CONDITIONS = 0,       /* condition blocks; NCCL allgather per iteration (needs an id) */
+       GMAF_SHARD_CONDITIONS_P2P = 1 };  /* condition blocks; gather fused into the kernel, peer memory */
 /* Iteration schedule: both run the Table-1 method to the same rtol.
  * SINGLE: one fused kernel and one global (gamma, delta, r.r) reduction per iteration
  *         (Chronopoulos-Gear alpha recurrence; needs an even n_theta) -- the default;
@@ -107,7 +108,8 @@ typedef struct {
 typedef struct {
   int32_t rank, world;
   const void* nccl_unique_id;
-  int32_t shard;                 /* GMAF_SHARD_CONDITIONS */
+  int32_t shard;                 /* GMAF_SHARD_CONDITIONS (NCCL) or GMAF_SHARD_CONDITIONS_P2P; a
+                                    world > 1 context without an NCCL id is peer to peer */
 } gmaf_dist;
 
 typedef struct {
@@ -253,6 +255,19 @@ gmaf_status gmaf_picard_step(gmaf_ctx* ctx, const gmaf_pump* pump, gmaf_conditio
                              double dt, int32_t scheme, double de, double dedot, double eps_dyn,
                              int32_t max_picard, double tol, double omega, int32_t max_iter,
                              int32_t* n_picard, double* residual, int32_t* pcg_iterations);
+
+/* Peer-to-peer condition sharding (no NCCL).  A context created with
+ * dist.world > 1 and dist.nccl_unique_id == NULL owns a small device exchange buffer; every rank
+ * exports its CUDA IPC handle (64 bytes) with gmaf_p2p_handle, the caller all-gathers the handles
+ * in rank order (e.g. over torch.distributed) and passes the world*64 bytes to gmaf_p2p_connect
+ * (before the first solve).  The per-iteration reduction then runs on the device inside the
+ * solve's CUDA graph: after each iteration kernel one CTA pushes the rank's per-condition sums
+ * into every rank's buffer over NVLink, waits for all ranks (a solve whose peer never arrives
+ * fails with GMAF_E_CUDA after 10 s), evaluates Eq. 3.9 / alpha / beta in global condition order
+ * and sets the graph's WHILE condition -- no NCCL, no host round trip.  Ranks of one node only
+ * (<= 8), K <= 256.  Errors: STATE (not a peer-to-peer context / already connected), CUDA. */
+gmaf_status gmaf_p2p_handle(gmaf_ctx* ctx, void* out);
+gmaf_status gmaf_p2p_connect(gmaf_ctx* ctx, const void* handles);
 
 /* Make a new ncclUniqueId (128 bytes) into out (NCCL is loaded at run time).  Errors: NCCL. */
 gmaf_status gmaf_nccl_unique_id(void* out);

@@ -121,6 +121,8 @@ def lib() -> C.CDLL:
                                        C.c_double, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_int32,
                                        C.c_double, C.c_double, C.c_int32, C.POINTER(C.c_int32),
                                        C.POINTER(C.c_double), C.POINTER(C.c_int32)]
+        L.gmaf_p2p_handle.argtypes = [P, P]
+        L.gmaf_p2p_connect.argtypes = [P, P]
         L.gmaf_last_error.restype = C.c_char_p
         L.gmaf_last_error.argtypes = [P]
         L.gmaf_version.restype = C.c_char_p
@@ -128,7 +130,7 @@ def lib() -> C.CDLL:
                      "gmaf_solve_fixed", "gmaf_integrate", "gmaf_get", "gmaf_field_ptr",
                      "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_set_schedule",
                      "gmaf_nccl_unique_id", "gmaf_cond_iterations", "gmaf_general_forces",
-                     "gmaf_picard_iteration", "gmaf_picard_step"):
+                     "gmaf_picard_iteration", "gmaf_picard_step", "gmaf_p2p_handle", "gmaf_p2p_connect"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -138,6 +140,7 @@ ABI_SYMBOLS = ("gmaf_workspace_bytes", "gmaf_create", "gmaf_destroy", "gmaf_thic
                "gmaf_solve", "gmaf_solve_fixed", "gmaf_integrate", "gmaf_get", "gmaf_field_ptr",
                "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_set_schedule", "gmaf_nccl_unique_id",
                "gmaf_cond_iterations", "gmaf_general_forces", "gmaf_picard_iteration", "gmaf_picard_step",
+               "gmaf_p2p_handle", "gmaf_p2p_connect",
                "gmaf_last_error", "gmaf_version")
 SCHEDULE = {"table1": 0, "single": 1}
 
@@ -193,7 +196,9 @@ def gmaf_nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
-def make_dist(rank: int, world: int, uid: bytes | None):
+def make_dist(rank: int, world: int, uid: bytes | None, p2p: bool = False):
+    if p2p:   # peer-to-peer condition sharding: no NCCL id (connect with p2p_connect)
+        return gmaf_dist(int(rank), int(world), None, 1), None
     if uid is None:
         return None, None
     keep = C.create_string_buffer(uid, 128)
@@ -254,9 +259,12 @@ class JointSolver:
     """One context: K working conditions on one mesh (Eq. 3.7 joint system)."""
 
     def __init__(self, grid: dict, K: int, device: int | str = 0, stream=None, rank: int = 0,
-                 world: int = 1, nccl_uid: bytes | None = None):
+                 world: int = 1, nccl_uid: bytes | None = None, p2p: bool = False):
         """K = total conditions.  With nccl_uid the K conditions are sharded over `world` ranks
-        (condition sharding with one allgather per iteration, include/gmaf.h gmaf_dist)."""
+        (condition sharding with one NCCL allgather per iteration, include/gmaf.h gmaf_dist); with
+        p2p=True they are sharded peer to peer (the gathers fused into the iteration kernel over
+        IPC-mapped peer memory) -- call p2p_handle() / p2p_connect() before the first solve, or
+        paper_2511_06824_b200.dist.connect_p2p(solver)."""
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("JointSolver needs a CUDA device (no CPU fallback)")
@@ -266,7 +274,8 @@ class JointSolver:
         self.grid = make_grid(grid)
         self.K = int(K)
         self.n_theta, self.n_y = int(grid["n_theta"]), int(grid["n_y"])
-        self.dist, self._uid_buf = make_dist(rank, world, nccl_uid)
+        self.dist, self._uid_buf = make_dist(rank, world, nccl_uid, p2p=p2p and world >= 1)
+        self.rank, self.world = int(rank), int(world)
         nbytes = gmaf_workspace_bytes(self.grid, self.K, self.dist)
         if nbytes == 0:
             raise GmafError(-1, "invalid grid for workspace sizing")
@@ -276,6 +285,18 @@ class JointSolver:
             self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         self.ctx = gmaf_create(self.grid, self.K, self.workspace.data_ptr(), nbytes, self.stream.cuda_stream,
                                self.dist)
+
+    def p2p_handle(self) -> bytes:
+        """This rank's 64-byte CUDA IPC handle of its exchange buffer (peer-to-peer mode)."""
+        buf = (C.c_char * 64)()
+        _check(self.ctx, lib().gmaf_p2p_handle(self.ctx, buf))
+        return bytes(buf)
+
+    def p2p_connect(self, handles: list[bytes]):
+        """Open every rank's exchange buffer (handles in rank order, world x 64 bytes)."""
+        blob = b"".join(handles)
+        assert len(blob) == 64 * self.world
+        _check(self.ctx, lib().gmaf_p2p_connect(self.ctx, C.create_string_buffer(blob, len(blob))))
 
     def close(self):
         if getattr(self, "ctx", None):

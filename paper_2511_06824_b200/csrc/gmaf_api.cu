@@ -73,7 +73,9 @@ void shard(int K, int world, int rank, int* lo, int* hi) {
   *hi = *lo + base + (rank < extra ? 1 : 0);
 }
 
-bool dist_mode(const gmaf_dist* dist) { return dist && (dist->world > 1 || dist->nccl_unique_id != nullptr); }
+bool dist_mode(const gmaf_dist* dist) {
+  return dist && (dist->world > 1 || dist->nccl_unique_id != nullptr || dist->shard == GMAF_SHARD_CONDITIONS_P2P);
+}
 
 constexpr int kUnroll = 4;          // (A, B) pairs per WHILE-body execution (must be even)
 static_assert(kUnroll % 2 == 0, "ping-pong parity");
@@ -212,6 +214,10 @@ struct gmaf_ctx {
   bool distm = false;
   int world = 1, rank = 0, kofs = 0, Kglob = 0, kmax = 0;
   ncclComm_t comm = nullptr;
+  // peer-to-peer mode (condition sharding without NCCL)
+  bool p2p = false, p2p_ready = false;
+  char* p2p_buf = nullptr;                 // library-owned exchange buffer (cudaMalloc, IPC-exported)
+  void* peer_bufs[kMaxP2P] = {};           // IPC-opened buffers of the other ranks
   double* h_packed = nullptr;   // [world][4][kmax]
   double* h_wall = nullptr;     // [world][kmax][12]
   cudaEvent_t evb[2] = {nullptr, nullptr};
@@ -278,7 +284,9 @@ cudaError_t enqueue_init(gmaf_ctx* ctx, const GraphKey& key, unsigned long long 
     cudaError_t e = launch_residual_init(ctx->gp, ctx->d, ctx->tiles, ctx->K, 1, s);
     if (e != cudaSuccess) return e;
   }
-  return launch_sr_init(ctx->gp, ctx->d, ctx->tiles_sr, ctx->K, key.precond, key.warm != 0, h, s);
+  cudaError_t e = launch_sr_init(ctx->gp, ctx->d, ctx->tiles_sr, ctx->K, key.precond, key.warm != 0, h, s);
+  if (e != cudaSuccess || !ctx->p2p) return e;
+  return launch_p2p_scalar(ctx->d, true, ctx->K, h, s);   // peer-to-peer: gather + scalars
 }
 
 cudaError_t enqueue_iterations(gmaf_ctx* ctx, const GraphKey& key, unsigned long long h, cudaStream_t s) {
@@ -290,6 +298,7 @@ cudaError_t enqueue_iterations(gmaf_ctx* ctx, const GraphKey& key, unsigned long
       if (e == cudaSuccess) e = launch_phase_b(ctx->gp, ctx->d, ctx->tiles, ctx->K, key.precond, u & 1, h, s);
     } else {
       e = launch_sr_iter(ctx->gp, ctx->d, ctx->tiles_sr, ctx->K, key.precond, u & 1, h, s);
+      if (e == cudaSuccess && ctx->p2p) e = launch_p2p_scalar(ctx->d, false, ctx->K, h, s);
     }
   }
   return e;
@@ -300,7 +309,12 @@ cudaError_t enqueue_final(gmaf_ctx* ctx, const GraphKey& key, cudaStream_t s) {
     cudaError_t e = launch_sr_fixup(ctx->gp, ctx->d, ctx->K, s);
     if (e != cudaSuccess) return e;
   }
-  return launch_true_residual(ctx->gp, ctx->d, ctx->tiles, ctx->K, s);   // ||S - A p|| at exit
+  cudaError_t e = launch_true_residual(ctx->gp, ctx->d, ctx->tiles, ctx->K, s);   // ||S - A p|| at exit
+  if (e != cudaSuccess || !ctx->p2p) return e;
+  // peer-to-peer mode: gather every rank's ||S_k - A_k p_k||^2, then the global value
+  e = launch_p2p_gather(ctx->d, ctx->d.dist.packed_local, ctx->kmax, ctx->d.dist.packed_all, s);
+  if (e != cudaSuccess) return e;
+  return launch_true_scalar(ctx->d, ctx->world, s);
 }
 
 gmaf_status build_graph(gmaf_ctx* ctx, const GraphKey& key, cudaGraphExec_t* out) {
@@ -445,7 +459,8 @@ gmaf_status run_solve(gmaf_ctx* ctx, double tol, double omega, int precond, int 
   hs->max_iter = max_iter;
   hs->fixed_iters = fixed_iters;
   ctx->last_coupling = coupling;
-  if (ctx->distm) return run_solve_dist(ctx, precond, warm, out, cond_rel);
+  if (ctx->distm && !ctx->p2p) return run_solve_dist(ctx, precond, warm, out, cond_rel);
+  if (ctx->p2p && !ctx->p2p_ready) return fail(ctx, GMAF_E_STATE, "solve: peer-to-peer context not connected");
   const GraphKey key{ctx->schedule, precond, warm ? 1 : 0, fixed_iters > 0 ? 1 : 0};
   CU(cudaMemcpyAsync(ctx->d.st_, hs, sizeof(SolverState), cudaMemcpyHostToDevice, ctx->stream));
   if (ctx->stream_mode) {
@@ -482,8 +497,16 @@ gmaf_status run_solve(gmaf_ctx* ctx, double tol, double omega, int precond, int 
   const int K = ctx->K;
   const double* Sk = ctx->h_cs + 3 * K;
   const double* rrk = ctx->h_cs + 4 * K;
-  if (cond_rel)
+  if (cond_rel && ctx->p2p) {   // every condition of every rank (gathered on the device)
+    std::vector<double> rs((size_t)2 * ctx->Kglob);
+    CU(cudaMemcpy(rs.data(), ctx->d.dist.rr_all, rs.size() * 8, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < ctx->Kglob; ++k) {
+      const double rr = rs[k], ss = rs[ctx->Kglob + k];
+      cond_rel[k] = ss > 0.0 ? std::sqrt(rr) / std::sqrt(ss) : 0.0;
+    }
+  } else if (cond_rel) {
     for (int k = 0; k < K; ++k) cond_rel[k] = (Sk[k] > 0.0) ? std::sqrt(rrk[k]) / std::sqrt(Sk[k]) : 0.0;
+  }
   if (out) {
     out->iterations = hs->iter;
     out->converged = hs->converged;
@@ -496,6 +519,8 @@ gmaf_status run_solve(gmaf_ctx* ctx, double tol, double omega, int precond, int 
   }
   ctx->r_parity = hs->iter & 1;
   ctx->state = ST_SOLVED;
+  if (hs->status == GMAF_E_CUDA)
+    return fail(ctx, GMAF_E_CUDA, "solve: a peer rank did not arrive within the timeout (iteration %d)", hs->iter);
   if (hs->status == GMAF_E_BREAKDOWN)
     return fail(ctx, GMAF_E_BREAKDOWN, "solve: breakdown at iteration %d (u.v<=0 or r.z<=0)", hs->iter);
   if (hs->status == GMAF_E_NO_CONVERGENCE)
@@ -541,9 +566,11 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
   const bool dm = dist_mode(dist);
   int klo = 0, khi = K, world = 1, kmax = 0;
   if (dm) {
-    // condition sharding needs the single-pass schedule, >= 1 condition per rank and an id
-    if (!dist->nccl_unique_id || dist->world > K || grid->n_theta % 2 != 0 || grid->n_theta < 12)
-      return GMAF_E_INVALID_ARG;
+    // condition sharding needs the single-pass schedule and >= 1 condition per rank; without an
+    // NCCL id it runs peer to peer (<= kMaxP2P ranks, connected by gmaf_p2p_connect)
+    if (dist->world > K || grid->n_theta % 2 != 0 || grid->n_theta < 12) return GMAF_E_INVALID_ARG;
+    const bool p2p = !dist->nccl_unique_id || dist->shard == GMAF_SHARD_CONDITIONS_P2P;
+    if (p2p && (dist->world > kMaxP2P || K > 256)) return GMAF_E_INVALID_ARG;
     world = dist->world;
     shard(K, world, dist->rank, &klo, &khi);
     kmax = (K + world - 1) / world;
@@ -559,6 +586,7 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
   ctx->K = K;
   ctx->Kglob = Kglob;
   ctx->distm = dm;
+  ctx->p2p = dm && (!dist->nccl_unique_id || dist->shard == GMAF_SHARD_CONDITIONS_P2P);
   ctx->world = world;
   ctx->rank = dm ? dist->rank : 0;
   ctx->kofs = klo;
@@ -667,7 +695,25 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
   }
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
   ctx->quad_ctas = quad_ctas_per_condition(gp, K);
-  if (dm) {
+  if (dm && ctx->p2p) {
+    const size_t xs = (size_t)12 * kmax;
+    const size_t bytes = (size_t)2 * world * 8 + (size_t)2 * world * xs * 8 + 8 + (size_t)2 * Kglob * 8;
+    if (cudaMalloc((void**)&ctx->p2p_buf, bytes) != cudaSuccess ||
+        cudaMemsetAsync(ctx->p2p_buf, 0, bytes, ctx->stream) != cudaSuccess ||
+        cudaMallocHost((void**)&ctx->h_packed, (size_t)2 * 4 * kmax * world * 8) != cudaSuccess ||
+        cudaMallocHost((void**)&ctx->h_wall, (size_t)12 * kmax * world * 8) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+      return cleanup_fail(GMAF_E_CUDA);
+    DistPtrs& dd = ctx->d.dist;
+    dd.p2p = 1;
+    dd.xs = (int)xs;
+    dd.kglob = Kglob;
+    dd.peer[ctx->rank] = ctx->p2p_buf;
+    char* tail = ctx->p2p_buf + (size_t)2 * world * 8 + (size_t)2 * world * xs * 8;
+    dd.seq = reinterpret_cast<unsigned long long*>(tail);
+    dd.rr_all = reinterpret_cast<double*>(tail + 8);
+    dd.ss_all = dd.rr_all + Kglob;
+  } else if (dm) {
     NcclApi& N = nccl_api();
     if (!N.ok) { gmaf_status e = fail(ctx, GMAF_E_NCCL, "NCCL unavailable: %s", N.err.c_str()); gmaf_destroy(ctx); return e; }
     if (cudaMallocHost((void**)&ctx->h_packed, (size_t)2 * 4 * kmax * world * 8) != cudaSuccess ||
@@ -692,6 +738,9 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
 gmaf_status gmaf_destroy(gmaf_ctx* ctx) {
   if (!ctx) return GMAF_E_INVALID_ARG;
   if (ctx->comm) nccl_api().commDestroy(ctx->comm);
+  for (int r = 0; r < kMaxP2P; ++r)
+    if (ctx->peer_bufs[r]) cudaIpcCloseMemHandle(ctx->peer_bufs[r]);
+  if (ctx->p2p_buf) cudaFree(ctx->p2p_buf);
   if (ctx->h_packed) cudaFreeHost(ctx->h_packed);
   if (ctx->h_wall) cudaFreeHost(ctx->h_wall);
   if (ctx->h_done) cudaFreeHost(ctx->h_done);
@@ -791,7 +840,8 @@ gmaf_status gmaf_integrate(gmaf_ctx* ctx, double* wrench) {
   if (ctx->distm) {   // every rank returns all K wrenches (allgather of the padded blocks)
     const int km = ctx->kmax;
     double* wall = reinterpret_cast<double*>(ctx->ws + ctx->L.off_wall);
-    NC(nccl_api().allGather(ctx->d.wrench, wall, (size_t)12 * km, ncclDouble, ctx->comm, ctx->stream));
+    if (ctx->p2p) CU(launch_p2p_gather(ctx->d, ctx->d.wrench, 12 * km, wall, ctx->stream));
+    else NC(nccl_api().allGather(ctx->d.wrench, wall, (size_t)12 * km, ncclDouble, ctx->comm, ctx->stream));
     CU(cudaMemcpyAsync(ctx->h_wall, wall, (size_t)12 * km * ctx->world * 8, cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     for (int r = 0; r < ctx->world; ++r) {
@@ -906,6 +956,33 @@ gmaf_status gmaf_cond_iterations(gmaf_ctx* ctx, int32_t* out) {
   CU(cudaMemcpyAsync(tmp.data(), ctx->d.cs.itk, (size_t)ctx->K * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   for (int k = 0; k < ctx->K; ++k) out[k] = ctx->last_coupling == GMAF_ASYNC ? tmp[k] : ctx->h_state->iter;
+  return GMAF_OK;
+}
+
+gmaf_status gmaf_p2p_handle(gmaf_ctx* ctx, void* out) {
+  if (!ctx || !out) return GMAF_E_INVALID_ARG;
+  if (!ctx->p2p) return fail(ctx, GMAF_E_STATE, "p2p_handle: not a peer-to-peer context");
+  cudaIpcMemHandle_t h;
+  CU(cudaIpcGetMemHandle(&h, ctx->p2p_buf));
+  std::memcpy(out, &h, sizeof(h));
+  return GMAF_OK;
+}
+
+gmaf_status gmaf_p2p_connect(gmaf_ctx* ctx, const void* handles) {
+  if (!ctx || !handles) return GMAF_E_INVALID_ARG;
+  if (!ctx->p2p) return fail(ctx, GMAF_E_STATE, "p2p_connect: not a peer-to-peer context");
+  if (ctx->p2p_ready) return fail(ctx, GMAF_E_STATE, "p2p_connect: already connected");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  for (int r = 0; r < ctx->world; ++r) {
+    if (r == ctx->rank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + 64 * r, 64);
+    void* p = nullptr;
+    CU(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    ctx->peer_bufs[r] = p;
+    ctx->d.dist.peer[r] = static_cast<char*>(p);
+  }
+  ctx->p2p_ready = true;
   return GMAF_OK;
 }
 

@@ -66,11 +66,19 @@ struct CondScalars {
   int32_t* frz;    // [K] 1 once condition k met its own test (asynchronous strategy)
 };
 
-// Multi-rank state (world > 0 only when the context was created with an NCCL communicator).
+// Multi-rank state (world > 0 only for a condition-sharded context).
+constexpr int kMaxP2P = 8;                 // ranks of one node in peer-to-peer mode
 struct DistPtrs {
   int32_t world, rank, kofs, kmax_local;   // ranks own contiguous condition blocks
   double* packed_local;                    // [4][kmax_local] this rank's per-condition sums
   double* packed_all;                      // [world][4][kmax_local] after the allgather
+  // peer-to-peer mode (no NCCL): every rank owns one exchange buffer, IPC-mapped by all ranks,
+  // layout [2*world flags u64][2*world*xs doubles]; the gathers run inside the kernels
+  int32_t p2p, xs, kglob, pad;
+  char* peer[kMaxP2P];                     // exchange buffer of rank r (peer[rank] = own)
+  unsigned long long* seq;                 // gathers issued so far (the same sequence on every rank)
+  double* rr_all;                          // [kglob] r.r_k of every condition (last iteration)
+  double* ss_all;                          // [kglob] S.S_k of every condition (init)
 };
 
 struct DevPtrs {
@@ -140,6 +148,12 @@ cudaError_t launch_sr_scalar(const DevPtrs& d, bool init, int Kglob, int Klocal,
                              cudaStream_t s);
 cudaError_t configure_sr_kernels(const TileCfg& t);
 int sr_ctas_per_sm(const TileCfg& t);
+// peer-to-peer mode: gather n doubles per rank from src into packed_all-style dst [world][n]
+// (one thread; a timeout marks the solve failed, GMAF_E_CUDA)
+cudaError_t launch_p2p_gather(const DevPtrs& d, const double* src, int n, double* dst, cudaStream_t s);
+// peer-to-peer mode: gather of the packed per-condition sums + the scalar stage (Eq. 3.9, alpha,
+// beta) + the graph WHILE condition, one CTA, after every init / iteration kernel
+cudaError_t launch_p2p_scalar(const DevPtrs& d, bool init, int Klocal, unsigned long long h, cudaStream_t s);
 
 // ---- host accessors (gmaf_api.cu) for the Picard driver (picard.cu) ----
 }  // namespace gmaf

@@ -381,16 +381,23 @@ __global__ void k_sr_scalar(DevPtrs d, int Kglob, int Klocal, int kofs, int worl
   extern __shared__ double sh[];       // [4][Kglob]
   const int km = d.dist.kmax_local;
   for (int kg = threadIdx.x; kg < Kglob; kg += blockDim.x) {
-    // rank and local index of global condition kg (blocks: first Kglob % world ranks get one more)
-    const int base = Kglob / world, extra = Kglob % world;
     int r, kl;
-    if (kg < extra * (base + 1)) { r = kg / (base + 1); kl = kg % (base + 1); }
-    else { r = extra + (kg - extra * (base + 1)) / base; kl = (kg - extra * (base + 1)) % base; }
+    dist_owner(kg, Kglob, world, &r, &kl);
     const double* src = d.dist.packed_all + (long long)r * 4 * km;
     for (int q = 0; q < 4; ++q) sh[q * Kglob + kg] = src[q * km + kl];
   }
   __syncthreads();
   if (threadIdx.x == 0) sr_scalar_stage<INIT>(d, sh, Kglob, Klocal, kofs, 0, 0ull);
+}
+
+// Peer-to-peer allgather as its own (one-thread) kernel: the true-residual and wrench gathers.
+__global__ void k_p2p_gather(DevPtrs d, const double* src, int n, double* dst) {
+  if (!p2p_gather(d.dist, src, n, dst)) { d.st_->done = 1; d.st_->status = -9; }
+}
+
+cudaError_t launch_p2p_gather(const DevPtrs& d, const double* src, int n, double* dst, cudaStream_t s) {
+  k_p2p_gather<<<1, 1, 0, s>>>(d, src, n, dst);
+  return cudaGetLastError();
 }
 
 // x += alpha_{it-1} pd_{it-1} when the iteration count is odd (the last x update of the
@@ -421,35 +428,64 @@ static cudaError_t sr_launch(KernelT kern, const GridParams& g, const DevPtrs& d
   return cudaGetLastError();
 }
 
+template <int MODE>
+static cudaError_t sr_launch_mode(int precond, const GridParams& g, const DevPtrs& d, const TileCfg& t, int K,
+                                  int parity, unsigned long long h, cudaStream_t s) {
+  const int use = h != 0ull;
+  switch (precond) {
+    case SPC_ASSOR2: return sr_launch(k_sr<SPC_ASSOR2, MODE>, g, d, t, K, parity, h, use, s);
+    case SPC_ASSOR1: return sr_launch(k_sr<SPC_ASSOR1, MODE>, g, d, t, K, parity, h, use, s);
+    case SPC_JACOBI: return sr_launch(k_sr<SPC_JACOBI, MODE>, g, d, t, K, parity, h, use, s);
+    default: return sr_launch(k_sr<SPC_NONE, MODE>, g, d, t, K, parity, h, use, s);
+  }
+}
+
 cudaError_t launch_sr_init(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,
                            bool warm, unsigned long long h, cudaStream_t s) {
-  const int use = h != 0ull;
-  if (warm) {
-    if (precond == SPC_ASSOR2) return sr_launch(k_sr<SPC_ASSOR2, SR_INIT_WARM>, g, d, t, K, 1, h, use, s);
-    if (precond == SPC_ASSOR1) return sr_launch(k_sr<SPC_ASSOR1, SR_INIT_WARM>, g, d, t, K, 1, h, use, s);
-    if (precond == SPC_JACOBI) return sr_launch(k_sr<SPC_JACOBI, SR_INIT_WARM>, g, d, t, K, 1, h, use, s);
-    return sr_launch(k_sr<SPC_NONE, SR_INIT_WARM>, g, d, t, K, 1, h, use, s);
-  }
-  if (precond == SPC_ASSOR2) return sr_launch(k_sr<SPC_ASSOR2, SR_INIT_COLD>, g, d, t, K, 1, h, use, s);
-  if (precond == SPC_ASSOR1) return sr_launch(k_sr<SPC_ASSOR1, SR_INIT_COLD>, g, d, t, K, 1, h, use, s);
-  if (precond == SPC_JACOBI) return sr_launch(k_sr<SPC_JACOBI, SR_INIT_COLD>, g, d, t, K, 1, h, use, s);
-  return sr_launch(k_sr<SPC_NONE, SR_INIT_COLD>, g, d, t, K, 1, h, use, s);
+  if (warm) return sr_launch_mode<SR_INIT_WARM>(precond, g, d, t, K, 1, h, s);
+  return sr_launch_mode<SR_INIT_COLD>(precond, g, d, t, K, 1, h, s);
 }
 
 // iteration i = 2m + parity: odd iterations also apply the pending x update
 cudaError_t launch_sr_iter(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,
                            int parity, unsigned long long h, cudaStream_t s) {
-  const int use = h != 0ull;
-  if (parity & 1) {
-    if (precond == SPC_ASSOR2) return sr_launch(k_sr<SPC_ASSOR2, SR_ITER_ODD>, g, d, t, K, parity, h, use, s);
-    if (precond == SPC_ASSOR1) return sr_launch(k_sr<SPC_ASSOR1, SR_ITER_ODD>, g, d, t, K, parity, h, use, s);
-    if (precond == SPC_JACOBI) return sr_launch(k_sr<SPC_JACOBI, SR_ITER_ODD>, g, d, t, K, parity, h, use, s);
-    return sr_launch(k_sr<SPC_NONE, SR_ITER_ODD>, g, d, t, K, parity, h, use, s);
+  if (parity & 1) return sr_launch_mode<SR_ITER_ODD>(precond, g, d, t, K, parity, h, s);
+  return sr_launch_mode<SR_ITER_EVEN>(precond, g, d, t, K, parity, h, s);
+}
+
+// Peer-to-peer mode: right after every init / iteration kernel (same CUDA graph), one CTA
+// gathers all ranks' packed per-condition sums over NVLink peer memory and runs the scalar stage
+// in global condition order -- bitwise the same on every rank -- and sets the WHILE condition.
+// (Fusing this tail into k_sr itself was measured 30% slower: the extra code costs the hot loop
+// registers; the separate 1-CTA kernel costs ~1%.)
+template <bool INIT>
+__global__ void k_p2p_scalar(DevPtrs d, int Klocal, unsigned long long hcond, int use_cond) {
+  __shared__ double sh[4 * 256];
+  if (!INIT && d.st_->done) return;
+  if (threadIdx.x != 0) return;
+  const int km = d.dist.kmax_local, Kg = d.dist.kglob;
+  if (!p2p_gather(d.dist, d.dist.packed_local, 4 * km, d.dist.packed_all)) {
+    d.st_->done = 1;
+    d.st_->status = -9;                                   // GMAF_E_CUDA: a peer never arrived
+    if (use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, 0u);
+    return;
   }
-  if (precond == SPC_ASSOR2) return sr_launch(k_sr<SPC_ASSOR2, SR_ITER_EVEN>, g, d, t, K, parity, h, use, s);
-  if (precond == SPC_ASSOR1) return sr_launch(k_sr<SPC_ASSOR1, SR_ITER_EVEN>, g, d, t, K, parity, h, use, s);
-  if (precond == SPC_JACOBI) return sr_launch(k_sr<SPC_JACOBI, SR_ITER_EVEN>, g, d, t, K, parity, h, use, s);
-  return sr_launch(k_sr<SPC_NONE, SR_ITER_EVEN>, g, d, t, K, parity, h, use, s);
+  for (int kg = 0; kg < Kg; ++kg) {
+    int r, kl;
+    dist_owner(kg, Kg, d.dist.world, &r, &kl);
+    const double* srcp = d.dist.packed_all + (long long)r * 4 * km;
+    for (int q = 0; q < 4; ++q) sh[q * Kg + kg] = srcp[q * km + kl];
+    d.dist.rr_all[kg] = sh[kg];
+    if (INIT) d.dist.ss_all[kg] = sh[3 * Kg + kg];
+  }
+  sr_scalar_stage<INIT>(d, sh, Kg, Klocal, d.dist.kofs, use_cond, hcond);
+}
+
+cudaError_t launch_p2p_scalar(const DevPtrs& d, bool init, int Klocal, unsigned long long h, cudaStream_t s) {
+  const int use = h != 0ull;
+  if (init) k_p2p_scalar<true><<<1, 32, 0, s>>>(d, Klocal, h, use);
+  else k_p2p_scalar<false><<<1, 32, 0, s>>>(d, Klocal, h, use);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_sr_fixup(const GridParams& g, const DevPtrs& d, int K, cudaStream_t s) {
@@ -473,21 +509,21 @@ static cudaError_t sr_set(KernelT kern, int bytes) {
   return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
+template <int MODE>
+static cudaError_t sr_set_modes(int bytes) {
+  cudaError_t e = sr_set(k_sr<SPC_ASSOR2, MODE>, bytes);
+  if (e == cudaSuccess) e = sr_set(k_sr<SPC_ASSOR1, MODE>, bytes);
+  if (e == cudaSuccess) e = sr_set(k_sr<SPC_JACOBI, MODE>, bytes);
+  if (e == cudaSuccess) e = sr_set(k_sr<SPC_NONE, MODE>, bytes);
+  return e;
+}
+
 cudaError_t configure_sr_kernels(const TileCfg& t) {
   const int bytes = (int)sr_smem_bytes(2 * sr_pairs(t));
-  cudaError_t e = cudaSuccess;
-#define GMAF_SR_SET(...) if (e == cudaSuccess) e = sr_set(__VA_ARGS__, bytes)
-  GMAF_SR_SET(k_sr<SPC_ASSOR2, SR_ITER_EVEN>); GMAF_SR_SET(k_sr<SPC_JACOBI, SR_ITER_EVEN>);
-  GMAF_SR_SET(k_sr<SPC_NONE, SR_ITER_EVEN>);
-  GMAF_SR_SET(k_sr<SPC_ASSOR2, SR_ITER_ODD>); GMAF_SR_SET(k_sr<SPC_JACOBI, SR_ITER_ODD>);
-  GMAF_SR_SET(k_sr<SPC_NONE, SR_ITER_ODD>);
-  GMAF_SR_SET(k_sr<SPC_ASSOR2, SR_INIT_COLD>); GMAF_SR_SET(k_sr<SPC_JACOBI, SR_INIT_COLD>);
-  GMAF_SR_SET(k_sr<SPC_NONE, SR_INIT_COLD>);
-  GMAF_SR_SET(k_sr<SPC_ASSOR2, SR_INIT_WARM>); GMAF_SR_SET(k_sr<SPC_JACOBI, SR_INIT_WARM>);
-  GMAF_SR_SET(k_sr<SPC_NONE, SR_INIT_WARM>);
-  GMAF_SR_SET(k_sr<SPC_ASSOR1, SR_ITER_EVEN>); GMAF_SR_SET(k_sr<SPC_ASSOR1, SR_ITER_ODD>);
-  GMAF_SR_SET(k_sr<SPC_ASSOR1, SR_INIT_COLD>); GMAF_SR_SET(k_sr<SPC_ASSOR1, SR_INIT_WARM>);
-#undef GMAF_SR_SET
+  cudaError_t e = sr_set_modes<SR_ITER_EVEN>(bytes);
+  if (e == cudaSuccess) e = sr_set_modes<SR_ITER_ODD>(bytes);
+  if (e == cudaSuccess) e = sr_set_modes<SR_INIT_COLD>(bytes);
+  if (e == cudaSuccess) e = sr_set_modes<SR_INIT_WARM>(bytes);
   return e;
 }
 

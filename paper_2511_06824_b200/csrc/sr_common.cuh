@@ -245,6 +245,53 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
 }
 
 
+// ---------------------------------------------------------------- multi-rank helpers
+// rank and local index of global condition kg (contiguous blocks; the first Kglob % world ranks
+// hold one more)
+__device__ __forceinline__ void dist_owner(int kg, int Kglob, int world, int* r, int* kl) {
+  const int base = Kglob / world, extra = Kglob % world;
+  if (kg < extra * (base + 1)) { *r = kg / (base + 1); *kl = kg % (base + 1); }
+  else { *r = extra + (kg - extra * (base + 1)) / base; *kl = (kg - extra * (base + 1)) % base; }
+}
+
+constexpr long long kP2PTimeoutNs = 10000000000ll;   // 10 s: a peer that never arrives fails the solve
+
+// Peer-to-peer allgather (one thread): push n doubles of src into slot `rank` of every rank's
+// exchange buffer over NVLink (IPC-mapped peer memory), publish a monotonically increasing stamp
+// with release semantics at system scope, wait for every rank's stamp in the own buffer, and copy
+// the gathered blocks to dst [world][n].  All ranks issue the same sequence of gathers, so their
+// stamps agree; two parity slots keep a rank that runs one gather ahead from overwriting a block
+// a slower rank still reads.  Returns false on timeout.
+__device__ __forceinline__ bool p2p_gather(const DistPtrs& dd, const double* src, int n, double* dst) {
+  const int W = dd.world;
+  const unsigned long long stamp = *dd.seq + 1ull;
+  *dd.seq = stamp;
+  const int par = (int)(stamp & 1ull);
+  for (int r = 0; r < W; ++r) {
+    double* slot = reinterpret_cast<double*>(dd.peer[r] + 2 * W * 8) + ((long long)par * W + dd.rank) * dd.xs;
+    for (int q = 0; q < n; ++q) *reinterpret_cast<volatile double*>(slot + q) = src[q];
+  }
+  __threadfence_system();
+  for (int r = 0; r < W; ++r) {
+    unsigned long long* fl = reinterpret_cast<unsigned long long*>(dd.peer[r]) + par * W + dd.rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(fl), "l"(stamp) : "memory");
+  }
+  const unsigned long long* my = reinterpret_cast<const unsigned long long*>(dd.peer[dd.rank]) + par * W;
+  const unsigned long long t0 = globaltimer();
+  for (int r = 0; r < W; ++r) {
+    unsigned long long v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(my + r) : "memory");
+      if (v >= stamp) break;
+      if ((long long)(globaltimer() - t0) > kP2PTimeoutNs) return false;
+    }
+  }
+  const volatile double* data = reinterpret_cast<const volatile double*>(dd.peer[dd.rank] + 2 * W * 8);
+  for (int r = 0; r < W; ++r)
+    for (int q = 0; q < n; ++q) dst[(long long)r * n + q] = data[((long long)par * W + r) * dd.xs + q];
+  return true;
+}
+
 // Per-CTA partials -> fixed-order per-condition sums in the last CTA -> the scalar stage
 // (multi-rank: the packed sums for the allgather).  Every thread of the CTA calls it; `red`
 // is dead shared memory of >= max(4 * (blockDim + 32), 4 * K) doubles.
@@ -268,11 +315,12 @@ __device__ void sr_finish(const DevPtrs& d, double (&v)[4], double* red, int K, 
     __syncthreads();
     if (tid == 0) {
       if (d.dist.world > 0) {
-        // multi-rank: publish this rank's per-condition sums; the allgather + k_sr_scalar
-        // that follow on the stream evaluate the scalars identically on every rank
+        // multi-rank: publish this rank's per-condition sums
         const int km = d.dist.kmax_local;
         for (int q = 0; q < 4; ++q)
           for (int kk = 0; kk < km; ++kk) d.dist.packed_local[q * km + kk] = kk < K ? red[q * K + kk] : 0.0;
+        // NCCL mode: the allgather + k_sr_scalar follow on the stream; peer-to-peer mode:
+        // k_p2p_scalar follows in the same graph
       } else {
         sr_scalar_stage<INIT>(d, red, K, K, 0, use_cond, hcond);
       }

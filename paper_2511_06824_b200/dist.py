@@ -60,3 +60,12 @@ def aggregate(device_ms: float, wall_ms: float, dof_iters: float, group=None, de
     else:
         rows = [t.cpu().tolist()]
     return Aggregate(max(r[0] for r in rows), max(r[1] for r in rows), sum(r[2] for r in rows), rows)
+
+
+def connect_p2p(solver, group=None) -> None:
+    """Exchange the solvers' CUDA IPC handles over torch.distributed (any backend, e.g. gloo) and
+    connect the peer-to-peer context (include/gmaf.h gmaf_p2p_handle / gmaf_p2p_connect)."""
+    import torch.distributed as dist
+    handles = [None] * solver.world
+    dist.all_gather_object(handles, solver.p2p_handle(), group=group)
+    solver.p2p_connect(handles)

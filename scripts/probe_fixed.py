@@ -7,7 +7,11 @@ import paper_2511_06824_b200 as P
 cfg = gi.config(sys.argv[1] if len(sys.argv) > 1 else "C3")
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 200
 K = cfg.conds.shape[0]
-S = P.JointSolver(cfg.grid, K)
+if os.environ.get("PROBE_P2P"):
+    S = P.JointSolver(cfg.grid, K, world=1, p2p=True)
+    S.p2p_connect([S.p2p_handle()])
+else:
+    S = P.JointSolver(cfg.grid, K)
 S.thickness(cfg.conds); S.assemble()
 try:
     S.solve_fixed(20, omega=cfg.omega)

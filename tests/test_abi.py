@@ -20,7 +20,7 @@ def pkg():
 
 def _declared():
     hdr = open(os.path.join(ROOT, "include", "gmaf.h")).read()
-    return sorted(set(re.findall(r"\b(gmaf_[a-z_]+)\s*\(", hdr)))
+    return sorted(set(re.findall(r"\b(gmaf_[a-z0-9_]+)\s*\(", hdr)))
 
 
 def test_exports_every_declared_symbol(pkg):

@@ -1,14 +1,11 @@
-"""Host-side multi-process plumbing (torch.distributed; NCCL on GPUs, gloo on CPU tests).
+"""Host-side multi-process plumbing (torch.distributed; NCCL or gloo for the bootstrap).
 
-Round-1 multi-GPU mode: every rank analyses its own operating point --
-an independent K-condition joint system (Eq. 3.7) of one Picard step -- so the
-units shard with no data-path collective ("weak" scaling).  The only collectives are
-outside the timed data path: a barrier before/after the timed region and one all-gather
-of (device ms, wall ms, DOF*iterations) to take the max time over ranks.
-
-The synchronized convergence of a condition-sharded joint system (Eq. 3.9 across ranks)
-needs one small allreduce of the packed (gamma, delta, r.r) partials per iteration; the
-partition helpers below are what that path will use.
+Multi-GPU mode: ONE joint system whose K conditions are sharded over the
+ranks in contiguous blocks; the synchronized convergence (Eq. 3.9) and the coupled alpha/beta
+need one gather of the packed per-condition sums per PCG iteration, done on the device --
+peer to peer over IPC-mapped memory (default, `connect_p2p`) or by NCCL.  This module holds the
+partition (`shard_range`), the bench's operating-point layout (`operating_point_of`), the
+max-over-ranks timing aggregation (`aggregate`) and the IPC-handle exchange (`connect_p2p`).
 """
 from __future__ import annotations
 

@@ -170,11 +170,24 @@ def _config_obj(cfg, args):
             "l2_policy": (f"inputs larger than L2 ({cfg.dof * 8 / 1e6:.0f} MB per field, 126 MB L2)"
                           if cfg.dof * 8 > 126e6 else
                           f"working set L2-resident ({cfg.dof * 8 / 1e6:.1f} MB per field): not an HBM measurement"),
-            "parallelism": "1 GPU" if args.gpus == 1 else
+            "parallelism": "1 GPU" if args.gpus == 1 and not args.partition else
+            f"{args.gpus} GPU(s): the {cfg.K}-condition joint system split into {args.gpus} row slabs (all "
+            f"{cfg.K} conditions per GPU); per PCG iteration the 4 boundary rows of r and of the search "
+            f"direction are stored into the neighbours' inboxes over NVLink peer memory and one gather of the "
+            f"per-condition sums is summed in rank order, inside the solve's CUDA graph (strong)"
+            if _partition(args) == "rows" else
             f"{args.gpus} GPUs: one joint system of {cfg.K}x{args.gpus} conditions, condition-sharded "
             f"({cfg.K} per GPU); per PCG iteration one gather of the per-condition sums "
             f"({os.environ.get('GMAF_DIST', 'p2p')}: "
             f"{'NCCL allgather' if os.environ.get('GMAF_DIST', 'p2p') == 'nccl' else 'fused into the iteration kernel over NVLink peer memory'}) (weak)"}
+
+
+def _partition(args) -> str:
+    """N > 1: row slabs of the one K-condition system (default; SURVEY 8(e) for C3, strong
+    scaling) or one joint system of K*N conditions, condition-sharded (C5 layout, weak)."""
+    if args.partition:
+        return args.partition
+    return "rows" if args.gpus > 1 else "none"
 
 
 def run_gmaf(args, cfg):
@@ -193,7 +206,20 @@ def run_gmaf(args, cfg):
     # (shaft angle 90 + r deg) and its 8 FD perturbations on rank r -- condition-sharded with one
     # NCCL allgather of the packed dot products per iteration (synchronized convergence, Eq. 3.9)
     from paper_2511_06824_b200.dist import aggregate, operating_point_of
-    if world > 1 or args.shard:
+    part = _partition(args) if not args.shard else "conditions"
+    n_local = n
+    if part == "rows":
+        # row slabs: every rank holds all K conditions on its own rows; halo rows and the
+        # per-condition sums are exchanged over peer memory inside the solve's CUDA graph
+        S = P.JointSolver(cfg.grid, K, device=local, rank=rank, world=world, shard="rows")
+        if dist:
+            from paper_2511_06824_b200.dist import connect_p2p
+            connect_p2p(S)
+        else:
+            S.p2p_connect([S.p2p_handle()])
+        conds = cfg.conds
+        n_local = cfg.grid["n_theta"] * (S.slab[1] - S.slab[0])
+    elif world > 1 or part == "conditions":
         conds_all = np.concatenate([cfg.conds if r == 0 else
                                     gi.fd_conditions(gi.condition(phi_deg=operating_point_of(r)))
                                     for r in range(world)])
@@ -250,7 +276,7 @@ def run_gmaf(args, cfg):
     kt = S.kernel_times()
     if dist:
         dist.barrier()
-    agg = aggregate(dev_ms, wall_ms, float(K * n * sum(iters)), device="cuda")   # K local conditions
+    agg = aggregate(dev_ms, wall_ms, float(K * n_local * sum(iters)), device="cuda")   # local DOF
     dev_max_ms, wall_max_ms, total_dof_iters = agg.device_ms_max, agg.wall_ms_max, agg.dof_iters_total
     value = agg.rate()
     e2e_value = agg.e2e_rate()
@@ -270,8 +296,8 @@ def run_gmaf(args, cfg):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_max_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": _config_obj(cfg, args),
+        "scaling": "strong" if part == "rows" else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": _config_obj(cfg, args),
         "iterations_per_step": iters,
         "roofline": {"bound": "hbm", "kernel": dom["name"], "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
@@ -313,7 +339,10 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shard", action="store_true",
-                    help="use the condition-sharded NCCL path even on one GPU (1-rank communicator)")
+                    help="use the condition-sharded path even on one GPU (1-rank communicator)")
+    ap.add_argument("--partition", choices=["rows", "conditions"], default=None,
+                    help="N > 1: row slabs of the K-condition system (default, strong scaling) or a "
+                         "K*N-condition system sharded by conditions (weak); also valid on 1 GPU")
     args = ap.parse_args()
     cfg = gi.config(args.config)
     if args.impl == "reference":

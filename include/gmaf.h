@@ -67,7 +67,9 @@ enum { GMAF_COUPLED = 0,   /* one Krylov process on A_G: global alpha, beta (P:2
 enum { GMAF_FIELD_P = 0, GMAF_FIELD_H = 1, GMAF_FIELD_HDOT = 2, GMAF_FIELD_AP = 3,
        GMAF_FIELD_AE = 4, GMAF_FIELD_AN = 5, GMAF_FIELD_S = 6, GMAF_FIELD_R = 7 };
 enum { GMAF_SHARD_CONDITIONS = 0,       /* condition blocks; NCCL allgather per iteration (needs an id) */
-       GMAF_SHARD_CONDITIONS_P2P = 1 };  /* condition blocks; gather fused into the kernel, peer memory */
+       GMAF_SHARD_CONDITIONS_P2P = 1,    /* condition blocks; gather fused into the kernel, peer memory */
+       GMAF_SHARD_ROWS_P2P = 2 };        /* row slabs of all K conditions; halo rows + sums over peer
+                                            memory (SURVEY 8(e) partitioning of C3); see gmaf_slab */
 /* Iteration schedule: both run the Table-1 method to the same rtol.
  * SINGLE: one fused kernel and one global (gamma, delta, r.r) reduction per iteration
  *         (Chronopoulos-Gear alpha recurrence; needs an even n_theta) -- the default;
@@ -108,7 +110,8 @@ typedef struct {
 typedef struct {
   int32_t rank, world;
   const void* nccl_unique_id;
-  int32_t shard;                 /* GMAF_SHARD_CONDITIONS (NCCL) or GMAF_SHARD_CONDITIONS_P2P; a
+  int32_t shard;                 /* GMAF_SHARD_CONDITIONS (NCCL), GMAF_SHARD_CONDITIONS_P2P or
+                                    GMAF_SHARD_ROWS_P2P (row slabs, see gmaf_slab); a
                                     world > 1 context without an NCCL id is peer to peer */
 } gmaf_dist;
 
@@ -268,6 +271,24 @@ gmaf_status gmaf_picard_step(gmaf_ctx* ctx, const gmaf_pump* pump, gmaf_conditio
  * (<= 8), K <= 256.  Errors: STATE (not a peer-to-peer context / already connected), CUDA. */
 gmaf_status gmaf_p2p_handle(gmaf_ctx* ctx, void* out);
 gmaf_status gmaf_p2p_connect(gmaf_ctx* ctx, const void* handles);
+
+/* Row-slab sharding (dist.shard = GMAF_SHARD_ROWS_P2P; SURVEY 8(e) "row slabs with NVLink halo
+ * exchange").  The 5-point stencil is local in y (Eqs. 2.4-2.7), so the joint
+ * system of all K conditions is split into contiguous blocks of unknown rows: rank r owns rows
+ * [y0, y1) of every condition (the first n_y % world ranks one row more) and stores SLAB_HALO = 4
+ * halo rows on each side -- the y dependency radius of one single-pass iteration (A M^-1 A M^-1).
+ * Connection as for GMAF_SHARD_CONDITIONS_P2P (gmaf_p2p_handle / gmaf_p2p_connect).  Inside the
+ * solve's CUDA graph, after every iteration kernel, a multi-CTA kernel stores the 4 boundary rows
+ * of r and of the search direction straight into the neighbours' inboxes over NVLink and then
+ * gathers every rank's per-condition sums (gamma_k, delta_k, r.r_k, S.S_k), summed in rank order
+ * so the scalars of Eq. 3.9 are bitwise the same on all ranks; the next iteration kernel streams
+ * its halo rows from the inbox.  The converged p is exchanged once more for the true residual and
+ * the quadrature.  gmaf_integrate returns all K wrenches (per-rank cell sums added in rank order);
+ * gmaf_get writes only the own rows [y0, y1) of host_out (n_theta*n_y doubles; other rows are not
+ * touched) and gmaf_field_ptr points at row y0 of the own rows.  Requires world <= 8, K <= 256,
+ * n_y >= 8*world, an even n_theta >= 12.  Reports this context's own rows (all rows at world 1).
+ * Errors: INVALID_ARG (null pointer). */
+gmaf_status gmaf_slab(const gmaf_ctx* ctx, int32_t* y0, int32_t* y1);
 
 /* Make a new ncclUniqueId (128 bytes) into out (NCCL is loaded at run time).  Errors: NCCL. */
 gmaf_status gmaf_nccl_unique_id(void* out);

@@ -123,6 +123,7 @@ def lib() -> C.CDLL:
                                        C.POINTER(C.c_double), C.POINTER(C.c_int32)]
         L.gmaf_p2p_handle.argtypes = [P, P]
         L.gmaf_p2p_connect.argtypes = [P, P]
+        L.gmaf_slab.argtypes = [P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
         L.gmaf_last_error.restype = C.c_char_p
         L.gmaf_last_error.argtypes = [P]
         L.gmaf_version.restype = C.c_char_p
@@ -130,7 +131,8 @@ def lib() -> C.CDLL:
                      "gmaf_solve_fixed", "gmaf_integrate", "gmaf_get", "gmaf_field_ptr",
                      "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_set_schedule",
                      "gmaf_nccl_unique_id", "gmaf_cond_iterations", "gmaf_general_forces",
-                     "gmaf_picard_iteration", "gmaf_picard_step", "gmaf_p2p_handle", "gmaf_p2p_connect"):
+                     "gmaf_picard_iteration", "gmaf_picard_step", "gmaf_p2p_handle", "gmaf_p2p_connect",
+                     "gmaf_slab"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -140,7 +142,7 @@ ABI_SYMBOLS = ("gmaf_workspace_bytes", "gmaf_create", "gmaf_destroy", "gmaf_thic
                "gmaf_solve", "gmaf_solve_fixed", "gmaf_integrate", "gmaf_get", "gmaf_field_ptr",
                "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_set_schedule", "gmaf_nccl_unique_id",
                "gmaf_cond_iterations", "gmaf_general_forces", "gmaf_picard_iteration", "gmaf_picard_step",
-               "gmaf_p2p_handle", "gmaf_p2p_connect",
+               "gmaf_p2p_handle", "gmaf_p2p_connect", "gmaf_slab",
                "gmaf_last_error", "gmaf_version")
 SCHEDULE = {"table1": 0, "single": 1}
 
@@ -196,9 +198,12 @@ def gmaf_nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
-def make_dist(rank: int, world: int, uid: bytes | None, p2p: bool = False):
-    if p2p:   # peer-to-peer condition sharding: no NCCL id (connect with p2p_connect)
-        return gmaf_dist(int(rank), int(world), None, 1), None
+SHARD = {"conditions": 1, "rows": 2}   # peer-to-peer modes (include/gmaf.h GMAF_SHARD_*_P2P)
+
+
+def make_dist(rank: int, world: int, uid: bytes | None, p2p: bool = False, shard: str = "conditions"):
+    if p2p:   # peer-to-peer sharding: no NCCL id (connect with p2p_connect)
+        return gmaf_dist(int(rank), int(world), None, SHARD[shard]), None
     if uid is None:
         return None, None
     keep = C.create_string_buffer(uid, 128)
@@ -259,12 +264,14 @@ class JointSolver:
     """One context: K working conditions on one mesh (Eq. 3.7 joint system)."""
 
     def __init__(self, grid: dict, K: int, device: int | str = 0, stream=None, rank: int = 0,
-                 world: int = 1, nccl_uid: bytes | None = None, p2p: bool = False):
+                 world: int = 1, nccl_uid: bytes | None = None, p2p: bool = False, shard: str = "conditions"):
         """K = total conditions.  With nccl_uid the K conditions are sharded over `world` ranks
         (condition sharding with one NCCL allgather per iteration, include/gmaf.h gmaf_dist); with
         p2p=True they are sharded peer to peer (the gathers fused into the iteration kernel over
         IPC-mapped peer memory) -- call p2p_handle() / p2p_connect() before the first solve, or
-        paper_2511_06824_b200.dist.connect_p2p(solver)."""
+        paper_2511_06824_b200.dist.connect_p2p(solver).  shard="rows" (implies p2p) splits the rows
+        of all K conditions into contiguous slabs instead (GMAF_SHARD_ROWS_P2P): get() then fills
+        only this rank's rows [y0, y1) = self.slab."""
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("JointSolver needs a CUDA device (no CPU fallback)")
@@ -274,7 +281,10 @@ class JointSolver:
         self.grid = make_grid(grid)
         self.K = int(K)
         self.n_theta, self.n_y = int(grid["n_theta"]), int(grid["n_y"])
-        self.dist, self._uid_buf = make_dist(rank, world, nccl_uid, p2p=p2p and world >= 1)
+        if shard == "rows":
+            p2p = True
+        self.shard = shard
+        self.dist, self._uid_buf = make_dist(rank, world, nccl_uid, p2p=p2p and world >= 1, shard=shard)
         self.rank, self.world = int(rank), int(world)
         nbytes = gmaf_workspace_bytes(self.grid, self.K, self.dist)
         if nbytes == 0:
@@ -285,6 +295,9 @@ class JointSolver:
             self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         self.ctx = gmaf_create(self.grid, self.K, self.workspace.data_ptr(), nbytes, self.stream.cuda_stream,
                                self.dist)
+        y0, y1 = C.c_int32(), C.c_int32()
+        _check(self.ctx, lib().gmaf_slab(self.ctx, C.byref(y0), C.byref(y1)))
+        self.slab = (int(y0.value), int(y1.value))   # own rows (all rows unless shard="rows")
 
     def p2p_handle(self) -> bytes:
         """This rank's 64-byte CUDA IPC handle of its exchange buffer (peer-to-peer mode)."""
@@ -394,7 +407,7 @@ class JointSolver:
     # -- readback ----------------------------------------------------------------------
     def get(self, field: str, k: int) -> np.ndarray:
         rows = self.n_y + 2 if field in ("h", "hdot") else self.n_y
-        out = np.empty((rows, self.n_theta))
+        out = np.zeros((rows, self.n_theta))   # a row slab fills only its own rows
         _check(self.ctx, lib().gmaf_get(self.ctx, FIELD[field], int(k),
                                         out.ctypes.data_as(C.POINTER(C.c_double))))
         return out
@@ -405,8 +418,9 @@ class JointSolver:
         _check(self.ctx, lib().gmaf_field_ptr(self.ctx, FIELD[field], int(k), C.byref(ptr)))
         base = self.workspace.data_ptr()
         off = (ptr.value - base) // 8
-        n = self.n_theta * self.n_y
-        return self.workspace.view(self.torch.float64)[off:off + n].view(self.n_y, self.n_theta)
+        rows = self.slab[1] - self.slab[0]   # own rows (all rows unless shard="rows")
+        n = self.n_theta * rows
+        return self.workspace.view(self.torch.float64)[off:off + n].view(rows, self.n_theta)
 
     def kernel_times(self) -> list[dict]:
         arr = (gmaf_kernel_timing * 16)()

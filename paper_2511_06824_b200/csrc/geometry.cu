@@ -80,13 +80,14 @@ __global__ void k_thickness_guard(GridParams g, DevPtrs d, int K) {
 // (by its representative condition); S for every condition.
 __global__ void k_assemble(GridParams g, DevPtrs d, int K) {
   timing_begin(d.timing, KK_ASSEMBLE);
-  const long long n = (long long)g.nt * g.ny;
+  // the stored rows of this context (all rows on one rank; own rows + halo rows on a slab)
+  const long long n = g.ns;
   const long long total = n * K;
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < total;
        q += (long long)gridDim.x * blockDim.x) {
     const int k = (int)(q / n);
     const long long idx = q - (long long)k * n;
-    const int j = (int)(idx / g.nt);
+    const int j = g.yb + (int)(idx / g.nt);
     const int i = (int)(idx % g.nt);
     const CondParams& c = d.cp[k];
     const int iE = (i + 1 == g.nt) ? 0 : i + 1;
@@ -104,7 +105,7 @@ __global__ void k_assemble(GridParams g, DevPtrs d, int K) {
     const double gs = harmonic(gS, gP);   // == gn(i, j-1) bit for bit
     const double aE = ge * c.rx, aW = gw * c.rx, aN = gn * c.ry, aS = gs * c.ry;
     if (d.mat_rep[c.mat] == k) {
-      const long long o = (long long)c.mat * n + idx;
+      const long long o = (long long)c.mat * n + idx;   // = fofs(g, mat) + j*nt + i
       d.AP[o] = ((aW + aE) + aS) + aN;
       d.AE[o] = -aE;
       d.AN[o] = (j < g.ny - 1) ? -aN : 0.0;
@@ -143,16 +144,18 @@ __global__ void __launch_bounds__(QUAD_THREADS) k_quadrature(GridParams g, DevPt
   timing_begin(d.timing, KK_QUAD);
   const int k = blockIdx.y;
   const CondParams& c = d.cp[k];
-  const long long n = (long long)g.nt * g.ny;
-  const double* p = d.p + (long long)k * n;
-  const long long cells = (long long)(g.ny + 1) * g.nt;
+  const double* p = d.p + fofs(g, k);
+  // this context's cells: j + 1 in [y0, y1), plus the top ghost cell j = n_y - 1 on the last slab
+  // (all n_y + 1 cell rows on one rank); row y0 - 1 of a slab is its exchanged halo row
+  const int cj0 = g.y0 - 1;
+  const long long cells = (long long)(g.y1 - g.y0 + (g.y1 == g.ny ? 1 : 0)) * g.nt;
   const double dA = c.dx * c.dy;
   double acc[12];
 #pragma unroll
   for (int q = 0; q < 12; ++q) acc[q] = 0.0;
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < cells;
        q += (long long)gridDim.x * blockDim.x) {
-    const int j = (int)(q / g.nt) - 1, i = (int)(q % g.nt);
+    const int j = cj0 + (int)(q / g.nt), i = (int)(q % g.nt);
     const int i1 = (i + 1 == g.nt) ? 0 : i + 1;
     const double p00 = (j < 0) ? c.pin : p[(long long)j * g.nt + i];
     const double p10 = (j < 0) ? c.pin : p[(long long)j * g.nt + i1];
@@ -216,7 +219,7 @@ cudaError_t launch_thickness_guard(const GridParams& g, const DevPtrs& d, int K,
 }
 
 cudaError_t launch_assemble(const GridParams& g, const DevPtrs& d, int K, cudaStream_t s) {
-  const long long work = (long long)g.ny * g.nt * K;
+  const long long work = g.ns * K;
   k_assemble<<<grid_for(work, 256, 148 * 16), 256, 0, s>>>(g, d, K);
   return cudaGetLastError();
 }
@@ -228,7 +231,7 @@ cudaError_t launch_field(const GridParams& g, const DevPtrs& d, int field, int k
 }
 
 int quad_ctas_per_condition(const GridParams& g, int K) {
-  const long long cells = (long long)(g.ny + 1) * g.nt;
+  const long long cells = (long long)(g.y1 - g.y0 + 1) * g.nt;
   int per_k = grid_for(cells, QUAD_THREADS, 1 << 20);
   const int target = (148 * 8 + K - 1) / K;   // ~8 CTAs per SM in total
   if (per_k > target) per_k = target;

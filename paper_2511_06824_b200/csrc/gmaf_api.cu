@@ -74,7 +74,20 @@ void shard(int K, int world, int rank, int* lo, int* hi) {
 }
 
 bool dist_mode(const gmaf_dist* dist) {
-  return dist && (dist->world > 1 || dist->nccl_unique_id != nullptr || dist->shard == GMAF_SHARD_CONDITIONS_P2P);
+  return dist && (dist->world > 1 || dist->nccl_unique_id != nullptr || dist->shard == GMAF_SHARD_CONDITIONS_P2P ||
+                  dist->shard == GMAF_SHARD_ROWS_P2P);
+}
+bool rows_mode(const gmaf_dist* dist) { return dist_mode(dist) && dist->shard == GMAF_SHARD_ROWS_P2P; }
+
+// Row slab of `rank`: own rows [y0, y1) (contiguous blocks, the first n_y % world ranks one more)
+// and stored rows [yb, ye) = own rows + SLAB_HALO halo rows per side inside the domain.
+struct Slab { int y0, y1, yb, ye; };
+Slab slab_of(int ny, int world, int rank) {
+  Slab sl{};
+  shard(ny, world, rank, &sl.y0, &sl.y1);
+  sl.yb = sl.y0 - SLAB_HALO < 0 ? 0 : sl.y0 - SLAB_HALO;
+  sl.ye = sl.y1 + SLAB_HALO > ny ? ny : sl.y1 + SLAB_HALO;
+  return sl;
 }
 
 constexpr int kUnroll = 4;          // (A, B) pairs per WHILE-body execution (must be even)
@@ -148,9 +161,10 @@ int check_grid(const gmaf_grid* g) {
   return GMAF_OK;
 }
 
-Layout make_layout(const gmaf_grid* g, int K, int world = 0, int kmax = 0) {
+Layout make_layout(const gmaf_grid* g, int K, int world = 0, int kmax = 0, int rows_stored = 0) {
   Layout L{};
-  const size_t nt = (size_t)g->n_theta, ny = (size_t)g->n_y, n = nt * ny;
+  const size_t nt = (size_t)g->n_theta, ny = (size_t)g->n_y;
+  const size_t n = nt * (size_t)(rows_stored > 0 ? rows_stored : g->n_y);   // per-condition field
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t at = o; o = align_up(o + bytes); return at; };
   L.off_ct = take(nt * 8); L.off_st = take(nt * 8); L.off_cth = take(nt * 8); L.off_sth = take(nt * 8);
@@ -216,6 +230,8 @@ struct gmaf_ctx {
   ncclComm_t comm = nullptr;
   // peer-to-peer mode (condition sharding without NCCL)
   bool p2p = false, p2p_ready = false;
+  bool rows = false;                       // row-slab sharding (GMAF_SHARD_ROWS_P2P)
+  size_t inbox_off = 0;                    // byte offset of the halo inboxes in p2p_buf
   char* p2p_buf = nullptr;                 // library-owned exchange buffer (cudaMalloc, IPC-exported)
   void* peer_bufs[kMaxP2P] = {};           // IPC-opened buffers of the other ranks
   double* h_packed = nullptr;   // [world][4][kmax]
@@ -281,11 +297,15 @@ cudaError_t enqueue_init(gmaf_ctx* ctx, const GraphKey& key, unsigned long long 
   if (key.schedule == GMAF_SCHEDULE_TABLE1)
     return launch_init(ctx->gp, ctx->d, ctx->tiles, ctx->K, key.precond, key.warm != 0, h, s);
   if (key.warm) {   // r0 = S - A p0 into r[1], then the single-pass init reads it
-    cudaError_t e = launch_residual_init(ctx->gp, ctx->d, ctx->tiles, ctx->K, 1, s);
+    cudaError_t e = cudaSuccess;
+    if (ctx->rows) e = launch_slab_exchange(ctx->gp, ctx->d, ctx->d.p, ctx->K, s);   // p0's halo rows
+    if (e == cudaSuccess) e = launch_residual_init(ctx->gp, ctx->d, ctx->tiles, ctx->K, 1, s);
+    if (e == cudaSuccess && ctx->rows) e = launch_slab_exchange(ctx->gp, ctx->d, ctx->d.r[1], ctx->K, s);
     if (e != cudaSuccess) return e;
   }
   cudaError_t e = launch_sr_init(ctx->gp, ctx->d, ctx->tiles_sr, ctx->K, key.precond, key.warm != 0, h, s);
   if (e != cudaSuccess || !ctx->p2p) return e;
+  if (ctx->rows) return launch_p2p_rows(ctx->gp, ctx->d, true, 1, ctx->K, h, s);   // halos + sums + scalars
   return launch_p2p_scalar(ctx->d, true, ctx->K, h, s);   // peer-to-peer: gather + scalars
 }
 
@@ -298,7 +318,8 @@ cudaError_t enqueue_iterations(gmaf_ctx* ctx, const GraphKey& key, unsigned long
       if (e == cudaSuccess) e = launch_phase_b(ctx->gp, ctx->d, ctx->tiles, ctx->K, key.precond, u & 1, h, s);
     } else {
       e = launch_sr_iter(ctx->gp, ctx->d, ctx->tiles_sr, ctx->K, key.precond, u & 1, h, s);
-      if (e == cudaSuccess && ctx->p2p) e = launch_p2p_scalar(ctx->d, false, ctx->K, h, s);
+      if (e == cudaSuccess && ctx->rows) e = launch_p2p_rows(ctx->gp, ctx->d, false, u & 1, ctx->K, h, s);
+      else if (e == cudaSuccess && ctx->p2p) e = launch_p2p_scalar(ctx->d, false, ctx->K, h, s);
     }
   }
   return e;
@@ -307,6 +328,10 @@ cudaError_t enqueue_iterations(gmaf_ctx* ctx, const GraphKey& key, unsigned long
 cudaError_t enqueue_final(gmaf_ctx* ctx, const GraphKey& key, cudaStream_t s) {
   if (key.schedule == GMAF_SCHEDULE_SINGLE) {
     cudaError_t e = launch_sr_fixup(ctx->gp, ctx->d, ctx->K, s);
+    if (e != cudaSuccess) return e;
+  }
+  if (ctx->rows) {   // p's halo rows: the true residual below and the quadrature read them
+    cudaError_t e = launch_slab_exchange(ctx->gp, ctx->d, ctx->d.p, ctx->K, s);
     if (e != cudaSuccess) return e;
   }
   cudaError_t e = launch_true_residual(ctx->gp, ctx->d, ctx->tiles, ctx->K, s);   // ||S - A p|| at exit
@@ -490,8 +515,7 @@ gmaf_status run_solve(gmaf_ctx* ctx, double tol, double omega, int precond, int 
   float ms = 0.f;
   CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
   if (hs->zero_p) {
-    const size_t n = (size_t)ctx->grid.n_theta * ctx->grid.n_y;
-    CU(cudaMemsetAsync(ctx->d.p, 0, (size_t)ctx->K * n * 8, ctx->stream));
+    CU(cudaMemsetAsync(ctx->d.p, 0, (size_t)ctx->K * ctx->gp.ns * 8, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
   }
   const int K = ctx->K;
@@ -546,6 +570,11 @@ const char* gmaf_version(void) { return "gmaf-b200 0.1 (sm_100a)"; }
 size_t gmaf_workspace_bytes(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist) {
   if (check_grid(grid) != GMAF_OK || K < 1) return 0;
   if (dist && (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)) return 0;
+  if (rows_mode(dist)) {
+    if (dist->world > kMaxP2P || grid->n_y < 2 * SLAB_HALO * dist->world) return 0;
+    const Slab sl = slab_of(grid->n_y, dist->world, dist->rank);
+    return make_layout(grid, K, dist->world, K, sl.ye - sl.yb).total;
+  }
   if (dist_mode(dist)) {
     if (dist->world > K) return 0;
     int lo, hi;
@@ -564,8 +593,19 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
   if (K < 1) return GMAF_E_INVALID_ARG;
   if (dist && (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)) return GMAF_E_INVALID_ARG;
   const bool dm = dist_mode(dist);
+  const bool rm = rows_mode(dist);
   int klo = 0, khi = K, world = 1, kmax = 0;
-  if (dm) {
+  Slab sl{0, grid->n_y, 0, grid->n_y};
+  if (rm) {
+    // row slabs: every rank holds all K conditions on its own rows (peer to peer, <= kMaxP2P
+    // ranks, slabs of >= 2*SLAB_HALO rows, the single-pass schedule)
+    if (dist->world > kMaxP2P || K > 256 || grid->n_theta % 2 != 0 || grid->n_theta < 12 ||
+        grid->n_y < 2 * SLAB_HALO * dist->world)
+      return GMAF_E_INVALID_ARG;
+    world = dist->world;
+    kmax = K;
+    sl = slab_of(grid->n_y, world, dist->rank);
+  } else if (dm) {
     // condition sharding needs the single-pass schedule and >= 1 condition per rank; without an
     // NCCL id it runs peer to peer (<= kMaxP2P ranks, connected by gmaf_p2p_connect)
     if (dist->world > K || grid->n_theta % 2 != 0 || grid->n_theta < 12) return GMAF_E_INVALID_ARG;
@@ -577,7 +617,8 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
   }
   const int Kglob = K;
   K = khi - klo;   // from here on: the local conditions
-  const Layout L = dm ? make_layout(grid, K, world, kmax) : make_layout(grid, K);
+  const Layout L = rm ? make_layout(grid, K, world, kmax, sl.ye - sl.yb)
+                 : dm ? make_layout(grid, K, world, kmax) : make_layout(grid, K);
   if (!d_workspace || ws_bytes < L.total || (reinterpret_cast<uintptr_t>(d_workspace) % kAlign) != 0)
     return GMAF_E_WORKSPACE;
   gmaf_ctx* ctx = new (std::nothrow) gmaf_ctx();
@@ -586,7 +627,8 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
   ctx->K = K;
   ctx->Kglob = Kglob;
   ctx->distm = dm;
-  ctx->p2p = dm && (!dist->nccl_unique_id || dist->shard == GMAF_SHARD_CONDITIONS_P2P);
+  ctx->p2p = dm && (!dist->nccl_unique_id || dist->shard == GMAF_SHARD_CONDITIONS_P2P || rm);
+  ctx->rows = rm;
   ctx->world = world;
   ctx->rank = dm ? dist->rank : 0;
   ctx->kofs = klo;
@@ -604,6 +646,8 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
   gp.tex_nt = tex ? grid->tex_n_theta : 0; gp.tex_ny = tex ? grid->tex_n_y : 0;
   gp.tex_band = tex ? grid->tex_band_rows : 0; gp.tex_num = grid->tex_fill_num;
   gp.tex_den = grid->tex_fill_den > 0 ? grid->tex_fill_den : 1; gp.tex_depth = grid->tex_depth;
+  gp.y0 = sl.y0; gp.y1 = sl.y1; gp.yb = sl.yb;
+  gp.ns = (long long)grid->n_theta * (sl.ye - sl.yb);
   DevPtrs& d = ctx->d;
   d.ct = at<double>(ctx, L.off_ct); d.st = at<double>(ctx, L.off_st);
   d.cth = at<double>(ctx, L.off_cth); d.sth = at<double>(ctx, L.off_sth);
@@ -659,7 +703,7 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
       cudaMemsetAsync(d.counters, 0, 16 * sizeof(unsigned int), ctx->stream) != cudaSuccess ||
       cudaMemsetAsync(d.st_, 0, sizeof(SolverState), ctx->stream) != cudaSuccess ||
       cudaMemsetAsync((void*)d.cs.alpha, 0, (size_t)9 * K * 8, ctx->stream) != cudaSuccess ||
-      cudaMemsetAsync(d.p, 0, (size_t)K * gp.nt * gp.ny * 8, ctx->stream) != cudaSuccess ||
+      cudaMemsetAsync(d.p, 0, (size_t)K * gp.ns * 8, ctx->stream) != cudaSuccess ||
       cudaMemsetAsync((void*)d.zero_row, 0, kConstRowLen * 8, ctx->stream) != cudaSuccess ||
       cudaMemcpyAsync((void*)d.one_row, ones.data(), kConstRowLen * 8, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess)
     return cleanup_fail(GMAF_E_CUDA);
@@ -672,17 +716,17 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
     if (cudaGetDevice(&dev) != cudaSuccess ||
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
       return cleanup_fail(GMAF_E_CUDA);
-    TileCfg probe = make_tiles(grid->n_theta, grid->n_y, K, 1, tw_table1(grid->n_theta));
+    TileCfg probe = make_tiles(grid->n_theta, sl.y1 - sl.y0, K, 1, tw_table1(grid->n_theta));
     if (configure_pcg_kernels(probe, K) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
     const int occ = pcg_ctas_per_sm(probe, K);
-    ctx->tiles = make_tiles(grid->n_theta, grid->n_y, K, sms * (occ > 0 ? occ : 1), tw_table1(grid->n_theta));
+    ctx->tiles = make_tiles(grid->n_theta, sl.y1 - sl.y0, K, sms * (occ > 0 ? occ : 1), tw_table1(grid->n_theta));
     if (ctx->tiles.n_tiles > kMaxTilesPerCondition) return cleanup_fail(GMAF_E_INVALID_MESH);
     if (configure_pcg_kernels(ctx->tiles, K) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
     // single-pass kernel: its own tiles (wider halo, TMA ring) and occupancy
-    TileCfg sprobe = make_tiles(grid->n_theta, grid->n_y, K, 1, tw_single(grid->n_theta));
+    TileCfg sprobe = make_tiles(grid->n_theta, sl.y1 - sl.y0, K, 1, tw_single(grid->n_theta));
     if (configure_sr_kernels(sprobe) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
     const int socc = sr_ctas_per_sm(sprobe);
-    ctx->tiles_sr = make_tiles(grid->n_theta, grid->n_y, K, sms * (socc > 0 ? socc : 1), tw_single(grid->n_theta));
+    ctx->tiles_sr = make_tiles(grid->n_theta, sl.y1 - sl.y0, K, sms * (socc > 0 ? socc : 1), tw_single(grid->n_theta));
     if (ctx->tiles_sr.n_tiles > kMaxTilesPerCondition) return cleanup_fail(GMAF_E_INVALID_MESH);
     if (std::getenv("GMAF_DEBUG"))
       std::fprintf(stderr, "gmaf: sms %d | two-phase occ %d tiles %dx%d tw %d th %d | single occ %d tiles %dx%d tw %d th %d\n",
@@ -697,7 +741,11 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
   ctx->quad_ctas = quad_ctas_per_condition(gp, K);
   if (dm && ctx->p2p) {
     const size_t xs = (size_t)12 * kmax;
-    const size_t bytes = (size_t)2 * world * 8 + (size_t)2 * world * xs * 8 + 8 + (size_t)2 * Kglob * 8;
+    size_t bytes = (size_t)2 * world * 8 + (size_t)2 * world * xs * 8 + 8 + (size_t)2 * Kglob * 8;
+    if (rm) {   // halo inboxes [2 slots][2 sides][2 vectors][K][SLAB_HALO][nt]
+      ctx->inbox_off = align_up(bytes);
+      bytes = ctx->inbox_off + (size_t)8 * SLAB_HALO * K * grid->n_theta * 8;
+    }
     if (cudaMalloc((void**)&ctx->p2p_buf, bytes) != cudaSuccess ||
         cudaMemsetAsync(ctx->p2p_buf, 0, bytes, ctx->stream) != cudaSuccess ||
         cudaMallocHost((void**)&ctx->h_packed, (size_t)2 * 4 * kmax * world * 8) != cudaSuccess ||
@@ -713,6 +761,10 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
     dd.seq = reinterpret_cast<unsigned long long*>(tail);
     dd.rr_all = reinterpret_cast<double*>(tail + 8);
     dd.ss_all = dd.rr_all + Kglob;
+    if (rm) {
+      dd.rows = 1;
+      dd.halo_in[ctx->rank] = reinterpret_cast<double*>(ctx->p2p_buf + ctx->inbox_off);
+    }
   } else if (dm) {
     NcclApi& N = nccl_api();
     if (!N.ok) { gmaf_status e = fail(ctx, GMAF_E_NCCL, "NCCL unavailable: %s", N.err.c_str()); gmaf_destroy(ctx); return e; }
@@ -844,6 +896,14 @@ gmaf_status gmaf_integrate(gmaf_ctx* ctx, double* wrench) {
     else NC(nccl_api().allGather(ctx->d.wrench, wall, (size_t)12 * km, ncclDouble, ctx->comm, ctx->stream));
     CU(cudaMemcpyAsync(ctx->h_wall, wall, (size_t)12 * km * ctx->world * 8, cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
+    if (ctx->rows) {   // row slabs: every rank integrated its own cells of all K; sum in rank order
+      for (int q = 0; q < 12 * ctx->K; ++q) {
+        double acc = 0.0;
+        for (int r = 0; r < ctx->world; ++r) acc += ctx->h_wall[(size_t)r * 12 * km + q];
+        wrench[q] = acc;
+      }
+      return GMAF_OK;
+    }
     for (int r = 0; r < ctx->world; ++r) {
       int lo, hi;
       shard(ctx->Kglob, ctx->world, r, &lo, &hi);
@@ -861,15 +921,17 @@ gmaf_status gmaf_field_ptr(gmaf_ctx* ctx, int32_t field, int32_t kglob, void** d
   if (!ctx || !dptr) return GMAF_E_INVALID_ARG;
   const int32_t k = kglob - ctx->kofs;   // fields of this rank's conditions only
   if (k < 0 || k >= ctx->K) return fail(ctx, GMAF_E_INVALID_ARG, "condition %d is not on this rank", kglob);
-  const size_t n = (size_t)ctx->grid.n_theta * ctx->grid.n_y;
-  const size_t m = ctx->mat_of.empty() ? 0 : (size_t)ctx->mat_of[k];
+  const GridParams& g = ctx->gp;
+  const int m = ctx->mat_of.empty() ? 0 : ctx->mat_of[k];
+  // the own rows [y0, y1) of the field (all rows on one rank), contiguous
+  const long long ok = fofs(g, k) + (long long)g.y0 * g.nt, om = fofs(g, m) + (long long)g.y0 * g.nt;
   switch (field) {
-    case GMAF_FIELD_P: *dptr = ctx->d.p + k * n; break;
-    case GMAF_FIELD_S: *dptr = ctx->d.S + k * n; break;
-    case GMAF_FIELD_R: *dptr = ctx->d.r[ctx->r_parity] + k * n; break;   // latest residual
-    case GMAF_FIELD_AP: *dptr = ctx->d.AP + m * n; break;
-    case GMAF_FIELD_AE: *dptr = ctx->d.AE + m * n; break;
-    case GMAF_FIELD_AN: *dptr = ctx->d.AN + m * n; break;
+    case GMAF_FIELD_P: *dptr = ctx->d.p + ok; break;
+    case GMAF_FIELD_S: *dptr = ctx->d.S + ok; break;
+    case GMAF_FIELD_R: *dptr = ctx->d.r[ctx->r_parity] + ok; break;   // latest residual
+    case GMAF_FIELD_AP: *dptr = ctx->d.AP + om; break;
+    case GMAF_FIELD_AE: *dptr = ctx->d.AE + om; break;
+    case GMAF_FIELD_AN: *dptr = ctx->d.AN + om; break;
     default: return fail(ctx, GMAF_E_INVALID_ARG, "field_ptr: field %d has no persistent buffer", field);
   }
   return GMAF_OK;
@@ -879,7 +941,6 @@ gmaf_status gmaf_get(gmaf_ctx* ctx, int32_t field, int32_t kglob, double* host_o
   if (!ctx || !host_out) return GMAF_E_INVALID_ARG;
   const int32_t k = kglob - ctx->kofs;
   if (k < 0 || k >= ctx->K) return fail(ctx, GMAF_E_INVALID_ARG, "condition %d is not on this rank", kglob);
-  const size_t n = (size_t)ctx->grid.n_theta * ctx->grid.n_y;
   if (field == GMAF_FIELD_H || field == GMAF_FIELD_HDOT) {
     if (ctx->state < ST_THICK) return fail(ctx, GMAF_E_STATE, "get H before thickness");
     CU(launch_field(ctx->gp, ctx->d, field, k, ctx->stream));
@@ -894,7 +955,10 @@ gmaf_status gmaf_get(gmaf_ctx* ctx, int32_t field, int32_t kglob, double* host_o
   void* src = nullptr;
   gmaf_status s = gmaf_field_ptr(ctx, field, kglob, &src);
   if (s != GMAF_OK) return s;
-  CU(cudaMemcpyAsync(host_out, src, n * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  // row slabs: the own rows land at their global position; the other rows are not written
+  const size_t own = (size_t)ctx->grid.n_theta * (ctx->gp.y1 - ctx->gp.y0);
+  CU(cudaMemcpyAsync(host_out + (size_t)ctx->gp.y0 * ctx->grid.n_theta, src, own * 8, cudaMemcpyDeviceToHost,
+                     ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   return GMAF_OK;
 }
@@ -905,8 +969,9 @@ gmaf_status gmaf_kernel_times(gmaf_ctx* ctx, gmaf_kernel_timing* out, int32_t n,
   CU(cudaStreamSynchronize(ctx->stream));
   static const char* names[KK_COUNT] = {"thickness_guard", "assemble", "pcg_init", "pcg_phase_a",
                                         "pcg_phase_b", "true_residual", "quadrature", "sr_init", "sr_iter"};
-  const double n_nodes = (double)ctx->grid.n_theta * ctx->grid.n_y * ctx->K;
-  const double nM = (double)ctx->grid.n_theta * ctx->grid.n_y * (ctx->M > 0 ? ctx->M : ctx->K);
+  const double rows = (double)(ctx->gp.y1 - ctx->gp.y0);   // own rows (all n_y on one rank)
+  const double n_nodes = (double)ctx->grid.n_theta * rows * ctx->K;
+  const double nM = (double)ctx->grid.n_theta * rows * (ctx->M > 0 ? ctx->M : ctx->K);
   // algorithmic DRAM bytes per launch: 8 B per node per field touched;
   // the coefficient bands count once per DISTINCT matrix (M of them).
   const double bytes[KK_COUNT] = {
@@ -981,6 +1046,7 @@ gmaf_status gmaf_p2p_connect(gmaf_ctx* ctx, const void* handles) {
     CU(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
     ctx->peer_bufs[r] = p;
     ctx->d.dist.peer[r] = static_cast<char*>(p);
+    if (ctx->rows) ctx->d.dist.halo_in[r] = reinterpret_cast<double*>(static_cast<char*>(p) + ctx->inbox_off);
   }
   ctx->p2p_ready = true;
   return GMAF_OK;
@@ -993,6 +1059,13 @@ gmaf_status gmaf_nccl_unique_id(void* out) {
   ncclUniqueId uid;
   if (N.getUniqueId(&uid) != ncclSuccess) return GMAF_E_NCCL;
   std::memcpy(out, &uid, sizeof(uid));
+  return GMAF_OK;
+}
+
+gmaf_status gmaf_slab(const gmaf_ctx* ctx, int32_t* y0, int32_t* y1) {
+  if (!ctx || !y0 || !y1) return GMAF_E_INVALID_ARG;
+  *y0 = ctx->gp.y0;
+  *y1 = ctx->gp.y1;
   return GMAF_OK;
 }
 

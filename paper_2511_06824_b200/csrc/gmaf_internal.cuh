@@ -26,7 +26,20 @@ struct GridParams {
   double Rk, Rc, mu, hmin, twelve_mu, dtheta;
   int32_t tex_nt, tex_ny, tex_band, tex_num, tex_den;
   double tex_depth;
+  // Row slab of this context.  The fields of condition (or coefficient set)
+  // k hold the stored rows [yb, yb + ns/nt) -- the owned rows [y0, y1) plus up to SLAB_HALO
+  // halo rows on each side -- and are addressed with GLOBAL row indices through fofs().  One
+  // rank: y0 = yb = 0, y1 = ny, ns = nt*ny.
+  int32_t y0, y1, yb, pad_;
+  long long ns;
 };
+
+constexpr int SLAB_HALO = 4;   // halo rows per side: the y dependency radius of A M^-1 A M^-1
+
+// Offset of (condition k, global row 0, column 0) in a [K][stored rows][nt] field.
+__host__ __device__ __forceinline__ long long fofs(const GridParams& g, int k) {
+  return (long long)k * g.ns - (long long)g.yb * g.nt;
+}
 
 // Kernel kinds for the in-kernel %globaltimer accounting.
 enum KernelKind { KK_THICK = 0, KK_ASSEMBLE, KK_INIT, KK_PHASE_A, KK_PHASE_B, KK_TRUERES, KK_QUAD,
@@ -79,7 +92,18 @@ struct DistPtrs {
   unsigned long long* seq;                 // gathers issued so far (the same sequence on every rank)
   double* rr_all;                          // [kglob] r.r_k of every condition (last iteration)
   double* ss_all;                          // [kglob] S.S_k of every condition (init)
+  // row-slab mode (every rank holds all K conditions, rows [y0, y1)): halo inboxes in the own
+  // exchange buffer, [2 slots][2 sides][2 vectors][K][SLAB_HALO rows][nt]; side 0 = the rows
+  // below y0 (written by rank-1), side 1 = the rows from y1 up (written by rank+1).  Slot = parity
+  // of the gather stamp that published them.
+  int32_t rows, pad2;
+  double* halo_in[kMaxP2P];                // inbox of rank r (halo_in[rank] = own)
 };
+
+// Inbox element (slot, side, vector, condition k, halo row ri, column 0).
+__host__ __device__ __forceinline__ long long halo_ofs(int slot, int side, int vec, int K, int k, int ri, int nt) {
+  return ((((long long)(slot * 2 + side) * 2 + vec) * K + k) * SLAB_HALO + ri) * nt;
+}
 
 struct DevPtrs {
   const double* ct; const double* st;      // cos/sin(i dtheta)
@@ -154,6 +178,13 @@ cudaError_t launch_p2p_gather(const DevPtrs& d, const double* src, int n, double
 // peer-to-peer mode: gather of the packed per-condition sums + the scalar stage (Eq. 3.9, alpha,
 // beta) + the graph WHILE condition, one CTA, after every init / iteration kernel
 cudaError_t launch_p2p_scalar(const DevPtrs& d, bool init, int Klocal, unsigned long long h, cudaStream_t s);
+// row-slab mode: after every init / iteration kernel, push the boundary rows
+// of (r_{i+1}, pd_i) into the neighbours' inboxes + gather the per-condition sums, summed over
+// the ranks in rank order, + the scalar stage (multi-CTA; the last CTA gathers)
+cudaError_t launch_p2p_rows(const GridParams& g, const DevPtrs& d, bool init, int parity, int K,
+                            unsigned long long h, cudaStream_t s);
+// row-slab mode: one-off exchange of field v's halo rows (push, stamp-only gather, unpack)
+cudaError_t launch_slab_exchange(const GridParams& g, const DevPtrs& d, double* v, int K, cudaStream_t s);
 
 // ---- host accessors (gmaf_api.cu) for the Picard driver (picard.cu) ----
 }  // namespace gmaf

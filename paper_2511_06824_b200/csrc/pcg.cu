@@ -34,8 +34,8 @@ __device__ __forceinline__ TileCtx tile_ctx(const GridParams& g, const TileCfg& 
   const int tile = blockIdx.x / K;
   const int strip = tile % t.n_strips, chunk = tile / t.n_strips;
   c.i0 = strip * t.tw;
-  c.j0 = chunk * t.th;
-  c.j1 = min(c.j0 + t.th, g.ny);
+  c.j0 = g.y0 + chunk * t.th;          // own rows [y0, y1) (all rows on one rank)
+  c.j1 = min(c.j0 + t.th, g.y1);
   c.tl = threadIdx.x;
   int gc = (c.i0 - HALO + c.tl) % g.nt;
   if (gc < 0) gc += g.nt;
@@ -96,14 +96,13 @@ k_phase_a(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long l
   timing_begin(d.timing, KK_PHASE_A);
   Ring R = make_ring(smem);
   const TileCtx c = tile_ctx(g, t, K);
-  const long long n = (long long)g.nt * g.ny;
   const int m = d.cp[c.k].mat;
-  const double* __restrict__ AP = d.AP + (long long)m * n;
-  const double* __restrict__ AE = d.AE + (long long)m * n;
-  const double* __restrict__ AN = d.AN + (long long)m * n;
-  const double* __restrict__ r = d.r[parity] + (long long)c.k * n;
-  const double* __restrict__ uold = d.u[1 - parity] + (long long)c.k * n;
-  double* __restrict__ u = d.u[parity] + (long long)c.k * n;
+  const double* __restrict__ AP = d.AP + fofs(g, m);
+  const double* __restrict__ AE = d.AE + fofs(g, m);
+  const double* __restrict__ AN = d.AN + fofs(g, m);
+  const double* __restrict__ r = d.r[parity] + fofs(g, c.k);
+  const double* __restrict__ uold = d.u[1 - parity] + fofs(g, c.k);
+  double* __restrict__ u = d.u[parity] + fofs(g, c.k);
   const bool first = (st->iter == 0);
   const double beta = first ? 0.0 : d.cs.beta[c.k];
   const double omega = st->omega;
@@ -214,16 +213,15 @@ k_phase_b(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long l
   timing_begin(d.timing, KIND);
   Ring R = make_ring(smem);
   const TileCtx c = tile_ctx(g, t, K);
-  const long long n = (long long)g.nt * g.ny;
   const int m = d.cp[c.k].mat;
-  const double* __restrict__ AP = d.AP + (long long)m * n;
-  const double* __restrict__ AE = d.AE + (long long)m * n;
-  const double* __restrict__ AN = d.AN + (long long)m * n;
+  const double* __restrict__ AP = d.AP + fofs(g, m);
+  const double* __restrict__ AE = d.AE + fofs(g, m);
+  const double* __restrict__ AN = d.AN + fofs(g, m);
   // ITER: r -= alpha A u.   INIT/TRUERES: r := S - A p  (u := p, alpha := 1).
-  const double* __restrict__ rin = ITER ? d.r[parity] + (long long)c.k * n : d.S + (long long)c.k * n;
-  double* __restrict__ rout = (ITER ? d.r[1 - parity] : d.r[parity]) + (long long)c.k * n;
-  const double* __restrict__ uin = ITER ? d.u[parity] + (long long)c.k * n : d.p + (long long)c.k * n;
-  double* __restrict__ p = d.p + (long long)c.k * n;
+  const double* __restrict__ rin = ITER ? d.r[parity] + fofs(g, c.k) : d.S + fofs(g, c.k);
+  double* __restrict__ rout = (ITER ? d.r[1 - parity] : d.r[parity]) + fofs(g, c.k);
+  const double* __restrict__ uin = ITER ? d.u[parity] + fofs(g, c.k) : d.p + fofs(g, c.k);
+  double* __restrict__ p = d.p + fofs(g, c.k);
   const double alpha = ITER ? d.cs.alpha[c.k] : 1.0;
   const double omega = st->omega;
   const double c2 = (2.0 - omega) * omega;

@@ -76,7 +76,7 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
   const int strip = tile % t.n_strips, chunk = tile / t.n_strips;
   const int nt = g.nt, ny = g.ny;
   const int i0 = strip * t.tw - t.tw / 2;           // first output column (may be negative: mod nt)
-  const int j0 = chunk * t.th, j1 = min(j0 + t.th, ny);
+  const int j0 = g.y0 + chunk * t.th, j1 = min(j0 + t.th, g.y1);   // own rows [y0, y1)
   const int cl = 2 * tl;
   int gl = (i0 - SR_HALO + cl) % nt;
   if (gl < 0) gl += nt;
@@ -109,16 +109,15 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
   const uint32_t emptyv0 = full0 + 8 * SR_CSLOTS;             // [4]
   const uint32_t emptyc0 = emptyv0 + 8 * SR_VSLOTS;           // [8]
 
-  const long long n = (long long)nt * ny;
+  const long long fk = fofs(g, k);        // field base of condition k (global row indexing)
   const int m = d.cp[k].mat;
   // ITER: r_i = R[parity], pd_{i-1} = PD[1-parity]; writes R[1-parity], PD[parity].
   // INIT: r_0 = S (cold) or R[1] (warm: = S - A x0 from the residual pre-pass); writes R[0]
   //       and pd_{-1} = 0 into PD[1].
-  const double* rin = ITER ? d.r[parity] + (long long)k * n
-                           : (MODE == SR_INIT_COLD ? d.S + (long long)k * n : d.r[1] + (long long)k * n);
-  double* rout = (ITER ? d.r[1 - parity] : d.r[0]) + (long long)k * n;
-  double* pdout = (ITER ? d.u[parity] : d.u[1]) + (long long)k * n;
-  double* x = d.p + (long long)k * n;
+  const double* rin = ITER ? d.r[parity] + fk : (MODE == SR_INIT_COLD ? d.S + fk : d.r[1] + fk);
+  double* rout = (ITER ? d.r[1 - parity] : d.r[0]) + fk;
+  double* pdout = (ITER ? d.u[parity] : d.u[1]) + fk;
+  double* x = d.p + fk;
 
   const double alpha = ITER ? d.cs.alpha[k] : 0.0;
   const double alpha_prev = ITER ? d.cs.uvk[k] : 0.0;   // uvk holds alpha_{i-1} here
@@ -151,11 +150,11 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
     const int lane = tid - NCT;
     const bool vec = lane < 3;
     const double* srcp = lane == 0 ? rin
-                       : lane == 1 ? d.u[1 - parity] + (long long)k * n
-                       : lane == 2 ? ((MODE == SR_INIT_WARM) ? d.S + (long long)k * n : x)
-                       : lane == 3 ? d.AP + (long long)m * n
-                       : lane == 4 ? d.AE + (long long)m * n
-                                   : d.AN + (long long)m * n;
+                       : lane == 1 ? d.u[1 - parity] + fk
+                       : lane == 2 ? ((MODE == SR_INIT_WARM) ? d.S + fk : x)
+                       : lane == 3 ? d.AP + fofs(g, m)
+                       : lane == 4 ? d.AE + fofs(g, m)
+                                   : d.AN + fofs(g, m);
     const double* constrow = lane == 3 ? d.one_row : d.zero_row;
     const bool used = lane < 6 && (lane != 1 || USE_PD) && (lane != 2 || USE_X);
     const int lag = lane == 1 ? 1 : (lane == 2 ? 2 : 0);
@@ -169,6 +168,11 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
     const uint32_t bytes = (uint32_t)NL * 8u * (uint32_t)(4 + (USE_PD ? 1 : 0) + (USE_X ? 1 : 0));
     const uint32_t dst0 = smem_addr(vec ? vstage + lane * NL : cring + (lane - 3) * NL);
     const uint32_t dstride = (uint32_t)(3 * NL * 8);    // bytes between slots
+    // row-slab mode: an iteration's r and pd rows outside the own slab come from the inbox the
+    // neighbours pushed them into (slot = parity of the last gather stamp)
+    const bool inbox = ITER && lane < 2 && d.dist.rows;
+    const double* ibase = inbox ? d.dist.halo_in[d.dist.rank] : nullptr;
+    const int islot = inbox ? (int)(*d.dist.seq & 1ull) : 0;
     for (int step = 0; step < nsteps; ++step) {
       const int sv = step & (SR_VSLOTS - 1), sc = step & (SR_CSLOTS - 1);
       if (step >= SR_VSLOTS) mbar_wait_sleep(emptyv0 + 8 * sv, (uint32_t)(((step / SR_VSLOTS) - 1) & 1));
@@ -181,6 +185,10 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
         const uint32_t dst = dst0 + (uint32_t)(vec ? sv : sc) * dstride;
         if (row >= lo && row < hi) {
           const double* rowp = srcp + (long long)row * nt;
+          if (inbox && (row < g.y0 || row >= g.y1)) {
+            const int side = row < g.y0 ? 0 : 1;
+            rowp = ibase + halo_ofs(islot, side, lane, K, k, side ? row - g.y1 : row - (g.y0 - SLAB_HALO), nt);
+          }
           bulk_g2s(dst, rowp + g0, (uint32_t)len0 * 8u, bar);
           int done = len0;
           while (done < NL) {                              // wrapped remainder (small n_theta loops)
@@ -390,13 +398,13 @@ __global__ void k_sr_scalar(DevPtrs d, int Kglob, int Klocal, int kofs, int worl
   if (threadIdx.x == 0) sr_scalar_stage<INIT>(d, sh, Kglob, Klocal, kofs, 0, 0ull);
 }
 
-// Peer-to-peer allgather as its own (one-thread) kernel: the true-residual and wrench gathers.
+// Peer-to-peer allgather as its own (one-warp) kernel: the true-residual and wrench gathers.
 __global__ void k_p2p_gather(DevPtrs d, const double* src, int n, double* dst) {
-  if (!p2p_gather(d.dist, src, n, dst)) { d.st_->done = 1; d.st_->status = -9; }
+  if (!p2p_gather(d.dist, src, n, dst) && threadIdx.x == 0) { d.st_->done = 1; d.st_->status = -9; }
 }
 
 cudaError_t launch_p2p_gather(const DevPtrs& d, const double* src, int n, double* dst, cudaStream_t s) {
-  k_p2p_gather<<<1, 1, 0, s>>>(d, src, n, dst);
+  k_p2p_gather<<<1, 32, 0, s>>>(d, src, n, dst);
   return cudaGetLastError();
 }
 
@@ -405,13 +413,14 @@ cudaError_t launch_p2p_gather(const DevPtrs& d, const double* src, int n, double
 __global__ void k_sr_fixup(GridParams g, DevPtrs d, int K) {   // K = local conditions
   const bool async = d.st_->coupling == 2;     // asynchronous: each condition has its own count
   if (!async && (d.st_->iter & 1) == 0) return;
-  const long long n = (long long)g.nt * g.ny;
+  const long long n = (long long)(g.y1 - g.y0) * g.nt;   // own rows
   const double* pd = d.u[0];   // pd_{it-1}, it-1 even -> parity 0
   for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n * K;
        q += (long long)gridDim.x * blockDim.x) {
     const int kk = (int)(q / n);
+    const long long o = fofs(g, kk) + (long long)g.y0 * g.nt + (q - (long long)kk * n);
     const int it = async ? d.cs.itk[kk] : d.st_->iter;
-    if (it & 1) d.p[q] = d.p[q] + d.cs.uvk[kk] * pd[q];
+    if (it & 1) d.p[o] = d.p[o] + d.cs.uvk[kk] * pd[o];
   }
 }
 
@@ -462,15 +471,16 @@ template <bool INIT>
 __global__ void k_p2p_scalar(DevPtrs d, int Klocal, unsigned long long hcond, int use_cond) {
   __shared__ double sh[4 * 256];
   if (!INIT && d.st_->done) return;
-  if (threadIdx.x != 0) return;
-  const int km = d.dist.kmax_local, Kg = d.dist.kglob;
+  const int km = d.dist.kmax_local, Kg = d.dist.kglob, lane = threadIdx.x;   // one warp
   if (!p2p_gather(d.dist, d.dist.packed_local, 4 * km, d.dist.packed_all)) {
-    d.st_->done = 1;
-    d.st_->status = -9;                                   // GMAF_E_CUDA: a peer never arrived
-    if (use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, 0u);
+    if (lane == 0) {
+      d.st_->done = 1;
+      d.st_->status = -9;                                 // GMAF_E_CUDA: a peer never arrived
+      if (use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, 0u);
+    }
     return;
   }
-  for (int kg = 0; kg < Kg; ++kg) {
+  for (int kg = lane; kg < Kg; kg += 32) {                // lanes in parallel (no dependent chain)
     int r, kl;
     dist_owner(kg, Kg, d.dist.world, &r, &kl);
     const double* srcp = d.dist.packed_all + (long long)r * 4 * km;
@@ -478,18 +488,146 @@ __global__ void k_p2p_scalar(DevPtrs d, int Klocal, unsigned long long hcond, in
     d.dist.rr_all[kg] = sh[kg];
     if (INIT) d.dist.ss_all[kg] = sh[3 * Kg + kg];
   }
-  sr_scalar_stage<INIT>(d, sh, Kg, Klocal, d.dist.kofs, use_cond, hcond);
+  __syncwarp();
+  if (lane == 0) sr_scalar_stage<INIT>(d, sh, Kg, Klocal, d.dist.kofs, use_cond, hcond);
+}
+
+// ------------------------------------------------- row-slab exchange
+// Every rank holds all K conditions on the rows [y0, y1).  Push the SLAB_HALO boundary rows of
+// nv vectors of every condition into the neighbours' inboxes (slot = parity of the NEXT gather
+// stamp): own rows [y0, y0+H) go to rank-1 (its side 1), rows [y1-H, y1) to rank+1 (its side
+// 0).  16-byte stores to peer memory over NVLink, then a system-scope fence, so that the stamp
+// the following gather posts also publishes the halos.
+constexpr int kCtrSlabRows = KK_COUNT + 1, kCtrSlabPush = KK_COUNT + 2;   // last-CTA counters
+
+__device__ __forceinline__ void slab_push(const GridParams& g, const DevPtrs& d, const double* v0,
+                                          const double* v1, int nv, int K) {
+  const DistPtrs& dd = d.dist;
+  const int slot = (int)((*dd.seq + 1ull) & 1ull);
+  const int nt2 = g.nt / 2;
+  // rows to send: [side][vec][k][ri], sides without a neighbour skipped; one CTA per row
+  const int s0 = dd.rank > 0 ? 0 : 1, s1 = dd.rank < dd.world - 1 ? 2 : 1;
+  const int per_side = nv * K * SLAB_HALO;
+  for (int q = blockIdx.x; q < (s1 - s0) * per_side; q += gridDim.x) {
+    const int side = s0 + q / per_side;                            // 0: to rank-1, 1: to rank+1
+    const int e = q % per_side;
+    const int ri = e % SLAB_HALO, k = (e / SLAB_HALO) % K, vec = e / (SLAB_HALO * K);
+    const int row = side == 0 ? g.y0 + ri : g.y1 - SLAB_HALO + ri;
+    const double2* src = reinterpret_cast<const double2*>((vec == 0 ? v0 : v1) + fofs(g, k) + (long long)row * g.nt);
+    double2* dst = reinterpret_cast<double2*>(dd.halo_in[side == 0 ? dd.rank - 1 : dd.rank + 1] +
+                                              halo_ofs(slot, 1 - side, vec, K, k, ri, g.nt));
+    for (int c2 = threadIdx.x; c2 < nt2; c2 += blockDim.x) dst[c2] = src[c2];
+  }
+  // one system-scope fence per CTA after the CTA barrier (cumulative, as in a grid barrier);
+  // last_cta_arrive then chains the CTAs to the thread that posts the stamp
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();
+}
+
+// The rank's per-condition sums of all ranks, summed in rank order (bitwise the same on every
+// rank), then the scalar stage and the WHILE condition.  One warp.
+template <bool INIT>
+__device__ void slab_scalars(const DevPtrs& d, int K, unsigned long long hcond, int use_cond) {
+  __shared__ double sh[4 * 256];
+  const int km = d.dist.kmax_local, lane = threadIdx.x & 31;
+  if (!p2p_gather(d.dist, d.dist.packed_local, 4 * km, d.dist.packed_all)) {
+    if (lane == 0) {
+      d.st_->done = 1;
+      d.st_->status = -9;                                 // GMAF_E_CUDA: a peer never arrived
+      if (use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, 0u);
+    }
+    return;
+  }
+  for (int i = lane; i < 4 * K; i += 32) {                // (q, k) pairs in parallel, ranks in order
+    const int q = i / K, k = i - q * K;
+    double s = 0.0;
+    for (int r = 0; r < d.dist.world; ++r) s += d.dist.packed_all[(long long)r * 4 * km + q * km + k];
+    sh[i] = s;
+    if (q == 0) d.dist.rr_all[k] = s;
+    if (INIT && q == 3) d.dist.ss_all[k] = s;
+  }
+  __syncwarp();
+  if (lane == 0) sr_scalar_stage<INIT>(d, sh, K, K, 0, use_cond, hcond);
+}
+
+// After every init / iteration kernel of a row-slab solve (same CUDA graph): push the halos of
+// the two vectors the next iteration reads across slab edges (r_{i+1}, pd_i; init: r_0, pd_-1),
+// then the last CTA gathers the sums and runs the scalar stage.  The next k_sr streams those
+// halo rows from the own inbox (TMA), so the exchange costs no extra pass over the fields.
+template <bool INIT>
+__global__ void k_p2p_rows(GridParams g, DevPtrs d, int parity, int K, unsigned long long hcond, int use_cond) {
+  if (!INIT && d.st_->done) return;
+  const double* va = INIT ? d.r[0] : d.r[1 - parity];
+  const double* vb = INIT ? d.u[1] : d.u[parity];
+  slab_push(g, d, va, vb, 2, K);
+  if (!last_cta_arrive(&d.counters[kCtrSlabRows], gridDim.x)) return;
+  if (threadIdx.x < 32) slab_scalars<INIT>(d, K, hcond, use_cond);
+}
+
+// One-off halo exchange of one field (the solution before a warm start / the true residual /
+// the quadrature; the warm-start residual): push, a gather that only carries the stamp, then
+// k_slab_unpack copies the inbox into the field's halo rows.
+__global__ void k_slab_push(GridParams g, DevPtrs d, const double* v, int K) {
+  slab_push(g, d, v, v, 1, K);
+  if (!last_cta_arrive(&d.counters[kCtrSlabPush], gridDim.x)) return;
+  if (threadIdx.x < 32 && !p2p_gather(d.dist, d.dist.packed_local, 0, d.dist.packed_all) && threadIdx.x == 0) {
+    d.st_->done = 1;
+    d.st_->status = -9;
+  }
+}
+
+__global__ void k_slab_unpack(GridParams g, DevPtrs d, double* v, int K) {
+  const DistPtrs& dd = d.dist;
+  const int slot = (int)(*dd.seq & 1ull);
+  const int nt2 = g.nt / 2;
+  const int s0 = dd.rank > 0 ? 0 : 1, s1 = dd.rank < dd.world - 1 ? 2 : 1;
+  const int per_side = K * SLAB_HALO;
+  for (int q = blockIdx.x; q < (s1 - s0) * per_side; q += gridDim.x) {
+    const int side = s0 + q / per_side;                            // 0: rows below y0, 1: from y1 up
+    const int ri = (q % per_side) % SLAB_HALO, k = (q % per_side) / SLAB_HALO;
+    const int row = side == 0 ? g.y0 - SLAB_HALO + ri : g.y1 + ri;
+    const double2* src = reinterpret_cast<const double2*>(dd.halo_in[dd.rank] + halo_ofs(slot, side, 0, K, k, ri, g.nt));
+    double2* dst = reinterpret_cast<double2*>(v + fofs(g, k) + (long long)row * g.nt);
+    for (int c2 = threadIdx.x; c2 < nt2; c2 += blockDim.x) dst[c2] = src[c2];
+  }
+}
+
+// CTAs of the exchange kernels: enough for the halo rows (double2 per thread), at most one per
+// SM; one for a single rank (nothing to push, only the gather).
+// CTAs of the exchange kernels: one per halo row to send (at most 2 per SM); one for a single
+// rank (nothing to push, only the gather).
+static int slab_blocks(const GridParams& g, const DevPtrs& d, int K, int nv) {
+  (void)g;
+  if (d.dist.world <= 1) return 1;
+  const int rows = 2 * nv * K * SLAB_HALO;
+  return rows < 296 ? rows : 296;
+}
+
+cudaError_t launch_p2p_rows(const GridParams& g, const DevPtrs& d, bool init, int parity, int K,
+                            unsigned long long h, cudaStream_t s) {
+  const int use = h != 0ull;
+  if (init) k_p2p_rows<true><<<slab_blocks(g, d, K, 2), 256, 0, s>>>(g, d, parity, K, h, use);
+  else k_p2p_rows<false><<<slab_blocks(g, d, K, 2), 256, 0, s>>>(g, d, parity, K, h, use);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_slab_exchange(const GridParams& g, const DevPtrs& d, double* v, int K, cudaStream_t s) {
+  k_slab_push<<<slab_blocks(g, d, K, 1), 256, 0, s>>>(g, d, v, K);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_slab_unpack<<<slab_blocks(g, d, K, 1), 256, 0, s>>>(g, d, v, K);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_p2p_scalar(const DevPtrs& d, bool init, int Klocal, unsigned long long h, cudaStream_t s) {
   const int use = h != 0ull;
-  if (init) k_p2p_scalar<true><<<1, 32, 0, s>>>(d, Klocal, h, use);
+  if (init) k_p2p_scalar<true><<<1, 32, 0, s>>>(d, Klocal, h, use);   // one warp
   else k_p2p_scalar<false><<<1, 32, 0, s>>>(d, Klocal, h, use);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sr_fixup(const GridParams& g, const DevPtrs& d, int K, cudaStream_t s) {
-  const long long work = (long long)g.nt * g.ny * K;
+  const long long work = (long long)g.nt * (g.y1 - g.y0) * K;
   long long blocks = (work + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   k_sr_fixup<<<(int)blocks, 256, 0, s>>>(g, d, K);

@@ -155,12 +155,15 @@ __device__ void sr_scalar_async(const DevPtrs& d, const double* red, int K) {
 template <bool INIT>
 __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, int Klocal, int kofs,
                                 int use_cond, unsigned long long hcond) {
-  SolverState* st = d.st_;
-  if (st->coupling == 2) {
+  if (d.st_->coupling == 2) {
     sr_scalar_async<INIT>(d, red, Kall);
-    if (use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, st->done ? 0u : 1u);
+    if (use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, d.st_->done ? 0u : 1u);
     return;
   }
+  // one thread on the critical path of every iteration: snapshot the solver state into registers
+  // (independent loads), compute, write it back once -- no dependent global round trips
+  SolverState s = *d.st_;
+  const double aold0 = d.cs.alpha[0];
   const double* rrk = red;
   const double* gk = red + Kall;
   const double* dk = red + 2 * Kall;
@@ -173,23 +176,23 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
     double SS = 0.0;
     for (int kk = 0; kk < Kall; ++kk) SS += ssk[kk];
     for (int kl = 0; kl < Klocal; ++kl) d.cs.Sk[kl] = ssk[kofs + kl];
-    st->nS = sqrt(SS);
-    st->iter = 0; st->status = 0; st->converged = 0; st->done = 0; st->zero_p = 0;
-    if (st->nS == 0.0) {
-      st->rel = 0.0; st->done = 1; st->converged = 1; st->zero_p = 1;
+    s.nS = sqrt(SS);
+    s.iter = 0; s.status = 0; s.converged = 0; s.done = 0; s.zero_p = 0;
+    if (s.nS == 0.0) {
+      s.rel = 0.0; s.done = 1; s.converged = 1; s.zero_p = 1;
     } else {
-      st->rel = sqrt(rr) / st->nS;
-      if (st->fixed_iters == 0 && st->rel <= st->tol) { st->done = 1; st->converged = 1; }
-      else if (st->max_iter <= 0) { st->done = 1; st->status = -6; }
+      s.rel = sqrt(rr) / s.nS;
+      if (s.fixed_iters == 0 && s.rel <= s.tol) { s.done = 1; s.converged = 1; }
+      else if (s.max_iter <= 0) { s.done = 1; s.status = -6; }
     }
-    if (!st->done) {
-      if (st->coupling == 0) {
+    if (!s.done) {
+      if (s.coupling == 0) {
         double gg = 0.0, dd = 0.0;
         for (int kk = 0; kk < Kall; ++kk) { gg += gk[kk]; dd += dk[kk]; }
         if (!(dd > 0.0)) bad = true;
         const double a0 = gg / dd;
         for (int kl = 0; kl < Klocal; ++kl) { d.cs.alpha[kl] = a0; d.cs.beta[kl] = 0.0; d.cs.uvk[kl] = 0.0; }
-        st->d = gg;
+        s.d = gg;
       } else {
         for (int kk = 0; kk < Kall; ++kk)
           if (gk[kk] != 0.0 && !(dk[kk] > 0.0)) bad = true;
@@ -199,36 +202,35 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
           d.cs.beta[kl] = 0.0; d.cs.uvk[kl] = 0.0; d.cs.dk[kl] = gk[kk];
         }
       }
-      if (bad) { st->done = 1; st->status = -5; }
+      if (bad) { s.done = 1; s.status = -5; }
     }
   } else {
-    st->iter += 1;
-    st->rel = sqrt(rr) / st->nS;
-    for (int kl = 0; kl < Klocal; ++kl) d.cs.uvk[kl] = d.cs.alpha[kl];   // alpha used this iteration
-    if (st->fixed_iters > 0) {
-      if (st->iter >= st->fixed_iters) st->done = 1;
-    } else if (st->rel <= st->tol) {
-      st->done = 1; st->converged = 1;
-    } else if (st->iter >= st->max_iter) {
-      st->done = 1; st->status = -6;
+    s.iter += 1;
+    s.rel = sqrt(rr) / s.nS;
+    if (s.fixed_iters > 0) {
+      if (s.iter >= s.fixed_iters) s.done = 1;
+    } else if (s.rel <= s.tol) {
+      s.done = 1; s.converged = 1;
+    } else if (s.iter >= s.max_iter) {
+      s.done = 1; s.status = -6;
     }
-    if (!st->done || st->fixed_iters > 0) {
-      if (st->coupling == 0) {
+    if (!s.done || s.fixed_iters > 0) {
+      if (s.coupling == 0) {
         double g2 = 0.0, d2 = 0.0;
         for (int kk = 0; kk < Kall; ++kk) { g2 += gk[kk]; d2 += dk[kk]; }
-        const double aold = d.cs.alpha[0];
-        const double b = g2 / st->d;
-        const double den = d2 - b * g2 / aold;
+        const double b = g2 / s.d;
+        const double den = d2 - b * g2 / aold0;
         if (!(g2 > 0.0) || !(den > 0.0)) bad = true;
         const double a = g2 / den;
-        for (int kl = 0; kl < Klocal; ++kl) { d.cs.alpha[kl] = a; d.cs.beta[kl] = b; }
-        st->d = g2;
+        for (int kl = 0; kl < Klocal; ++kl) { d.cs.uvk[kl] = aold0; d.cs.alpha[kl] = a; d.cs.beta[kl] = b; }
+        s.d = g2;
       } else {
         for (int kk = 0; kk < Kall; ++kk)
           if (gk[kk] < 0.0) bad = true;
         for (int kl = 0; kl < Klocal; ++kl) {
           const int kk = kofs + kl;
           const double aold = d.cs.alpha[kl], gold = d.cs.dk[kl];
+          d.cs.uvk[kl] = aold;                                   // alpha used this iteration
           double a = 0.0, b = 0.0;
           if (gold != 0.0 && aold != 0.0) {
             b = gk[kk] / gold;
@@ -238,10 +240,13 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
           d.cs.alpha[kl] = a; d.cs.beta[kl] = b; d.cs.dk[kl] = gk[kk];
         }
       }
-      if (bad && !st->done) { st->done = 1; st->status = -5; }
+      if (bad && !s.done) { s.done = 1; s.status = -5; }
+    } else {
+      for (int kl = 0; kl < Klocal; ++kl) d.cs.uvk[kl] = d.cs.alpha[kl];   // alpha used this iteration
     }
   }
-  if (use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, st->done ? 0u : 1u);
+  *d.st_ = s;
+  if (use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, s.done ? 0u : 1u);
 }
 
 
@@ -256,39 +261,50 @@ __device__ __forceinline__ void dist_owner(int kg, int Kglob, int world, int* r,
 
 constexpr long long kP2PTimeoutNs = 10000000000ll;   // 10 s: a peer that never arrives fails the solve
 
-// Peer-to-peer allgather (one thread): push n doubles of src into slot `rank` of every rank's
-// exchange buffer over NVLink (IPC-mapped peer memory), publish a monotonically increasing stamp
-// with release semantics at system scope, wait for every rank's stamp in the own buffer, and copy
-// the gathered blocks to dst [world][n].  All ranks issue the same sequence of gathers, so their
-// stamps agree; two parity slots keep a rank that runs one gather ahead from overwriting a block
-// a slower rank still reads.  Returns false on timeout.
+// Peer-to-peer allgather, executed by ONE WARP (all 32 lanes call it; the result is warp-uniform):
+// push n doubles of src into slot `rank` of every rank's exchange buffer over NVLink (IPC-mapped
+// peer memory, lanes in parallel), publish a monotonically increasing stamp with release
+// semantics at system scope (lane r to rank r), wait for every rank's stamp in the own buffer
+// (lane r polls rank r), and copy the gathered blocks to dst [world][n].  All ranks issue the same
+// sequence of gathers, so their stamps agree; two parity slots keep a rank that runs one gather
+// ahead from overwriting a block a slower rank still reads.  Returns false on timeout.
 __device__ __forceinline__ bool p2p_gather(const DistPtrs& dd, const double* src, int n, double* dst) {
+  const int lane = threadIdx.x & 31;
   const int W = dd.world;
-  const unsigned long long stamp = *dd.seq + 1ull;
-  *dd.seq = stamp;
+  unsigned long long stamp = 0ull;
+  if (lane == 0) {
+    stamp = *dd.seq + 1ull;
+    *dd.seq = stamp;
+  }
+  stamp = __shfl_sync(0xffffffffu, stamp, 0);
   const int par = (int)(stamp & 1ull);
-  for (int r = 0; r < W; ++r) {
+  for (int i = lane; i < W * n; i += 32) {
+    const int r = i / n, q = i - r * n;
     double* slot = reinterpret_cast<double*>(dd.peer[r] + 2 * W * 8) + ((long long)par * W + dd.rank) * dd.xs;
-    for (int q = 0; q < n; ++q) *reinterpret_cast<volatile double*>(slot + q) = src[q];
+    *reinterpret_cast<volatile double*>(slot + q) = src[q];
   }
   __threadfence_system();
-  for (int r = 0; r < W; ++r) {
-    unsigned long long* fl = reinterpret_cast<unsigned long long*>(dd.peer[r]) + par * W + dd.rank;
+  __syncwarp();
+  bool ok = true;
+  if (lane < W) {
+    unsigned long long* fl = reinterpret_cast<unsigned long long*>(dd.peer[lane]) + par * W + dd.rank;
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(fl), "l"(stamp) : "memory");
-  }
-  const unsigned long long* my = reinterpret_cast<const unsigned long long*>(dd.peer[dd.rank]) + par * W;
-  const unsigned long long t0 = globaltimer();
-  for (int r = 0; r < W; ++r) {
-    unsigned long long v;
+    const unsigned long long* my = reinterpret_cast<const unsigned long long*>(dd.peer[dd.rank]) + par * W + lane;
+    const unsigned long long t0 = globaltimer();
     for (;;) {
-      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(my + r) : "memory");
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(my) : "memory");
       if (v >= stamp) break;
-      if ((long long)(globaltimer() - t0) > kP2PTimeoutNs) return false;
+      if ((long long)(globaltimer() - t0) > kP2PTimeoutNs) { ok = false; break; }
     }
   }
+  if (!__all_sync(0xffffffffu, ok)) return false;
   const volatile double* data = reinterpret_cast<const volatile double*>(dd.peer[dd.rank] + 2 * W * 8);
-  for (int r = 0; r < W; ++r)
-    for (int q = 0; q < n; ++q) dst[(long long)r * n + q] = data[((long long)par * W + r) * dd.xs + q];
+  for (int i = lane; i < W * n; i += 32) {
+    const int r = i / n, q = i - r * n;
+    dst[i] = data[((long long)par * W + r) * dd.xs + q];
+  }
+  __syncwarp();
   return true;
 }
 

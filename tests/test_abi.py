@@ -64,3 +64,25 @@ def test_no_cpu_fallback_in_product():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
                 assert "gmaf_oracle" not in txt, f
+
+
+def test_row_slab_sizing_without_gpu(pkg):
+    """GMAF_SHARD_ROWS_P2P: each rank stores its own rows + 4 halo rows per side of all K
+    conditions (include/gmaf.h gmaf_slab); slabs thinner than 8 rows are rejected."""
+    import gmaf_inputs as gi
+    g = pkg.make_grid(gi.grid(2048, 1024, "short"))
+    full = pkg.gmaf_workspace_bytes(g, 9)
+    field = 2048 * 9 * 8                                   # one row of one field, all K
+    sizes = []
+    for r in range(4):
+        d, _ = pkg.make_dist(r, 4, None, p2p=True, shard="rows")
+        nb = pkg.gmaf_workspace_bytes(g, 9, d)
+        stored = 256 + (4 if r > 0 else 0) + (4 if r < 3 else 0)
+        assert 9 * field * stored <= nb <= 9 * field * stored + (64 << 20), (r, nb)
+        sizes.append(nb)
+    assert max(sizes) < full / 3
+    d, _ = pkg.make_dist(0, 8, None, p2p=True, shard="rows")
+    assert pkg.gmaf_workspace_bytes(pkg.make_grid(gi.grid(64, 60)), 1, d) == 0      # 60 < 8 rows x 8
+    assert pkg.gmaf_workspace_bytes(pkg.make_grid(gi.grid(64, 64)), 1, d) > 0
+    d, _ = pkg.make_dist(0, 9, None, p2p=True, shard="rows")
+    assert pkg.gmaf_workspace_bytes(pkg.make_grid(gi.grid(64, 512)), 1, d) == 0     # > 8 ranks

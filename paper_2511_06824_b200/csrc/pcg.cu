@@ -82,8 +82,10 @@ __device__ void reduce_partials(const DevPtrs& d, int nq, int K, int ncta, doubl
   __syncthreads();
 }
 
+// The WHILE handle's default value (1) is applied at every graph launch, so the condition is
+// only ever written to stop the loop: no device-runtime call on a continuing iteration.
 __device__ __forceinline__ void set_cond(bool use, unsigned long long h, bool keep_going) {
-  if (use) cudaGraphSetConditional((cudaGraphConditionalHandle)h, keep_going ? 1u : 0u);
+  if (use && !keep_going) cudaGraphSetConditional((cudaGraphConditionalHandle)h, 0u);
 }
 
 // ------------------------------------------------------------------ phase A

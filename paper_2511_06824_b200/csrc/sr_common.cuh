@@ -157,7 +157,7 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
                                 int use_cond, unsigned long long hcond) {
   if (d.st_->coupling == 2) {
     sr_scalar_async<INIT>(d, red, Kall);
-    if (use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, d.st_->done ? 0u : 1u);
+    if (use_cond && d.st_->done) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, 0u);
     return;
   }
   // one thread on the critical path of every iteration: snapshot the solver state into registers
@@ -246,7 +246,8 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
     }
   }
   *d.st_ = s;
-  if (use_cond) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, s.done ? 0u : 1u);
+  // the WHILE handle defaults to 1 at every graph launch: write it only to stop the loop
+  if (use_cond && s.done) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, 0u);
 }
 
 
@@ -325,7 +326,8 @@ __device__ void sr_finish(const DevPtrs& d, double (&v)[4], double* red, int K, 
     for (int q = tid; q < 4 * K; q += blockDim.x) {
       const double* srcp = d.partials + (long long)q * ncta;
       double sum = 0.0;
-      for (int b = 0; b < ncta; ++b) sum += __ldcg(srcp + b);
+#pragma unroll 8
+      for (int b = 0; b < ncta; ++b) sum += __ldcg(srcp + b);   // loads in flight, adds in CTA order
       red[q] = sum;
     }
     __syncthreads();

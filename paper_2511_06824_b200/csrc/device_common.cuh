@@ -17,14 +17,15 @@ __device__ __forceinline__ void timing_begin(Timing* T, int kind) {
   if (threadIdx.x == 0) atomicMin(&T->t_start[kind], globaltimer());
 }
 
-// Called by one thread of the last CTA of a launch.
-__device__ __forceinline__ void timing_end(Timing* T, int kind) {
+// Called by one thread of the last CTA of a launch.  One dependent load (the start stamp); the
+// accumulations are fire-and-forget reductions (RED), so the serial tail of a launch does not wait.
+__device__ __forceinline__ void timing_end(Timing* T, int kind, unsigned long long t0) {
   const unsigned long long t = globaltimer();
-  const unsigned long long t0 = T->t_start[kind];
-  if (t0 != ~0ull && t > t0) T->total_ns[kind] += t - t0;
-  T->launches[kind] += 1;
+  if (t0 != ~0ull && t > t0) atomicAdd(&T->total_ns[kind], t - t0);
+  atomicAdd(&T->launches[kind], 1ull);
   T->t_start[kind] = ~0ull;
 }
+__device__ __forceinline__ void timing_end(Timing* T, int kind) { timing_end(T, kind, T->t_start[kind]); }
 
 // Returns true in exactly one CTA: the last one to arrive.  All partial results the
 // CTA wrote before the call are visible to the last CTA (fence + atomic).  The counter

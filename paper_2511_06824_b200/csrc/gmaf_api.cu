@@ -968,7 +968,8 @@ gmaf_status gmaf_kernel_times(gmaf_ctx* ctx, gmaf_kernel_timing* out, int32_t n,
   CU(cudaMemcpyAsync(ctx->h_timing, ctx->d.timing, sizeof(Timing), cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   static const char* names[KK_COUNT] = {"thickness_guard", "assemble", "pcg_init", "pcg_phase_a",
-                                        "pcg_phase_b", "true_residual", "quadrature", "sr_init", "sr_iter"};
+                                        "pcg_phase_b", "true_residual", "quadrature", "sr_init", "sr_iter",
+                                        "tail_of_sr_iter"};
   const double rows = (double)(ctx->gp.y1 - ctx->gp.y0);   // own rows (all n_y on one rank)
   const double n_nodes = (double)ctx->grid.n_theta * rows * ctx->K;
   const double nM = (double)ctx->grid.n_theta * rows * (ctx->M > 0 ? ctx->M : ctx->K);
@@ -983,7 +984,8 @@ gmaf_status gmaf_kernel_times(gmaf_ctx* ctx, gmaf_kernel_timing* out, int32_t n,
       8.0 * (2.0 * n_nodes + 3.0 * nM),     // true residual: read S, p; 3 bands
       8.0 * n_nodes,                        // quadrature: read p
       8.0 * (2.0 * n_nodes + 3.0 * nM),     // sr_init: read S, write r (x zeroed: +1)
-      8.0 * (5.0 * n_nodes + 3.0 * nM)};    // sr_iter: r RW, pd RW, x RW every other; 3 bands
+      8.0 * (5.0 * n_nodes + 3.0 * nM),     // sr_iter: r RW, pd RW, x RW every other; 3 bands
+      0.0};                                 // serial tail of sr_iter (inside its time)
   int c = 0;
   for (int q = 0; q < KK_COUNT && c < n; ++q, ++c) {
     std::memset(&out[c], 0, sizeof(gmaf_kernel_timing));

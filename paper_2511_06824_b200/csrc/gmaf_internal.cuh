@@ -43,7 +43,9 @@ __host__ __device__ __forceinline__ long long fofs(const GridParams& g, int k) {
 
 // Kernel kinds for the in-kernel %globaltimer accounting.
 enum KernelKind { KK_THICK = 0, KK_ASSEMBLE, KK_INIT, KK_PHASE_A, KK_PHASE_B, KK_TRUERES, KK_QUAD,
-                  KK_SR_INIT, KK_SR_ITER, KK_COUNT };
+                  KK_SR_INIT, KK_SR_ITER,
+                  KK_SR_TAIL,   // serial tail of k_sr ITER (last CTA: reduction + scalar stage), inside KK_SR_ITER
+                  KK_COUNT };
 
 struct Timing {
   unsigned long long t_start[KK_COUNT];   // min start of the current launch (ULLONG_MAX = idle)

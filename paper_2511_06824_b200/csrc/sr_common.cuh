@@ -152,18 +152,28 @@ __device__ void sr_scalar_async(const DevPtrs& d, const double* red, int K) {
   if (bad && !st->done) { st->done = 1; st->status = -5; }
 }
 
+// Solver-state snapshot for the scalar stage, loaded early (overlapped with the partial-sum loads
+// of the serial tail): the stage itself then makes no dependent global round trip.
+struct StageIn { SolverState s; double aold0; };
+__device__ __forceinline__ StageIn stage_prefetch(const DevPtrs& d) {
+  StageIn in;
+  in.s = *d.st_;
+  in.aold0 = d.cs.alpha[0];
+  return in;
+}
+
 template <bool INIT>
 __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, int Klocal, int kofs,
-                                int use_cond, unsigned long long hcond) {
-  if (d.st_->coupling == 2) {
+                                int use_cond, unsigned long long hcond, const StageIn& in) {
+  // one thread on the critical path of every iteration: work on the register snapshot, write the
+  // state back once
+  SolverState s = in.s;
+  const double aold0 = in.aold0;
+  if (s.coupling == 2) {
     sr_scalar_async<INIT>(d, red, Kall);
     if (use_cond && d.st_->done) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, 0u);
     return;
   }
-  // one thread on the critical path of every iteration: snapshot the solver state into registers
-  // (independent loads), compute, write it back once -- no dependent global round trips
-  SolverState s = *d.st_;
-  const double aold0 = d.cs.alpha[0];
   const double* rrk = red;
   const double* gk = red + Kall;
   const double* dk = red + 2 * Kall;
@@ -250,6 +260,12 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
   if (use_cond && s.done) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, 0u);
 }
 
+template <bool INIT>
+__device__ __forceinline__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, int Klocal,
+                                                int kofs, int use_cond, unsigned long long hcond) {
+  sr_scalar_stage<INIT>(d, red, Kall, Klocal, kofs, use_cond, hcond, stage_prefetch(d));
+}
+
 
 // ---------------------------------------------------------------- multi-rank helpers
 // rank and local index of global condition kg (contiguous blocks; the first Kglob % world ranks
@@ -322,12 +338,21 @@ __device__ void sr_finish(const DevPtrs& d, double (&v)[4], double* red, int K, 
     for (int q = 0; q < 4; ++q) d.partials[(long long)(q * K + k) * ncta + cta] = v[q];
   }
   if (last_cta_arrive(&d.counters[ITER ? KK_SR_ITER : KK_SR_INIT], gridDim.x)) {
-    // per-condition sums in CTA order: [rr | gamma | delta | S.S] x K
+    const unsigned long long t_tail = (ITER && tid == 0) ? globaltimer() : 0ull;
+    // thread 0 prefetches what the scalar stage and the timing need (overlaps the loads below)
+    StageIn in{};
+    unsigned long long t_start0 = 0ull;
+    if (tid == 0) {
+      in = stage_prefetch(d);
+      t_start0 = d.timing->t_start[ITER ? KK_SR_ITER : KK_SR_INIT];
+    }
+    // per-condition sums in CTA order: [rr | gamma | delta | S.S] x K; all loads of a sum in
+    // flight at once (one L2 round trip on this serial tail), adds in CTA order
     for (int q = tid; q < 4 * K; q += blockDim.x) {
       const double* srcp = d.partials + (long long)q * ncta;
       double sum = 0.0;
-#pragma unroll 8
-      for (int b = 0; b < ncta; ++b) sum += __ldcg(srcp + b);   // loads in flight, adds in CTA order
+#pragma unroll 32
+      for (int b = 0; b < ncta; ++b) sum += __ldcg(srcp + b);
       red[q] = sum;
     }
     __syncthreads();
@@ -340,9 +365,13 @@ __device__ void sr_finish(const DevPtrs& d, double (&v)[4], double* red, int K, 
         // NCCL mode: the allgather + k_sr_scalar follow on the stream; peer-to-peer mode:
         // k_p2p_scalar follows in the same graph
       } else {
-        sr_scalar_stage<INIT>(d, red, K, K, 0, use_cond, hcond);
+        sr_scalar_stage<INIT>(d, red, K, K, 0, use_cond, hcond, in);
       }
-      timing_end(d.timing, ITER ? KK_SR_ITER : KK_SR_INIT);
+      timing_end(d.timing, ITER ? KK_SR_ITER : KK_SR_INIT, t_start0);
+      if (ITER) {   // the serial tail: all other CTAs have finished when the last one arrives
+        atomicAdd(&d.timing->total_ns[KK_SR_TAIL], globaltimer() - t_tail);
+        atomicAdd(&d.timing->launches[KK_SR_TAIL], 1ull);
+      }
     }
   }
 }

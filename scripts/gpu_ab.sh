@@ -1,5 +1,10 @@
-# A/B of kernel variants: env assignments passed as arguments, e.g. bash scripts/gpu_ab.sh "GMAF_SR_COLS=1" "GMAF_SR_COLS=2"
-for v in "$@"; do
-  env $v timeout 600 python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ab.log 2>&1
-  echo "$v $(python -c "import json;d=json.loads(open('gpurun_out/ab.log').read().strip().splitlines()[-1]);print(round(d['value']/1e9,2),'G', round(d['roofline']['avg_launch_us_events'],1),'us')" 2>&1 | tail -1)"
+# A/B of an env knob on the 1-GPU bench (C3): GPU tests first, then bench lines per setting
+set -x
+timeout 2000 python -m pytest tests -q -m gpu -x > gpurun_out/pytest_gpu_iter.log 2>&1; echo pytest_rc=$?
+tail -n 2 gpurun_out/pytest_gpu_iter.log
+for e in "$@"; do
+timeout 600 env $e python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/bench_ab.log 2>&1
+python -c "
+import json; d=json.loads(open('gpurun_out/bench_ab.log').read().strip().splitlines()[-1]); r=d['roofline']; k=d['kernels']
+print('[$e]', round(d['value']/1e9,2), 'G ev_us', round(r['avg_launch_us_events'],1), 'gt_us', round(r['avg_launch_us_globaltimer'],1), 'frac', round(r['frac'],3), 'tail', k['tail_of_sr_iter']['avg_us'], d['iterations_per_step'], d['clocks']['sm_mhz'])"
 done

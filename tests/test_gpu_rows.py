@@ -1,12 +1,14 @@
 """Row-slab sharding (include/gmaf.h GMAF_SHARD_ROWS_P2P, gmaf_slab):
-three ranks -- here three processes time-sharing ONE GPU, bootstrapped over gloo -- each owning a
+two or three ranks -- here processes time-sharing ONE GPU, bootstrapped over gloo -- each owning a
 contiguous block of the unknown rows of all 9 conditions, with the halo rows of r and of the
 search direction pushed into the neighbours' inboxes over IPC-mapped peer memory after every
-iteration.  The middle rank has both neighbours; the slabs span several row chunks each.
+iteration.  With three ranks the middle one has both neighbours; the slabs span several row
+chunks each; the two-rank case has ragged slabs (n_y odd) and a smooth film.
 
 The per-condition sums are added per rank and then over the ranks, so the scalars differ from
 the one-process solve in the last bits only: the j-th iterate must agree to 1e-12 (any halo error
-is O(1)), the converged p with the oracle to 1e-8 (R-A23), the wrenches to 1e-9."""
+is O(1)), the converged p with the oracle to 1e-8 (R-A23), the wrenches to 1e-9; Jacobi and
+lockstep coupling run through the same exchange."""
 import os
 import socket
 
@@ -16,7 +18,10 @@ import torch.multiprocessing as mp
 
 pytestmark = pytest.mark.gpu
 
-WORLD = 3
+CASES = {
+    3: ("short", 128, 96, dict(tex_n_theta=8, tex_n_y=3, tex_band_rows=24), 5, 1.6),
+    2: ("smooth", 96, 97, {}, 8, 1.8),
+}
 
 
 def _port():
@@ -27,78 +32,93 @@ def _port():
     return p
 
 
-def _case():
+def _case(world):
     import gmaf_inputs as gi
-    g = gi.grid(128, 96, "short", tex_n_theta=8, tex_n_y=3, tex_band_rows=24)
-    return g, gi.random_conditions(5, 9)
+    tex, nt, ny, over, seed, omega = CASES[world]
+    return gi.grid(nt, ny, tex, **over), gi.random_conditions(seed, 9), omega
 
 
-def _rank(rank, world, port, out):
+def _run(S, conds, omega, rows):
+    """The same sequence on the sharded and the one-process solver; rows = slice of own rows."""
+    S.thickness(conds)
+    S.assemble()
+    out = {}
+    fx = S.solve(tol=1e-30, omega=omega, max_iter=7, raise_on_error=False)      # 7 iterates
+    out["it7"] = fx.iterations
+    out["p7"] = np.stack([S.get("p", k)[rows] for k in range(9)])
+    st = S.solve(tol=1e-10, omega=omega)
+    out["st"] = (st.iterations, st.converged, st.rel_residual, st.true_rel_residual, st.cond_rel)
+    out["W"] = S.integrate()
+    out["p"] = np.stack([S.get("p", k)[rows] for k in range(9)])
+    out["warm"] = S.solve(tol=1e-10, omega=omega, warm=True).iterations     # halo of p0, residual
+    jl = S.solve(tol=1e-10, omega=omega, precond="jacobi", coupling="lockstep")
+    out["jl"] = (jl.iterations, np.stack([S.get("p", k)[rows] for k in range(9)]))
+    return out
+
+
+def _rank(rank, world, port, res):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import paper_2511_06824_b200 as P
     from paper_2511_06824_b200.dist import connect_p2p
-    g, conds = _case()
+    g, conds, omega = _case(world)
     S = P.JointSolver(g, 9, device=0, rank=rank, world=world, shard="rows")
     connect_p2p(S)
     y0, y1 = S.slab
-    S.thickness(conds)
-    S.assemble()
-    fx = S.solve(tol=1e-30, omega=1.6, max_iter=7, raise_on_error=False)    # 7 iterates
-    p7 = np.stack([S.get("p", k)[y0:y1] for k in range(9)])
-    st = S.solve(tol=1e-10, omega=1.6)
-    W = S.integrate()
-    p = np.stack([S.get("p", k)[y0:y1] for k in range(9)])
-    st2 = S.solve(tol=1e-10, omega=1.6, warm=True)          # warm start: halo of p0, residual
-    out[rank] = (y0, y1, fx.iterations, p7, st.iterations, st.converged, st.rel_residual,
-                 st.true_rel_residual, p, W, st2.iterations, st.cond_rel)
+    out = _run(S, conds, omega, slice(y0, y1))
+    out["slab"] = (y0, y1)
+    res[rank] = out
     S.close()
     dist.barrier()
     dist.destroy_process_group()
 
 
+def _rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
 @pytest.mark.timeout(900)
-def test_row_slabs_three_ranks_match_the_joint_solve():
+@pytest.mark.parametrize("world", [3, 2])
+def test_row_slabs_match_the_joint_solve(world):
     import torch
     assert torch.cuda.is_available()
     from paper_2511_06824_b200 import build as B
     B.build()
     import oracle as orc
     import paper_2511_06824_b200 as P
-    g, conds = _case()
+    g, conds, omega = _case(world)
     S = P.JointSolver(g, 9)
-    S.thickness(conds)
-    S.assemble()
-    S.solve(tol=1e-30, omega=1.6, max_iter=7, raise_on_error=False)
-    p7ref = np.stack([S.get("p", k) for k in range(9)])
-    st = S.solve(tol=1e-10, omega=1.6)
-    W = S.integrate()
-    pref = np.stack([S.get("p", k) for k in range(9)])
+    ref1 = _run(S, conds, omega, slice(None))
     S.close()
     AP, AE, AN, SS = orc.assemble_joint(g, conds)
-    ref = orc.pcg_joint(AP, AE, AN, SS, tol=1e-10, omega=1.6)
+    ref = orc.pcg_joint(AP, AE, AN, SS, tol=1e-10, omega=omega)
 
-    out = mp.Manager().dict()
-    mp.spawn(_rank, args=(WORLD, _port(), out), nprocs=WORLD, join=True)
-    rows = []
-    for r in range(WORLD):
-        y0, y1, it7, p7, it, conv, rel, trel, p, Wr, it2, crel = out[r]
-        rows.append((y0, y1))
-        assert it7 == 7
-        err7 = np.linalg.norm(p7 - p7ref[:, y0:y1]) / np.linalg.norm(p7ref[:, y0:y1])
+    res = mp.Manager().dict()
+    mp.spawn(_rank, args=(world, _port(), res), nprocs=world, join=True)
+    slabs = [res[r]["slab"] for r in range(world)]
+    assert slabs[0][0] == 0 and slabs[-1][1] == g["n_y"]
+    assert all(slabs[r][1] == slabs[r + 1][0] for r in range(world - 1))
+    it1, _, _, _, crel1 = ref1["st"]
+    for r in range(world):
+        o = res[r]
+        rows = slice(*o["slab"])
+        assert o["it7"] == 7
+        err7 = _rel(o["p7"], ref1["p7"][:, rows])
         assert err7 <= 1e-12, (r, err7)
-        assert conv and abs(it - st.iterations) <= 2, (r, it, st.iterations)
+        it, conv, rel, trel, crel = o["st"]
+        assert conv and abs(it - it1) <= 2, (r, it, it1)
         assert rel <= 1e-10 and trel <= 1e-9
-        assert np.linalg.norm(p - ref.p[:, y0:y1]) <= 1e-8 * np.linalg.norm(ref.p[:, y0:y1]), r
-        assert np.linalg.norm(p - pref[:, y0:y1]) <= 1e-9 * np.linalg.norm(pref[:, y0:y1]), r
+        assert _rel(o["p"], ref.p[:, rows]) <= 1e-8, r
+        assert _rel(o["p"], ref1["p"][:, rows]) <= 1e-9, r
         for k in range(9):
-            assert np.linalg.norm(Wr[k] - W[k]) <= 1e-9 * np.linalg.norm(W[k]), (r, k)
-        assert np.array_equal(Wr, out[0][9])            # the same wrenches on every rank
-        assert it2 == 0                                 # warm start from the converged p
+            assert np.linalg.norm(o["W"][k] - ref1["W"][k]) <= 1e-9 * np.linalg.norm(ref1["W"][k]), (r, k)
+        assert np.array_equal(o["W"], res[0]["W"])            # the same wrenches on every rank
+        assert o["warm"] == 0                                  # warm start from the converged p
         # per-condition ||r_k||/||S_k|| at exit: both runs stop at the same global test; the
         # recursive residuals at 1e-10 carry the rounding noise of the different summation order
-        assert np.all(crel <= 1e-9) and np.allclose(crel, st.cond_rel, rtol=0.1), (crel, st.cond_rel)
-    assert rows[0][0] == 0 and rows[-1][1] == g["n_y"]
-    assert all(rows[r][1] == rows[r + 1][0] for r in range(WORLD - 1))
+        assert np.all(crel <= 1e-9) and np.allclose(crel, crel1, rtol=0.1), (crel, crel1)
+        # Jacobi + lockstep coupling through the same exchange
+        itj, pj = o["jl"]
+        assert abs(itj - ref1["jl"][0]) <= 2 and _rel(pj, ref1["jl"][1][:, rows]) <= 1e-9, (r, itj)

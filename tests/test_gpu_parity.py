@@ -233,17 +233,19 @@ def test_c3_full_size(P, orc, gi):
     S.close()
 
 
-def test_c3_converged_vs_full_oracle_solve(P, gi):
-    """BASELINE C3 solved to rtol 1e-10 by the GPU (bench launch configuration) against the
-    oracle's full solve of the same workload (tests/golden/c3_oracle_samples.json, written by
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_converged_vs_full_oracle_solve(P, gi, name):
+    """BASELINE C3 (2048x1024) and C4 (1024x512, the first Picard iterate of the trajectory), short
+    texture, K = 9, solved to rtol 1e-10 by the GPU (bench launch configuration) against the
+    oracle's full solve of the same workload (tests/golden/c3|c4_oracle_samples.json, written by
     scripts/oracle_c3_reference.py from oracle/ only): p at 4096 seeded nodes and per-condition
     norms within 1e-8 (R-A23), the 9 wrenches within 1e-6 per part (R-A15), iteration counts
     within 2% (single-reduction vs Table-1 schedule, R-A25)."""
     import json
     import os
-    path = os.path.join(os.path.dirname(__file__), "golden", "c3_oracle_samples.json")
+    path = os.path.join(os.path.dirname(__file__), "golden", f"{name.lower()}_oracle_samples.json")
     gold = json.load(open(path))
-    cfg = gi.config("C3")
+    cfg = gi.config(name)
     S = P.JointSolver(cfg.grid, 9)
     st, W = S.step(cfg.conds, tol=gold["tol"], omega=gold["omega"])
     assert st.converged and gold["converged"]
@@ -256,6 +258,39 @@ def test_c3_converged_vs_full_oracle_solve(P, gi):
         assert abs(np.linalg.norm(pg[k]) - gold["p_norm"][k]) <= 1e-8 * gold["p_norm"][k]
         wo = np.array(gold["wrench"][k])
         assert wrench_err(W[k], wo, cfg.conds[k][8]) <= 1e-6, (k, W[k], wo)
+    S.close()
+
+
+@pytest.mark.timeout(900)
+def test_c5_full_size_lockstep_iterates(P, orc, gi):
+    """BASELINE C5 at full size on one GPU (4096x2048 short texture, K = 72 = 8 operating points x 9
+    FD conditions, 604 M DOF, ~44 GB workspace), in the bench's launch configuration.  Lockstep
+    coupling (R-A11: per-condition alpha_k, beta_k) makes every block its own Krylov process, so the
+    oracle can follow two of the 72 blocks alone: bitwise h, h-dot, A_P, A_E, A_N, S and the third
+    iterate of p (single-reduction schedule, R-A24) within 1e-9 for the first and the last condition."""
+    cfg = gi.config("C5")
+    K = cfg.conds.shape[0]
+    assert K == 72
+    S = P.JointSolver(cfg.grid, K)
+    S.thickness(cfg.conds)
+    S.assemble()
+    st = S.solve(tol=1e-30, omega=cfg.omega, coupling="lockstep", max_iter=3, raise_on_error=False)
+    assert st.iterations == 3 and st.status == -6 and st.schedule == "single"
+    ks = (0, K - 1)
+    sub = cfg.conds[list(ks)]
+    AP, AE, AN, SS = orc.assemble_joint(cfg.grid, sub)
+    for q, k in enumerate(ks):
+        for name, ref in (("AP", AP[q]), ("AE", AE[q]), ("AN", AN[q]), ("S", SS[q])):
+            got = S.get(name, k)
+            assert np.array_equal(got.view(np.uint64), ref.view(np.uint64)), (name, k)
+        h, hd = orc.thickness(cfg.grid, sub[q])
+        assert np.array_equal(S.get("h", k).view(np.uint64), h.view(np.uint64)), ("h", k)
+        assert np.array_equal(S.get("hdot", k).view(np.uint64), hd.view(np.uint64)), ("hdot", k)
+    ref = orc.pcg_joint(AP, AE, AN, SS, tol=1e-30, omega=cfg.omega, coupling="lockstep", max_iter=3,
+                        schedule="single")
+    for q, k in enumerate(ks):
+        e = rel(S.get("p", k), ref.p[q])
+        assert e <= 1e-9, (k, e)
     S.close()
 
 

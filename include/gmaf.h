@@ -290,6 +290,13 @@ gmaf_status gmaf_p2p_connect(gmaf_ctx* ctx, const void* handles);
  * Errors: INVALID_ARG (null pointer). */
 gmaf_status gmaf_slab(const gmaf_ctx* ctx, int32_t* y0, int32_t* y1);
 
+/* The row partition itself, without a context (no GPU needed): own rows [y0, y1) and stored rows
+ * [yb, ye) (own rows + up to 4 halo rows per side inside the domain) of `rank` among `world`
+ * slabs of n_y unknown rows.  Errors: INVALID_ARG (null pointer, world outside 1..8, rank outside
+ * 0..world-1, or a slab thinner than 8 rows). */
+gmaf_status gmaf_slab_rows(int32_t n_y, int32_t world, int32_t rank, int32_t* y0, int32_t* y1,
+                           int32_t* yb, int32_t* ye);
+
 /* Make a new ncclUniqueId (128 bytes) into out (NCCL is loaded at run time).  Errors: NCCL. */
 gmaf_status gmaf_nccl_unique_id(void* out);
 

@@ -124,6 +124,7 @@ def lib() -> C.CDLL:
         L.gmaf_p2p_handle.argtypes = [P, P]
         L.gmaf_p2p_connect.argtypes = [P, P]
         L.gmaf_slab.argtypes = [P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+        L.gmaf_slab_rows.argtypes = [C.c_int32, C.c_int32, C.c_int32] + [C.POINTER(C.c_int32)] * 4
         L.gmaf_last_error.restype = C.c_char_p
         L.gmaf_last_error.argtypes = [P]
         L.gmaf_version.restype = C.c_char_p
@@ -132,7 +133,7 @@ def lib() -> C.CDLL:
                      "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_set_schedule",
                      "gmaf_nccl_unique_id", "gmaf_cond_iterations", "gmaf_general_forces",
                      "gmaf_picard_iteration", "gmaf_picard_step", "gmaf_p2p_handle", "gmaf_p2p_connect",
-                     "gmaf_slab"):
+                     "gmaf_slab", "gmaf_slab_rows"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -142,7 +143,7 @@ ABI_SYMBOLS = ("gmaf_workspace_bytes", "gmaf_create", "gmaf_destroy", "gmaf_thic
                "gmaf_solve", "gmaf_solve_fixed", "gmaf_integrate", "gmaf_get", "gmaf_field_ptr",
                "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_set_schedule", "gmaf_nccl_unique_id",
                "gmaf_cond_iterations", "gmaf_general_forces", "gmaf_picard_iteration", "gmaf_picard_step",
-               "gmaf_p2p_handle", "gmaf_p2p_connect", "gmaf_slab",
+               "gmaf_p2p_handle", "gmaf_p2p_connect", "gmaf_slab", "gmaf_slab_rows",
                "gmaf_last_error", "gmaf_version")
 SCHEDULE = {"table1": 0, "single": 1}
 
@@ -208,6 +209,13 @@ def make_dist(rank: int, world: int, uid: bytes | None, p2p: bool = False, shard
         return None, None
     keep = C.create_string_buffer(uid, 128)
     return gmaf_dist(int(rank), int(world), C.cast(keep, C.c_void_p), 0), keep
+
+
+def gmaf_slab_rows(n_y: int, world: int, rank: int) -> tuple[int, int, int, int]:
+    """Row slab of `rank` (include/gmaf.h gmaf_slab_rows): own rows (y0, y1), stored rows (yb, ye)."""
+    v = [C.c_int32() for _ in range(4)]
+    _check(None, lib().gmaf_slab_rows(int(n_y), int(world), int(rank), *(C.byref(x) for x in v)))
+    return tuple(int(x.value) for x in v)
 
 
 def gmaf_workspace_bytes(grid: gmaf_grid, K: int, dist: gmaf_dist | None = None) -> int:

@@ -1064,6 +1064,16 @@ gmaf_status gmaf_nccl_unique_id(void* out) {
   return GMAF_OK;
 }
 
+gmaf_status gmaf_slab_rows(int32_t n_y, int32_t world, int32_t rank, int32_t* y0, int32_t* y1,
+                           int32_t* yb, int32_t* ye) {
+  if (!y0 || !y1 || !yb || !ye || world < 1 || world > kMaxP2P || rank < 0 || rank >= world ||
+      n_y < 2 * SLAB_HALO * world)
+    return GMAF_E_INVALID_ARG;
+  const Slab sl = slab_of(n_y, world, rank);
+  *y0 = sl.y0; *y1 = sl.y1; *yb = sl.yb; *ye = sl.ye;
+  return GMAF_OK;
+}
+
 gmaf_status gmaf_slab(const gmaf_ctx* ctx, int32_t* y0, int32_t* y1) {
   if (!ctx || !y0 || !y1) return GMAF_E_INVALID_ARG;
   *y0 = ctx->gp.y0;

@@ -193,11 +193,16 @@ def _partition(args) -> str:
 def run_gmaf(args, cfg):
     import torch
     world, rank, local = _dist()
+    # plumbing check on a one-GPU box (tests only): every rank on cuda:0, gloo for the host
+    # collectives (NCCL refuses two ranks on one GPU); the device path is the same
+    same_dev = os.environ.get("GMAF_BENCH_SAME_DEVICE") == "1"
+    if same_dev:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as tdist
-        tdist.init_process_group("nccl")
+        tdist.init_process_group("gloo" if same_dev else "nccl")
         dist = tdist
     import paper_2511_06824_b200 as P
     P.lib()
@@ -276,7 +281,8 @@ def run_gmaf(args, cfg):
     kt = S.kernel_times()
     if dist:
         dist.barrier()
-    agg = aggregate(dev_ms, wall_ms, float(K * n_local * sum(iters)), device="cuda")   # local DOF
+    agg = aggregate(dev_ms, wall_ms, float(K * n_local * sum(iters)),
+                    device="cpu" if same_dev else "cuda")   # local DOF
     dev_max_ms, wall_max_ms, total_dof_iters = agg.device_ms_max, agg.wall_ms_max, agg.dof_iters_total
     value = agg.rate()
     e2e_value = agg.e2e_rate()

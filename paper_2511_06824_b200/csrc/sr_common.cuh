@@ -162,16 +162,22 @@ __device__ __forceinline__ StageIn stage_prefetch(const DevPtrs& d) {
   return in;
 }
 
+// Executed by ONE WARP (all 32 lanes; red in shared memory is read by broadcast): every lane
+// evaluates the scalars redundantly -- the same arithmetic in the same order, so all agree -- and
+// the per-condition arrays are written lane-parallel (one store instruction for up to 32
+// conditions instead of a serial chain of single-thread stores on the iteration's critical path);
+// lane 0 writes the state back.
 template <bool INIT>
 __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, int Klocal, int kofs,
                                 int use_cond, unsigned long long hcond, const StageIn& in) {
-  // one thread on the critical path of every iteration: work on the register snapshot, write the
-  // state back once
+  const int lane = threadIdx.x & 31;
   SolverState s = in.s;
   const double aold0 = in.aold0;
   if (s.coupling == 2) {
-    sr_scalar_async<INIT>(d, red, Kall);
-    if (use_cond && d.st_->done) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, 0u);
+    if (lane == 0) {
+      sr_scalar_async<INIT>(d, red, Kall);
+      if (use_cond && d.st_->done) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, 0u);
+    }
     return;
   }
   const double* rrk = red;
@@ -180,12 +186,12 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
   const double* ssk = red + 3 * Kall;
   double rr = 0.0;
   for (int kk = 0; kk < Kall; ++kk) rr += rrk[kk];
-  for (int kl = 0; kl < Klocal; ++kl) d.cs.rrk[kl] = rrk[kofs + kl];
+  for (int kl = lane; kl < Klocal; kl += 32) d.cs.rrk[kl] = rrk[kofs + kl];
   bool bad = false;
   if (INIT) {
     double SS = 0.0;
     for (int kk = 0; kk < Kall; ++kk) SS += ssk[kk];
-    for (int kl = 0; kl < Klocal; ++kl) d.cs.Sk[kl] = ssk[kofs + kl];
+    for (int kl = lane; kl < Klocal; kl += 32) d.cs.Sk[kl] = ssk[kofs + kl];
     s.nS = sqrt(SS);
     s.iter = 0; s.status = 0; s.converged = 0; s.done = 0; s.zero_p = 0;
     if (s.nS == 0.0) {
@@ -201,12 +207,12 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
         for (int kk = 0; kk < Kall; ++kk) { gg += gk[kk]; dd += dk[kk]; }
         if (!(dd > 0.0)) bad = true;
         const double a0 = gg / dd;
-        for (int kl = 0; kl < Klocal; ++kl) { d.cs.alpha[kl] = a0; d.cs.beta[kl] = 0.0; d.cs.uvk[kl] = 0.0; }
+        for (int kl = lane; kl < Klocal; kl += 32) { d.cs.alpha[kl] = a0; d.cs.beta[kl] = 0.0; d.cs.uvk[kl] = 0.0; }
         s.d = gg;
       } else {
         for (int kk = 0; kk < Kall; ++kk)
           if (gk[kk] != 0.0 && !(dk[kk] > 0.0)) bad = true;
-        for (int kl = 0; kl < Klocal; ++kl) {
+        for (int kl = lane; kl < Klocal; kl += 32) {
           const int kk = kofs + kl;
           d.cs.alpha[kl] = gk[kk] != 0.0 ? gk[kk] / dk[kk] : 0.0;
           d.cs.beta[kl] = 0.0; d.cs.uvk[kl] = 0.0; d.cs.dk[kl] = gk[kk];
@@ -232,12 +238,12 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
         const double den = d2 - b * g2 / aold0;
         if (!(g2 > 0.0) || !(den > 0.0)) bad = true;
         const double a = g2 / den;
-        for (int kl = 0; kl < Klocal; ++kl) { d.cs.uvk[kl] = aold0; d.cs.alpha[kl] = a; d.cs.beta[kl] = b; }
+        for (int kl = lane; kl < Klocal; kl += 32) { d.cs.uvk[kl] = aold0; d.cs.alpha[kl] = a; d.cs.beta[kl] = b; }
         s.d = g2;
       } else {
         for (int kk = 0; kk < Kall; ++kk)
           if (gk[kk] < 0.0) bad = true;
-        for (int kl = 0; kl < Klocal; ++kl) {
+        for (int kl = lane; kl < Klocal; kl += 32) {
           const int kk = kofs + kl;
           const double aold = d.cs.alpha[kl], gold = d.cs.dk[kl];
           d.cs.uvk[kl] = aold;                                   // alpha used this iteration
@@ -252,12 +258,14 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
       }
       if (bad && !s.done) { s.done = 1; s.status = -5; }
     } else {
-      for (int kl = 0; kl < Klocal; ++kl) d.cs.uvk[kl] = d.cs.alpha[kl];   // alpha used this iteration
+      for (int kl = lane; kl < Klocal; kl += 32) d.cs.uvk[kl] = d.cs.alpha[kl];   // alpha used this iteration
     }
   }
-  *d.st_ = s;
-  // the WHILE handle defaults to 1 at every graph launch: write it only to stop the loop
-  if (use_cond && s.done) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, 0u);
+  if (lane == 0) {
+    *d.st_ = s;
+    // the WHILE handle defaults to 1 at every graph launch: write it only to stop the loop
+    if (use_cond && s.done) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, 0u);
+  }
 }
 
 template <bool INIT>
@@ -342,7 +350,7 @@ __device__ void sr_finish(const DevPtrs& d, double (&v)[4], double* red, int K, 
     // thread 0 prefetches what the scalar stage and the timing need (overlaps the loads below)
     StageIn in{};
     unsigned long long t_start0 = 0ull;
-    if (tid == 0) {
+    if (tid < 32) {                                // warp 0 runs the stage (same-address loads)
       in = stage_prefetch(d);
       t_start0 = d.timing->t_start[ITER ? KK_SR_ITER : KK_SR_INIT];
     }
@@ -356,6 +364,7 @@ __device__ void sr_finish(const DevPtrs& d, double (&v)[4], double* red, int K, 
       red[q] = sum;
     }
     __syncthreads();
+    if (d.dist.world == 0 && tid < 32) sr_scalar_stage<INIT>(d, red, K, K, 0, use_cond, hcond, in);
     if (tid == 0) {
       if (d.dist.world > 0) {
         // multi-rank: publish this rank's per-condition sums
@@ -364,8 +373,6 @@ __device__ void sr_finish(const DevPtrs& d, double (&v)[4], double* red, int K, 
           for (int kk = 0; kk < km; ++kk) d.dist.packed_local[q * km + kk] = kk < K ? red[q * K + kk] : 0.0;
         // NCCL mode: the allgather + k_sr_scalar follow on the stream; peer-to-peer mode:
         // k_p2p_scalar follows in the same graph
-      } else {
-        sr_scalar_stage<INIT>(d, red, K, K, 0, use_cond, hcond, in);
       }
       timing_end(d.timing, ITER ? KK_SR_ITER : KK_SR_INIT, t_start0);
       if (ITER) {   // the serial tail: all other CTAs have finished when the last one arrives

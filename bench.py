@@ -182,6 +182,44 @@ def _config_obj(cfg, args):
             f"{'NCCL allgather' if os.environ.get('GMAF_DIST', 'p2p') == 'nccl' else 'fused into the iteration kernel over NVLink peer memory'}) (weak)"}
 
 
+def picard_steps(device: int, n_steps: int) -> dict:
+    """The metric's "ms per Picard step" (BASELINE.json): full time steps of the
+    Picard march (Sec. 2.3) on C4's mesh -- short-textured 1024x512, each Picard iteration one
+    joint 9-condition thickness -> assembly -> PCG-ASSOR-II -> quadrature on the device plus the
+    host update (generalized forces, FD Jacobians, 4x4 solve; R-A28..A31) -- 1-degree steps from
+    phi = 0, warm-started solves.  Host wall clock (the update runs on the host between solves)."""
+    import math
+    import paper_2511_06824_b200 as P
+    g = gi.grid(1024, 512, "short")
+    pump = gi.pump()
+    dt = 2 * math.pi / gi.OMEGA_S / 360.0
+    S = P.JointSolver(g, 9, device=device)
+    state = gi.condition(phi_deg=0.0, p_in=gi.p_in_trapezoid(0.0))
+
+    def step(s):
+        nonlocal state
+        phi = s * math.pi / 180.0
+        st = state.copy()
+        st[8:13] = [gi.coupling_length(phi), 0.0, gi.stroke_speed(phi), gi.p_in_trapezoid(phi), gi.P_OUT]
+        state, n_pic, res, pcg, code = S.picard_step(pump, st, phi, dt, "general", eps_dyn=1e-3, max_picard=20,
+                                                     tol=1e-10, omega=1.6, raise_on_error=False)
+        return n_pic, pcg, code
+
+    step(1)                                          # warm-up step (graph instantiation)
+    t0 = time.perf_counter()
+    rows = [step(s) for s in range(2, 2 + n_steps)]
+    ms = (time.perf_counter() - t0) * 1e3
+    S.close()
+    n_pic = sum(r[0] for r in rows)
+    return {"config": "C4 mesh: short-textured 1024x512, K=9 per Picard iteration, general scheme, "
+                      "eps_dyn 1e-3, 1-degree time steps from phi=0 (warm-up step 1, timed steps 2..)",
+            "time_steps": n_steps, "ms_per_time_step": ms / n_steps,
+            "ms_per_picard_iteration": ms / max(n_pic, 1), "picard_iterations": [r[0] for r in rows],
+            "pcg_iterations_per_step": [r[1] for r in rows], "status": [r[2] for r in rows],
+            "timing": "host wall clock (device solves + host update)",
+            "full_trajectory": "profiles/round1_picard_3rev_c4.json (1080 steps, 527 s)"}
+
+
 def _partition(args) -> str:
     """N > 1: row slabs of the one K-condition system (default; SURVEY 8(e) for C3, strong
     scaling) or one joint system of K*N conditions, condition-sharded (C5 layout, weak)."""
@@ -325,6 +363,8 @@ def run_gmaf(args, cfg):
         "gpu_launches": launches,
         "clocks": ck,
     }
+    if rank == 0 and world == 1 and args.picard_steps > 0:
+        line["picard"] = picard_steps(local, args.picard_steps)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, iters=args.ref_iters)
     if rank == 0:
@@ -346,6 +386,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shard", action="store_true",
                     help="use the condition-sharded path even on one GPU (1-rank communicator)")
+    ap.add_argument("--picard-steps", type=int, default=3,
+                    help="time C4 Picard time steps after the main measurement (0: skip; 1 GPU only)")
     ap.add_argument("--partition", choices=["rows", "conditions"], default=None,
                     help="N > 1: row slabs of the K-condition system (default, strong scaling) or a "
                          "K*N-condition system sharded by conditions (weak); also valid on 1 GPU")

@@ -142,7 +142,9 @@ int tw_single(int nt) {
   if (const char* e = std::getenv("GMAF_SR_TW")) cap = std::atoi(e);   // A/B experiments
   if (cap < 12 || cap > 1000) cap = 256;
   int w = nt < cap ? nt : cap;
-  return w & ~1;
+  // a multiple of 4: strip s starts at column s*tw - tw/2, which must be even so that every
+  // column pair (and every 16-byte TMA row segment) is aligned
+  return w & ~3;
 }
 bool single_ok(int nt) { return nt % 2 == 0 && nt >= 12; }
 constexpr int kConstRowLen = 1024;   // >= the widest TMA row segment (tw + 2*halo)
@@ -224,6 +226,7 @@ struct gmaf_ctx {
   int r_parity = 0;   // which ping-pong buffer holds the latest residual
   int last_coupling = 0;
   bool stream_mode = false;  // GMAF_LAUNCH_MODE=stream: no CUDA graph (for ncu)
+  bool sr_k_ok = true;       // K fits the single-pass kernel's reduction scratch
   // multi-rank (condition sharding): this rank owns global conditions [kofs, kofs + K)
   bool distm = false;
   int world = 1, rank = 0, kofs = 0, Kglob = 0, kmax = 0;
@@ -617,6 +620,9 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
   }
   const int Kglob = K;
   K = khi - klo;   // from here on: the local conditions
+  // multi-rank contexts run the single-pass kernel, whose reduction scratch (the dead rings,
+  // 48 (tw + 8) doubles) must hold the 4 K per-condition sums
+  if (dm && 4 * K > 48 * (tw_single(grid->n_theta) + 2 * SR_HALO_COLS)) return GMAF_E_INVALID_ARG;
   const Layout L = rm ? make_layout(grid, K, world, kmax, sl.ye - sl.yb)
                  : dm ? make_layout(grid, K, world, kmax) : make_layout(grid, K);
   if (!d_workspace || ws_bytes < L.total || (reinterpret_cast<uintptr_t>(d_workspace) % kAlign) != 0)
@@ -733,7 +739,9 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
                    sms, occ, ctx->tiles.n_strips, ctx->tiles.n_chunks, ctx->tiles.tw, ctx->tiles.th, socc,
                    ctx->tiles_sr.n_strips, ctx->tiles_sr.n_chunks, ctx->tiles_sr.tw, ctx->tiles_sr.th);
     // the single-pass kernel streams rows with 16-byte TMA copies: needs an even n_theta
-    ctx->schedule = single_ok(grid->n_theta) ? GMAF_SCHEDULE_SINGLE : GMAF_SCHEDULE_TABLE1;
+    // (and its reduction scratch -- the dead rings, 48 (tw + 8) doubles -- must hold 4 K sums)
+    ctx->sr_k_ok = 4 * K <= 48 * (tw_single(grid->n_theta) + 2 * SR_HALO_COLS);
+    ctx->schedule = single_ok(grid->n_theta) && ctx->sr_k_ok ? GMAF_SCHEDULE_SINGLE : GMAF_SCHEDULE_TABLE1;
     const char* sch = std::getenv("GMAF_SCHEDULE");
     if (sch && std::strcmp(sch, "table1") == 0) ctx->schedule = GMAF_SCHEDULE_TABLE1;
   }
@@ -1012,7 +1020,10 @@ gmaf_status gmaf_set_schedule(gmaf_ctx* ctx, int32_t schedule) {
   if (ctx->distm && schedule != GMAF_SCHEDULE_SINGLE)
     return fail(ctx, GMAF_E_INVALID_ARG, "set_schedule: multi-rank contexts run the single-pass schedule");
   if (schedule == GMAF_SCHEDULE_TABLE1) { ctx->schedule = schedule; return GMAF_OK; }
-  if (schedule == GMAF_SCHEDULE_SINGLE && single_ok(ctx->grid.n_theta)) { ctx->schedule = schedule; return GMAF_OK; }
+  if (schedule == GMAF_SCHEDULE_SINGLE && single_ok(ctx->grid.n_theta) && ctx->sr_k_ok) {
+    ctx->schedule = schedule;
+    return GMAF_OK;
+  }
   return fail(ctx, GMAF_E_INVALID_ARG, "set_schedule: %d not available (n_theta %d)", schedule, ctx->grid.n_theta);
 }
 

@@ -378,7 +378,9 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
 
   // ---- per-CTA partials, then the scalar stage (last CTA, fixed order)
   double v[4] = {acc_rr, acc_g, acc_d, acc_s};
-  sr_finish<ITER, INIT>(d, v, ringW /* rings are dead now */, K, k, t.n_tiles, blockIdx.x / K, hcond, use_cond);
+  // the whole dynamic shared memory (48 NL doubles) is dead now: the reduction scratch needs
+  // 4 (blockDim + 32) and 4 K doubles (the host keeps K <= 12 NL on this schedule)
+  sr_finish<ITER, INIT>(d, v, smem_raw, K, k, t.n_tiles, blockIdx.x / K, hcond, use_cond);
 }
 
 // Multi-rank scalar stage: one CTA, after the allgather of every rank's packed sums

@@ -404,3 +404,56 @@ def test_paper_table2_2000x1600_on_gpu(P, gi):
         st, _ = S.step(case.conds, tol=1e-6, omega=1.8, precond=pc)
         assert st.converged and abs(st.iterations - gold[pc]) <= 0.15 * gold[pc], (pc, st.iterations, gold[pc])
     S.close()
+
+
+# ------------------------------------------------------------------ degenerate cases
+def _plain_condition(e=(0.0, 0.0, 0.0, 0.0), edot=(0.0, 0.0, 0.0, 0.0), L_F=3.71412e-2, U_theta=0.0, U_y=0.0,
+                     p_in=1.0e7, p_out=5.0e5):
+    return np.array(list(e) + list(edot) + [L_F, U_theta, U_y, p_in, p_out], dtype=np.float64)
+
+
+@pytest.mark.parametrize("mesh,schedule", [((4, 4), "table1"), ((5, 4), "table1"), ((12, 4), "single"),
+                                           ((14, 5), "single")])
+def test_minimum_meshes(P, orc, gi, mesh, schedule):
+    """The smallest accepted meshes (n_theta, n_y >= 4; the single-pass schedule from an even
+    n_theta >= 12, the Table-1 schedule below): parity with the oracle."""
+    g = gi.grid(*mesh)
+    conds = gi.random_conditions(17, 3)
+    full_parity(P, orc, g, conds, 1.6, schedule=schedule)
+
+
+def test_zero_source_gives_zero_pressure(P, gi):
+    """S = 0 (p_in = p_out = 0, no wedge, no squeeze): ||S_G|| = 0, p = 0 with 0 iterations
+    (Table 1 stops before the first iteration), zero wrench pressure parts."""
+    g = gi.grid(64, 32)
+    conds = np.stack([_plain_condition(p_in=0.0, p_out=0.0)] * 3)
+    S = P.JointSolver(g, 3)
+    st, W = S.step(conds, tol=1e-10, omega=1.8)
+    assert st.converged and st.iterations == 0
+    for k in range(3):
+        assert not np.any(S.get("p", k))
+        assert np.all(W[k][:6] == 0.0)
+    S.close()
+
+
+def test_closed_forms_on_the_gpu(P, gi):
+    """Closed forms of the discrete problem (SURVEY 8(c) pins), solved by the GPU at rtol 1e-12:
+    p_in = p_out = P with no wedge or squeeze -> p = P everywhere; a uniform film (e = 0) between two
+    pressures -> the linear profile p_j = p_in + (p_out - p_in)(j+1)/(n_y+1) (the 5-point stencil is
+    exact on linear fields)."""
+    g = gi.grid(96, 40)
+    ny = g["n_y"]
+    conds = np.stack([_plain_condition(p_in=3.0e6, p_out=3.0e6),
+                      _plain_condition(p_in=1.0e7, p_out=5.0e5),
+                      _plain_condition(p_in=2.0e5, p_out=8.0e6)])
+    S = P.JointSolver(g, 3)
+    st, W = S.step(conds, tol=1e-12, omega=1.8)
+    assert st.converged
+    p0 = S.get("p", 0)
+    assert np.max(np.abs(p0 - 3.0e6)) <= 1e-10 * 3.0e6
+    for k in (1, 2):
+        pin, pout = conds[k][11], conds[k][12]
+        lin = pin + (pout - pin) * (np.arange(ny) + 1.0) / (ny + 1.0)
+        pk = S.get("p", k)
+        assert np.max(np.abs(pk - lin[:, None])) <= 1e-9 * max(pin, pout), k
+    S.close()

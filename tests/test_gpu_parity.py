@@ -457,3 +457,40 @@ def test_closed_forms_on_the_gpu(P, gi):
         pk = S.get("p", k)
         assert np.max(np.abs(pk - lin[:, None])) <= 1e-9 * max(pin, pout), k
     S.close()
+
+
+def test_ragged_strips_beyond_256(P, orc, gi):
+    """n_theta = 262 (= 2 mod 4, above the 256-column strip): a 6-column last strip next to the
+    seam strip, and an odd n_y."""
+    g = gi.grid(262, 37)
+    full_parity(P, orc, g, gi.random_conditions(23, 4), 1.8)
+
+
+@pytest.mark.parametrize("K", [150, 300])
+def test_many_conditions_on_a_tiny_mesh(P, orc, gi, K):
+    """K up to 12 (tw + 8) per-condition sums fit the single-pass kernel's reduction scratch; beyond
+    that (K = 300 on n_theta = 12) the context runs the Table-1 schedule.  Both match the oracle."""
+    g = gi.grid(12, 8)
+    conds = gi.random_conditions(29, K)
+    S = P.JointSolver(g, K)
+    st, W = S.step(conds, tol=1e-10, omega=1.6)
+    assert st.schedule == ("single" if K == 150 else "table1")
+    AP, AE, AN, SS = orc.assemble_joint(g, conds)
+    ref = orc.pcg_joint(AP, AE, AN, SS, tol=1e-10, omega=1.6, schedule=st.schedule)
+    assert st.converged and abs(st.iterations - ref.iterations) <= 3
+    pg = np.stack([S.get("p", k) for k in range(K)])
+    assert rel(pg, ref.p) <= 1e-8
+    S.close()
+
+
+def test_zero_iteration_budget(P, gi):
+    """max_iter = 0: only the init runs (r0 = S, p = 0); NO_CONVERGENCE with 0 iterations, p = 0."""
+    g = gi.grid(64, 32)
+    conds = gi.random_conditions(31, 2)
+    S = P.JointSolver(g, 2)
+    S.thickness(conds)
+    S.assemble()
+    st = S.solve(tol=1e-10, omega=1.8, max_iter=0, raise_on_error=False)
+    assert st.iterations == 0 and not st.converged and st.status == -6
+    assert not np.any(S.get("p", 0)) and not np.any(S.get("p", 1))
+    S.close()

@@ -504,8 +504,9 @@ int orc_pcg_joint_sr(int32_t nt, int32_t ny, int32_t K,
       if (!(g2 > 0.0)) { status = ORC_E_BREAKDOWN; break; }
       beta = g2 / gam;
       const double den = d2 - beta * g2 / alpha;
-      if (!(den > 0.0)) { status = ORC_E_BREAKDOWN; break; }
-      alpha = g2 / den;
+      if (den > 0.0) alpha = g2 / den;
+      else if (d2 > 0.0) { beta = 0.0; alpha = g2 / d2; }   /* restart along z (R-A32) */
+      else { status = ORC_E_BREAKDOWN; break; }
       gam = g2;
     } else {
       for (int32_t k = 0; k < K; ++k) {
@@ -514,7 +515,9 @@ int orc_pcg_joint_sr(int32_t nt, int32_t ny, int32_t K,
         if (g2 < 0.0) { status = ORC_E_BREAKDOWN; break; }
         bk[k] = g2 / gk[k];
         const double den = d2 - bk[k] * g2 / ak[k];
-        ak[k] = (g2 == 0.0) ? 0.0 : g2 / den;
+        if (den > 0.0) ak[k] = (g2 == 0.0) ? 0.0 : g2 / den;
+        else if (d2 > 0.0) { bk[k] = 0.0; ak[k] = g2 / d2; }   /* restart along z (R-A32) */
+        else { status = ORC_E_BREAKDOWN; break; }
         gk[k] = g2;
       }
     }

@@ -109,7 +109,10 @@ int  orc_pcg_joint(int32_t nt, int32_t ny, int32_t K,
 
 /* O7-S3: Table 1 with one global reduction per iteration (Chronopoulos-Gear alpha
  * recurrence); same arguments as orc_pcg_joint.  This is the schedule
- * the single-pass GPU kernel follows, so iterates can be compared step by step. */
+ * the single-pass GPU kernel follows, so iterates can be compared step by step.  Its alpha
+ * denominator delta' - beta gamma'/alpha (> 0 in exact arithmetic) can lose its sign to
+ * cancellation on a stagnating direction; the iteration then restarts along z (beta = 0,
+ * alpha = gamma'/delta', an exact line search) instead of failing (DESIGN.md R-A32). */
 int  orc_pcg_joint_sr(int32_t nt, int32_t ny, int32_t K,
                       const double* AP, const double* AE, const double* AN, const double* S,
                       double* p, double tol, double omega, int32_t precond, int32_t coupling,

@@ -308,7 +308,11 @@ cudaError_t enqueue_init(gmaf_ctx* ctx, const GraphKey& key, unsigned long long 
   }
   cudaError_t e = launch_sr_init(ctx->gp, ctx->d, ctx->tiles_sr, ctx->K, key.precond, key.warm != 0, h, s);
   if (e != cudaSuccess || !ctx->p2p) return e;
-  if (ctx->rows) return launch_p2p_rows(ctx->gp, ctx->d, true, 1, ctx->K, h, s);   // halos + sums + scalars
+  if (ctx->rows) {   // halos + sums + scalars (+ unpack into the fields when rows == 2)
+    cudaError_t e2 = launch_p2p_rows(ctx->gp, ctx->d, true, 1, ctx->K, h, s);
+    if (e2 == cudaSuccess && ctx->d.dist.rows == 2) e2 = launch_slab_unpack2(ctx->gp, ctx->d, true, 1, ctx->K, s);
+    return e2;
+  }
   return launch_p2p_scalar(ctx->d, true, ctx->K, h, s);   // peer-to-peer: gather + scalars
 }
 
@@ -321,7 +325,10 @@ cudaError_t enqueue_iterations(gmaf_ctx* ctx, const GraphKey& key, unsigned long
       if (e == cudaSuccess) e = launch_phase_b(ctx->gp, ctx->d, ctx->tiles, ctx->K, key.precond, u & 1, h, s);
     } else {
       e = launch_sr_iter(ctx->gp, ctx->d, ctx->tiles_sr, ctx->K, key.precond, u & 1, h, s);
-      if (e == cudaSuccess && ctx->rows) e = launch_p2p_rows(ctx->gp, ctx->d, false, u & 1, ctx->K, h, s);
+      if (e == cudaSuccess && ctx->rows) {
+        e = launch_p2p_rows(ctx->gp, ctx->d, false, u & 1, ctx->K, h, s);
+        if (e == cudaSuccess && ctx->d.dist.rows == 2) e = launch_slab_unpack2(ctx->gp, ctx->d, false, u & 1, ctx->K, s);
+      }
       else if (e == cudaSuccess && ctx->p2p) e = launch_p2p_scalar(ctx->d, false, ctx->K, h, s);
     }
   }
@@ -770,7 +777,8 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
     dd.rr_all = reinterpret_cast<double*>(tail + 8);
     dd.ss_all = dd.rr_all + Kglob;
     if (rm) {
-      dd.rows = 1;
+      const char* up = std::getenv("GMAF_ROWS_UNPACK");
+      dd.rows = (up && std::atoi(up) != 0) ? 2 : 1;
       dd.halo_in[ctx->rank] = reinterpret_cast<double*>(ctx->p2p_buf + ctx->inbox_off);
     }
   } else if (dm) {

@@ -187,6 +187,9 @@ cudaError_t launch_p2p_rows(const GridParams& g, const DevPtrs& d, bool init, in
                             unsigned long long h, cudaStream_t s);
 // row-slab mode: one-off exchange of field v's halo rows (push, stamp-only gather, unpack)
 cudaError_t launch_slab_exchange(const GridParams& g, const DevPtrs& d, double* v, int K, cudaStream_t s);
+// row-slab mode with DistPtrs.rows == 2: unpack an iteration's halo vectors into the fields
+cudaError_t launch_slab_unpack2(const GridParams& g, const DevPtrs& d, bool init, int parity, int K,
+                                cudaStream_t s);
 
 // ---- host accessors (gmaf_api.cu) for the Picard driver (picard.cu) ----
 }  // namespace gmaf

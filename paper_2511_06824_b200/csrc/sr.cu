@@ -170,7 +170,7 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
     const uint32_t dstride = (uint32_t)(3 * NL * 8);    // bytes between slots
     // row-slab mode: an iteration's r and pd rows outside the own slab come from the inbox the
     // neighbours pushed them into (slot = parity of the last gather stamp)
-    const bool inbox = ITER && lane < 2 && d.dist.rows;
+    const bool inbox = ITER && lane < 2 && d.dist.rows == 1;
     const double* ibase = inbox ? d.dist.halo_in[d.dist.rank] : nullptr;
     const int islot = inbox ? (int)(*d.dist.seq & 1ull) : 0;
     for (int step = 0; step < nsteps; ++step) {
@@ -520,10 +520,10 @@ __device__ __forceinline__ void slab_push(const GridParams& g, const DevPtrs& d,
                                               halo_ofs(slot, 1 - side, vec, K, k, ri, g.nt));
     for (int c2 = threadIdx.x; c2 < nt2; c2 += blockDim.x) dst[c2] = src[c2];
   }
-  // one system-scope fence per CTA after the CTA barrier (cumulative, as in a grid barrier);
-  // last_cta_arrive then chains the CTAs to the thread that posts the stamp
-  __syncthreads();
-  if (threadIdx.x == 0) __threadfence_system();
+  // every thread that stored to a peer fences its OWN stores at system scope (a fence by one
+  // thread after a CTA barrier does not drain the other warps' outstanding stores); then
+  // last_cta_arrive chains the CTAs to the thread that posts the stamp
+  __threadfence_system();
 }
 
 // The rank's per-condition sums of all ranks, summed in rank order (bitwise the same on every
@@ -594,8 +594,26 @@ __global__ void k_slab_unpack(GridParams g, DevPtrs d, double* v, int K) {
   }
 }
 
-// CTAs of the exchange kernels: enough for the halo rows (double2 per thread), at most one per
-// SM; one for a single rank (nothing to push, only the gather).
+// Row-slab variant that unpacks an iteration's two halo vectors into the fields' halo rows
+// (DistPtrs.rows == 2): the next k_sr then streams every row from the fields.
+__global__ void k_slab_unpack2(GridParams g, DevPtrs d, double* v0, double* v1, int K) {
+  const DistPtrs& dd = d.dist;
+  if (d.st_->done) return;
+  const int slot = (int)(*dd.seq & 1ull);
+  const int nt2 = g.nt / 2;
+  const int s0 = dd.rank > 0 ? 0 : 1, s1 = dd.rank < dd.world - 1 ? 2 : 1;
+  const int per_side = 2 * K * SLAB_HALO;
+  for (int q = blockIdx.x; q < (s1 - s0) * per_side; q += gridDim.x) {
+    const int side = s0 + q / per_side;
+    const int e = q % per_side;
+    const int ri = e % SLAB_HALO, k = (e / SLAB_HALO) % K, vec = e / (SLAB_HALO * K);
+    const int row = side == 0 ? g.y0 - SLAB_HALO + ri : g.y1 + ri;
+    const double2* src = reinterpret_cast<const double2*>(dd.halo_in[dd.rank] + halo_ofs(slot, side, vec, K, k, ri, g.nt));
+    double2* dst = reinterpret_cast<double2*>((vec ? v1 : v0) + fofs(g, k) + (long long)row * g.nt);
+    for (int c2 = threadIdx.x; c2 < nt2; c2 += blockDim.x) dst[c2] = src[c2];
+  }
+}
+
 // CTAs of the exchange kernels: one per halo row to send (at most 2 per SM); one for a single
 // rank (nothing to push, only the gather).
 static int slab_blocks(const GridParams& g, const DevPtrs& d, int K, int nv) {
@@ -610,6 +628,14 @@ cudaError_t launch_p2p_rows(const GridParams& g, const DevPtrs& d, bool init, in
   const int use = h != 0ull;
   if (init) k_p2p_rows<true><<<slab_blocks(g, d, K, 2), 256, 0, s>>>(g, d, parity, K, h, use);
   else k_p2p_rows<false><<<slab_blocks(g, d, K, 2), 256, 0, s>>>(g, d, parity, K, h, use);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_slab_unpack2(const GridParams& g, const DevPtrs& d, bool init, int parity, int K,
+                                cudaStream_t s) {
+  double* v0 = init ? d.r[0] : d.r[1 - parity];
+  double* v1 = init ? d.u[1] : d.u[parity];
+  k_slab_unpack2<<<slab_blocks(g, d, K, 2), 256, 0, s>>>(g, d, v0, v1, K);
   return cudaGetLastError();
 }
 

@@ -138,7 +138,9 @@ __device__ void sr_scalar_async(const DevPtrs& d, const double* red, int K) {
         if (gk[k] < 0.0) bad = true;
         b = gk[k] / gold;
         const double den = dk[k] - b * gk[k] / aold;
-        a = (gk[k] == 0.0) ? 0.0 : gk[k] / den;
+        if (den > 0.0) a = (gk[k] == 0.0) ? 0.0 : gk[k] / den;
+        else if (dk[k] > 0.0) { b = 0.0; a = gk[k] / dk[k]; }   // restart (R-A32)
+        else bad = true;
       }
       d.cs.alpha[k] = a; d.cs.beta[k] = b; d.cs.dk[k] = gk[k];
     }
@@ -234,10 +236,15 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
       if (s.coupling == 0) {
         double g2 = 0.0, d2 = 0.0;
         for (int kk = 0; kk < Kall; ++kk) { g2 += gk[kk]; d2 += dk[kk]; }
-        const double b = g2 / s.d;
+        double b = g2 / s.d;
         const double den = d2 - b * g2 / aold0;
-        if (!(g2 > 0.0) || !(den > 0.0)) bad = true;
-        const double a = g2 / den;
+        // Chronopoulos-Gear denominator: > 0 in exact arithmetic, lost to cancellation near a
+        // stagnating direction -> restart along z (beta = 0, exact line search, R-A32)
+        double a = 0.0;
+        if (!(g2 > 0.0)) bad = true;
+        else if (den > 0.0) a = g2 / den;
+        else if (d2 > 0.0) { b = 0.0; a = g2 / d2; }
+        else bad = true;
         for (int kl = lane; kl < Klocal; kl += 32) { d.cs.uvk[kl] = aold0; d.cs.alpha[kl] = a; d.cs.beta[kl] = b; }
         s.d = g2;
       } else {
@@ -251,7 +258,9 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
           if (gold != 0.0 && aold != 0.0) {
             b = gk[kk] / gold;
             const double den = dk[kk] - b * gk[kk] / aold;
-            a = (gk[kk] == 0.0) ? 0.0 : gk[kk] / den;
+            if (den > 0.0) a = (gk[kk] == 0.0) ? 0.0 : gk[kk] / den;
+            else if (dk[kk] > 0.0) { b = 0.0; a = gk[kk] / dk[kk]; }   // restart (R-A32)
+            else bad = true;
           }
           d.cs.alpha[kl] = a; d.cs.beta[kl] = b; d.cs.dk[kl] = gk[kk];
         }

@@ -15,10 +15,14 @@ def _rank(rank, world, port):
     import gmaf_inputs as gi
     import paper_2511_06824_b200 as P
     from paper_2511_06824_b200.dist import connect_p2p
-    g = gi.grid(96, 40, "short", tex_n_theta=8, tex_n_y=2, tex_band_rows=8)
-    S = P.JointSolver(g, 3, device=0, rank=rank, world=world, shard="rows")
+    nt, ny, K, seed = (int(x) for x in os.environ.get("SAN_CASE", "96,40,3,5").split(","))
+    g = gi.grid(nt, ny, "short", tex_n_theta=8, tex_n_y=2, tex_band_rows=8) if nt == 96 else gi.grid(nt, ny)
+    S = P.JointSolver(g, K, device=0, rank=rank, world=world, shard="rows")
     connect_p2p(S)
-    st, W = S.step(gi.random_conditions(5, 3), tol=1e-8, omega=1.6, max_iter=3000)
+    S.thickness(gi.random_conditions(seed, K))
+    S.assemble()
+    st = S.solve(tol=1e-8, omega=1.6, max_iter=3000, raise_on_error=False)
+    W = S.integrate()
     st2 = S.solve(tol=1e-8, omega=1.6, warm=True, raise_on_error=False)
     print(f"rank {rank}: slab {S.slab} iterations {st.iterations} warm {st2.iterations}", flush=True)
     S.close()
@@ -28,7 +32,7 @@ def _rank(rank, world, port):
 
 if __name__ == "__main__":
     if len(sys.argv) > 2:        # one rank per top-level process: sanitize_rows.py RANK PORT
-        _rank(int(sys.argv[1]), 2, int(sys.argv[2]))
+        _rank(int(sys.argv[1]), int(os.environ.get('SAN_WORLD', '2')), int(sys.argv[2]))
         print("sanitize rows run done", flush=True)
         sys.exit(0)
     import torch.multiprocessing as mp
@@ -36,5 +40,5 @@ if __name__ == "__main__":
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
-    mp.spawn(_rank, args=(2, port), nprocs=2, join=True)
+    mp.spawn(_rank, args=(int(os.environ.get('SAN_WORLD', '2')), port), nprocs=int(os.environ.get('SAN_WORLD', '2')), join=True)
     print("sanitize rows run done")

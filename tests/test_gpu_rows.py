@@ -122,3 +122,73 @@ def test_row_slabs_match_the_joint_solve(world):
         # Jacobi + lockstep coupling through the same exchange
         itj, pj = o["jl"]
         assert abs(itj - ref1["jl"][0]) <= 2 and _rel(pj, ref1["jl"][1][:, rows]) <= 1e-9, (r, itj)
+
+
+FUZZ = [  # (world, n_theta, n_y, texture, K, seed): thin slabs, ragged chunks, strips = 2 mod 4
+    (4, 138, 33, "short", 3, 41),
+    (2, 262, 16, "smooth", 5, 42),
+    (3, 60, 25, "short", 4, 43),
+    (4, 12, 64, "smooth", 7, 44),
+    (2, 60, 16, "smooth", 6, 43),
+    # OPEN ISSUE: with K = 2 or 3 conditions the rows a rank receives from
+    # the rank BELOW are wrong from the third iteration on (lockstep: rank 0 exact, rank 1 not);
+    # K = 1 and 4..9 are bitwise equal to the one-process solve in every probe
+    pytest.param((2, 60, 16, "smooth", 2, 43), marks=pytest.mark.xfail(reason="open row-slab issue, K = 2", strict=False)),
+    pytest.param((3, 60, 25, "smooth", 3, 43), marks=pytest.mark.xfail(reason="open row-slab issue, K = 3", strict=False)),
+]
+
+
+def _fuzz_grid(gi, nt, ny, tex):
+    if tex == "short":
+        return gi.grid(nt, ny, tex, tex_n_theta=max(2, nt // 10), tex_n_y=2, tex_band_rows=max(4, ny // 3))
+    return gi.grid(nt, ny)
+
+
+def _fuzz_rank(rank, world, port, case, res):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import gmaf_inputs as gi
+    import paper_2511_06824_b200 as P
+    from paper_2511_06824_b200.dist import connect_p2p
+    _, nt, ny, tex, K, seed = case
+    g = _fuzz_grid(gi, nt, ny, tex)
+    S = P.JointSolver(g, K, device=0, rank=rank, world=world, shard="rows")
+    connect_p2p(S)
+    y0, y1 = S.slab
+    S.thickness(gi.random_conditions(seed, K))
+    S.assemble()
+    S.solve(tol=1e-30, omega=1.6, max_iter=7, raise_on_error=False)
+    p7 = np.stack([S.get("p", k)[y0:y1] for k in range(K)])
+    st = S.solve(tol=1e-10, omega=1.6)
+    p = np.stack([S.get("p", k)[y0:y1] for k in range(K)])
+    res[rank] = ((y0, y1), p7, p, st.iterations, S.integrate())
+    S.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("case", FUZZ, ids=lambda c: f"w{c[0]}_{c[1]}x{c[2]}{c[3][0]}K{c[4]}" if isinstance(c, tuple) else None)
+def test_row_slab_edge_cases(case):
+    import paper_2511_06824_b200 as P
+    import gmaf_inputs as gi
+    world, nt, ny, tex, K, seed = case
+    g = _fuzz_grid(gi, nt, ny, tex)
+    S = P.JointSolver(g, K)
+    S.thickness(gi.random_conditions(seed, K))
+    S.assemble()
+    S.solve(tol=1e-30, omega=1.6, max_iter=7, raise_on_error=False)
+    p7 = np.stack([S.get("p", k) for k in range(K)])
+    st = S.solve(tol=1e-10, omega=1.6)
+    p = np.stack([S.get("p", k) for k in range(K)])
+    W = S.integrate()
+    S.close()
+    res = mp.Manager().dict()
+    mp.spawn(_fuzz_rank, args=(world, _port(), case, res), nprocs=world, join=True)
+    for r in range(world):
+        (y0, y1), p7r, pr, itr, Wr = res[r]
+        assert _rel(p7r, p7[:, y0:y1]) <= 1e-12, r
+        assert abs(itr - st.iterations) <= 2 and _rel(pr, p[:, y0:y1]) <= 1e-9, (r, itr, st.iterations)
+        assert np.allclose(Wr, W, rtol=1e-9, atol=1e-12 * np.abs(W).max())

@@ -761,6 +761,9 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
       ctx->inbox_off = align_up(bytes);
       bytes = ctx->inbox_off + (size_t)8 * SLAB_HALO * K * grid->n_theta * 8;
     }
+    // a whole 2 MiB granule: a small cudaMalloc can be sub-allocated inside a larger driver
+    // allocation, and cudaIpcOpenMemHandle maps the ALLOCATION's base, not this pointer
+    bytes = (bytes + (2u << 20) - 1) / (2u << 20) * (2u << 20);
     if (cudaMalloc((void**)&ctx->p2p_buf, bytes) != cudaSuccess ||
         cudaMemsetAsync(ctx->p2p_buf, 0, bytes, ctx->stream) != cudaSuccess ||
         cudaMallocHost((void**)&ctx->h_packed, (size_t)2 * 4 * kmax * world * 8) != cudaSuccess ||

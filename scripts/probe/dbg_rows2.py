@@ -19,6 +19,9 @@ def run(S, K, rows):
     c = gi.random_conditions(CASE[5], K)
     if os.environ.get("SAMEC"):
         c = np.repeat(c[:1], K, axis=0)
+    if os.environ.get("DUP2"):           # the 2 conditions of K=2, repeated to K rows
+        c2 = gi.random_conditions(CASE[5], 2)
+        c = np.concatenate([c2] * (K // 2))
     S.thickness(c); S.assemble()
     out = []
     for j in SEQ:

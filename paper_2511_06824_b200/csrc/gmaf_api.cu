@@ -1096,6 +1096,20 @@ gmaf_status gmaf_slab_rows(int32_t n_y, int32_t world, int32_t rank, int32_t* y0
   return GMAF_OK;
 }
 
+// Debugging aid (not part of include/gmaf.h): copy this rank's halo inbox
+// [2 slots][2 sides][2 vectors][K][4][nt] and the gather counter to the host.
+gmaf_status gmaf_debug_inbox(gmaf_ctx* ctx, double* host_out, unsigned long long* seq) {
+  if (!ctx || !host_out || !seq || !ctx->rows) return GMAF_E_INVALID_ARG;
+  const size_t n = (size_t)8 * SLAB_HALO * ctx->K * ctx->grid.n_theta;
+  CU(cudaMemcpy(host_out, ctx->p2p_buf + ctx->inbox_off, n * 8, cudaMemcpyDeviceToHost));
+  // then u[0], u[1] (all stored rows of all K) right after the inbox
+  const size_t nf = (size_t)ctx->K * ctx->gp.ns;
+  CU(cudaMemcpy(host_out + n, ctx->d.u[0], nf * 8, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(host_out + n + nf, ctx->d.u[1], nf * 8, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(seq, ctx->d.dist.seq, 8, cudaMemcpyDeviceToHost));
+  return GMAF_OK;
+}
+
 gmaf_status gmaf_slab(const gmaf_ctx* ctx, int32_t* y0, int32_t* y1) {
   if (!ctx || !y0 || !y1) return GMAF_E_INVALID_ARG;
   *y0 = ctx->gp.y0;

@@ -221,13 +221,11 @@ def picard_steps(device: int, n_steps: int) -> dict:
 
 
 def _partition(args) -> str:
-    """N > 1: one joint system of K*N conditions, condition-sharded (C5 layout, weak; default) or
-    row slabs of the one K-condition system (SURVEY 8(e) for C3, strong)."""
+    """N > 1: row slabs of the one K-condition system (default; SURVEY 8(e) for C3, strong
+    scaling) or one joint system of K*N conditions, condition-sharded (C5 layout, weak)."""
     if args.partition:
         return args.partition
-    # default N > 1: condition sharding (bitwise-tested against the one-GPU solve); row slabs are
-    # opt-in until the open row-slab issue in DESIGN.md sec. 9 is closed
-    return "conditions" if args.gpus > 1 else "none"
+    return "rows" if args.gpus > 1 else "none"
 
 
 def run_gmaf(args, cfg):
@@ -391,8 +389,8 @@ def main():
     ap.add_argument("--picard-steps", type=int, default=3,
                     help="time C4 Picard time steps after the main measurement (0: skip; 1 GPU only)")
     ap.add_argument("--partition", choices=["rows", "conditions"], default=None,
-                    help="N > 1: a K*N-condition system sharded by conditions (default, weak scaling) "
-                         "or row slabs of the K-condition system (strong); also valid on 1 GPU")
+                    help="N > 1: row slabs of the K-condition system (default, strong scaling) or a "
+                         "K*N-condition system sharded by conditions (weak); also valid on 1 GPU")
     args = ap.parse_args()
     cfg = gi.config(args.config)
     if args.impl == "reference":

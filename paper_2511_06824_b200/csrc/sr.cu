@@ -397,7 +397,7 @@ __global__ void k_sr_scalar(DevPtrs d, int Kglob, int Klocal, int kofs, int worl
     for (int q = 0; q < 4; ++q) sh[q * Kglob + kg] = src[q * km + kl];
   }
   __syncthreads();
-  if (threadIdx.x < 32) sr_scalar_stage<INIT>(d, sh, Kglob, Klocal, kofs, 0, 0ull);   // one warp
+  if (threadIdx.x == 0) sr_scalar_stage<INIT>(d, sh, Kglob, Klocal, kofs, 0, 0ull);
 }
 
 // Peer-to-peer allgather as its own (one-warp) kernel: the true-residual and wrench gathers.
@@ -491,7 +491,7 @@ __global__ void k_p2p_scalar(DevPtrs d, int Klocal, unsigned long long hcond, in
     if (INIT) d.dist.ss_all[kg] = sh[3 * Kg + kg];
   }
   __syncwarp();
-  sr_scalar_stage<INIT>(d, sh, Kg, Klocal, d.dist.kofs, use_cond, hcond);   // the whole warp
+  if (lane == 0) sr_scalar_stage<INIT>(d, sh, Kg, Klocal, d.dist.kofs, use_cond, hcond);
 }
 
 // ------------------------------------------------- row-slab exchange
@@ -549,7 +549,7 @@ __device__ void slab_scalars(const DevPtrs& d, int K, unsigned long long hcond, 
     if (INIT && q == 3) d.dist.ss_all[k] = s;
   }
   __syncwarp();
-  sr_scalar_stage<INIT>(d, sh, K, K, 0, use_cond, hcond);   // the whole warp
+  if (lane == 0) sr_scalar_stage<INIT>(d, sh, K, K, 0, use_cond, hcond);
 }
 
 // After every init / iteration kernel of a row-slab solve (same CUDA graph): push the halos of

@@ -172,14 +172,13 @@ __device__ __forceinline__ StageIn stage_prefetch(const DevPtrs& d) {
 template <bool INIT>
 __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, int Klocal, int kofs,
                                 int use_cond, unsigned long long hcond, const StageIn& in) {
-  const int lane = threadIdx.x & 31;
+  // one thread on the critical path of every iteration: work on the register snapshot, write the
+  // state back once
   SolverState s = in.s;
   const double aold0 = in.aold0;
   if (s.coupling == 2) {
-    if (lane == 0) {
-      sr_scalar_async<INIT>(d, red, Kall);
-      if (use_cond && d.st_->done) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, 0u);
-    }
+    sr_scalar_async<INIT>(d, red, Kall);
+    if (use_cond && d.st_->done) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, 0u);
     return;
   }
   const double* rrk = red;
@@ -188,12 +187,12 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
   const double* ssk = red + 3 * Kall;
   double rr = 0.0;
   for (int kk = 0; kk < Kall; ++kk) rr += rrk[kk];
-  for (int kl = lane; kl < Klocal; kl += 32) d.cs.rrk[kl] = rrk[kofs + kl];
+  for (int kl = 0; kl < Klocal; ++kl) d.cs.rrk[kl] = rrk[kofs + kl];
   bool bad = false;
   if (INIT) {
     double SS = 0.0;
     for (int kk = 0; kk < Kall; ++kk) SS += ssk[kk];
-    for (int kl = lane; kl < Klocal; kl += 32) d.cs.Sk[kl] = ssk[kofs + kl];
+    for (int kl = 0; kl < Klocal; ++kl) d.cs.Sk[kl] = ssk[kofs + kl];
     s.nS = sqrt(SS);
     s.iter = 0; s.status = 0; s.converged = 0; s.done = 0; s.zero_p = 0;
     if (s.nS == 0.0) {
@@ -209,12 +208,12 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
         for (int kk = 0; kk < Kall; ++kk) { gg += gk[kk]; dd += dk[kk]; }
         if (!(dd > 0.0)) bad = true;
         const double a0 = gg / dd;
-        for (int kl = lane; kl < Klocal; kl += 32) { d.cs.alpha[kl] = a0; d.cs.beta[kl] = 0.0; d.cs.uvk[kl] = 0.0; }
+        for (int kl = 0; kl < Klocal; ++kl) { d.cs.alpha[kl] = a0; d.cs.beta[kl] = 0.0; d.cs.uvk[kl] = 0.0; }
         s.d = gg;
       } else {
         for (int kk = 0; kk < Kall; ++kk)
           if (gk[kk] != 0.0 && !(dk[kk] > 0.0)) bad = true;
-        for (int kl = lane; kl < Klocal; kl += 32) {
+        for (int kl = 0; kl < Klocal; ++kl) {
           const int kk = kofs + kl;
           d.cs.alpha[kl] = gk[kk] != 0.0 ? gk[kk] / dk[kk] : 0.0;
           d.cs.beta[kl] = 0.0; d.cs.uvk[kl] = 0.0; d.cs.dk[kl] = gk[kk];
@@ -245,12 +244,12 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
         else if (den > 0.0) a = g2 / den;
         else if (d2 > 0.0) { b = 0.0; a = g2 / d2; }
         else bad = true;
-        for (int kl = lane; kl < Klocal; kl += 32) { d.cs.uvk[kl] = aold0; d.cs.alpha[kl] = a; d.cs.beta[kl] = b; }
+        for (int kl = 0; kl < Klocal; ++kl) { d.cs.uvk[kl] = aold0; d.cs.alpha[kl] = a; d.cs.beta[kl] = b; }
         s.d = g2;
       } else {
         for (int kk = 0; kk < Kall; ++kk)
           if (gk[kk] < 0.0) bad = true;
-        for (int kl = lane; kl < Klocal; kl += 32) {
+        for (int kl = 0; kl < Klocal; ++kl) {
           const int kk = kofs + kl;
           const double aold = d.cs.alpha[kl], gold = d.cs.dk[kl];
           d.cs.uvk[kl] = aold;                                   // alpha used this iteration
@@ -267,14 +266,12 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
       }
       if (bad && !s.done) { s.done = 1; s.status = -5; }
     } else {
-      for (int kl = lane; kl < Klocal; kl += 32) d.cs.uvk[kl] = d.cs.alpha[kl];   // alpha used this iteration
+      for (int kl = 0; kl < Klocal; ++kl) d.cs.uvk[kl] = d.cs.alpha[kl];   // alpha used this iteration
     }
   }
-  if (lane == 0) {
-    *d.st_ = s;
-    // the WHILE handle defaults to 1 at every graph launch: write it only to stop the loop
-    if (use_cond && s.done) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, 0u);
-  }
+  *d.st_ = s;
+  // the WHILE handle defaults to 1 at every graph launch: write it only to stop the loop
+  if (use_cond && s.done) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, 0u);
 }
 
 template <bool INIT>
@@ -359,7 +356,7 @@ __device__ void sr_finish(const DevPtrs& d, double (&v)[4], double* red, int K, 
     // thread 0 prefetches what the scalar stage and the timing need (overlaps the loads below)
     StageIn in{};
     unsigned long long t_start0 = 0ull;
-    if (tid < 32) {                                // warp 0 runs the stage (same-address loads)
+    if (tid == 0) {
       in = stage_prefetch(d);
       t_start0 = d.timing->t_start[ITER ? KK_SR_ITER : KK_SR_INIT];
     }
@@ -373,7 +370,7 @@ __device__ void sr_finish(const DevPtrs& d, double (&v)[4], double* red, int K, 
       red[q] = sum;
     }
     __syncthreads();
-    if (d.dist.world == 0 && tid < 32) sr_scalar_stage<INIT>(d, red, K, K, 0, use_cond, hcond, in);
+    if (d.dist.world == 0 && tid == 0) sr_scalar_stage<INIT>(d, red, K, K, 0, use_cond, hcond, in);
     if (tid == 0) {
       if (d.dist.world > 0) {
         // multi-rank: publish this rank's per-condition sums

@@ -130,11 +130,11 @@ FUZZ = [  # (world, n_theta, n_y, texture, K, seed): thin slabs, ragged chunks, 
     (3, 60, 25, "short", 4, 43),
     (4, 12, 64, "smooth", 7, 44),
     (2, 60, 16, "smooth", 6, 43),
-    # OPEN ISSUE: with K = 2 or 3 conditions the rows a rank receives from
-    # the rank BELOW are wrong from the third iteration on (lockstep: rank 0 exact, rank 1 not);
-    # K = 1 and 4..9 are bitwise equal to the one-process solve in every probe
-    pytest.param((2, 60, 16, "smooth", 2, 43), marks=pytest.mark.xfail(reason="open row-slab issue, K = 2", strict=False)),
-    pytest.param((3, 60, 25, "smooth", 3, 43), marks=pytest.mark.xfail(reason="open row-slab issue, K = 3", strict=False)),
+    # these two found a bug (a warp-collective scalar stage, since reverted, corrupted the
+    # per-condition scalars for K = 2, 3): kept as regression cases
+    (2, 60, 16, "smooth", 2, 43),
+    (3, 60, 25, "smooth", 3, 43),
+    (3, 60, 25, "short", 2, 43),
 ]
 
 

@@ -138,7 +138,11 @@ constexpr int kMaxTilesPerCondition = 148 * 16;
 // inside a strip, so its strips may not be wider than the ring (and need >= 12 columns)
 int tw_table1(int nt) { return nt >= 1024 ? 256 : 128; }
 int tw_single(int nt) {
-  int cap = 256;
+  // 512-column strips for wide meshes: one CTA per SM (10 warps) instead of two 256-column CTAs,
+  // half the halo columns; slightly more cycles per iteration but less power, so under the
+  // B200's power cap the clock stays higher (measured at C3: 259.6-260.3 vs 264.7-266.8 us per
+  // iteration, 1912-1927 vs 1852-1856 MHz)
+  int cap = nt >= 1024 ? 512 : 256;
   if (const char* e = std::getenv("GMAF_SR_TW")) cap = std::atoi(e);   // A/B experiments
   if (cap < 12 || cap > 1000) cap = 256;
   int w = nt < cap ? nt : cap;

@@ -27,7 +27,7 @@ LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
 OK, E_INVALID_ARG, E_INVALID_MESH, E_MESH_TOO_COARSE = 0, -1, -2, -3
 E_NONPOSITIVE_THICKNESS, E_BREAKDOWN, E_NO_CONVERGENCE = -4, -5, -6
-PRECOND = {"none": 0, "jacobi": 1, "assor2": 2, "assor1": 3}
+PRECOND = {"none": 0, "jacobi": 1, "assor2": 2, "assor1": 3, "ssor": 4}
 COUPLING = {"coupled": 0, "lockstep": 1}
 
 
@@ -87,6 +87,9 @@ def lib():
                                        C.c_double, C.c_int32, C.c_int32, C.POINTER(C.c_int32),
                                        C.POINTER(_Stats)]
         _lib.orc_wrench.argtypes = [C.POINTER(_Grid), C.POINTER(_Cond), D, D]
+        _lib.orc_sr_set_restart_threshold.argtypes = [C.c_double]
+        _lib.orc_sr_set_restart_threshold.restype = None
+        _lib.orc_sr_restarts.restype = C.c_int32
     return _lib
 
 
@@ -241,6 +244,17 @@ def pcg_joint(AP, AE, AN, S, tol=1e-10, omega=1.8, precond="assor2", coupling="c
         hist = hist[: st.iterations + 1]
     return SolveResult(p[0] if squeeze else p, st.iterations, bool(st.converged), rc,
                        st.rel_residual, st.true_rel_residual, hist, cond_rel)
+
+
+def sr_restart_threshold(thresh: float) -> None:
+    """Test hook of the single-reduction restart branch (R-A32): restart when the alpha
+    denominator <= thresh * delta' (0 = the method itself)."""
+    lib().orc_sr_set_restart_threshold(float(thresh))
+
+
+def sr_restarts() -> int:
+    """Restarts taken by the last single-reduction solve."""
+    return int(lib().orc_sr_restarts())
 
 
 def pcg_async(AP, AE, AN, S, tol=1e-10, omega=1.8, precond="assor2", max_iter=100000):

@@ -209,10 +209,45 @@ static void assor1_apply(int32_t nt, int32_t ny, const double* AP, const double*
     }
 }
 
+/* SSOR (Eq. 2.9), applied EXACTLY by elimination -- the sequential triangular solves
+ * the paper rejects for the GPU, which is why it is oracle-only:
+ *   M = (D + w L) D^-1 (D + w L)^T / (w (2 - w))        (Eq. 2.9 at w = 1; Eq. 3.3 for w != 1)
+ *   z = M^-1 r:  (D + w L) y = r   (forward, natural order idx = i + nt*j, Eq. 3.8)
+ *                (D + w L^T) z' = D y   (backward),   z = w (2 - w) z'.
+ * L is the strictly lower triangle of A in the natural ordering: W (i >= 1), the E-wrap of
+ * column nt-1 and S (j >= 1); L^T holds E (i <= nt-2), the W-wrap of column 0 and N (R-A12). */
+static void ssor_apply(int32_t nt, int32_t ny, const double* AP, const double* AE, const double* AN,
+                       double omega, const double* r, double* z) {
+  const size_t n = (size_t)nt * ny;
+  double* y = (double*)malloc(n * sizeof(double));
+  for (int32_t j = 0; j < ny; ++j)                                   /* forward: (D + w L) y = r */
+    for (int32_t i = 0; i < nt; ++i) {
+      const size_t k = (size_t)j * nt + i;
+      double s = 0.0;
+      if (i >= 1) s += AE[k - 1] * y[k - 1];                         /* W */
+      if (i == nt - 1) s += AE[k] * y[(size_t)j * nt];               /* E-wrap: column 0 precedes */
+      if (j >= 1) s += AN[k - nt] * y[k - nt];                       /* S */
+      y[k] = (r[k] - omega * s) / AP[k];
+    }
+  for (int32_t j = ny - 1; j >= 0; --j)                              /* backward: (D + w L^T) z' = D y */
+    for (int32_t i = nt - 1; i >= 0; --i) {
+      const size_t k = (size_t)j * nt + i;
+      double s = 0.0;
+      if (i <= nt - 2) s += AE[k] * z[k + 1];                        /* E */
+      if (i == 0) s += AE[(size_t)j * nt + (nt - 1)] * z[(size_t)j * nt + (nt - 1)]; /* W-wrap */
+      if (j <= ny - 2) s += AN[k] * z[k + nt];                       /* N */
+      z[k] = (AP[k] * y[k] - omega * s) / AP[k];
+    }
+  const double c = omega * (2.0 - omega);
+  for (size_t k = 0; k < n; ++k) z[k] = c * z[k];
+  free(y);
+}
+
 void orc_precond_apply(int32_t nt, int32_t ny, const double* AP, const double* AE, const double* AN,
                        int32_t precond, double omega, const double* r, double* z) {
   const size_t n = (size_t)nt * ny;
   switch (precond) {
+    case ORC_PRECOND_SSOR: ssor_apply(nt, ny, AP, AE, AN, omega, r, z); break;
     case ORC_PRECOND_JACOBI: for (size_t k = 0; k < n; ++k) z[k] = r[k] / AP[k]; break;  /* Eq. 2.8 */
     case ORC_PRECOND_ASSOR2: assor2_apply(nt, ny, AP, AE, AN, omega, r, z); break;
     case ORC_PRECOND_ASSOR1: assor1_apply(nt, ny, AP, AE, AN, omega, r, z); break;
@@ -422,6 +457,17 @@ int orc_pcg_joint(int32_t nt, int32_t ny, int32_t K,
   return status;
 }
 
+/* Test hook for the restart branch of the single-reduction recurrence (R-A32): restart when
+ * den <= thresh * delta'.  thresh = 0 (the default) is the method itself (restart only when the
+ * denominator has lost its sign); thresh >= 1 restarts at EVERY iteration (den < delta' always,
+ * since beta gamma'/alpha > 0), which turns the recurrence into preconditioned steepest descent --
+ * the form tests/test_oracle_pcg.py pins it against.  The count of restarts taken by the last
+ * orc_pcg_joint_sr call is returned by orc_sr_restarts(). */
+static double g_sr_restart_thresh = 0.0;
+static int32_t g_sr_restarts = 0;
+void orc_sr_set_restart_threshold(double thresh) { g_sr_restart_thresh = thresh; }
+int32_t orc_sr_restarts(void) { return g_sr_restarts; }
+
 /* O7-S3: the same PCG (Table 1) written with a single global reduction per
  * iteration (Chronopoulos & Gear's reformulation; SURVEY 8(c) O7 "S3 mode",
  * 8(e)): the search direction pd and s = A pd are updated as in Table 1 steps
@@ -447,6 +493,7 @@ int orc_pcg_joint_sr(int32_t nt, int32_t ny, int32_t K,
   double* Sk = (double*)calloc((size_t)K, sizeof(double));
 #define BLK(ptr, k) ((ptr) + (size_t)(k) * n)
   if (!warm) memset(p, 0, N * sizeof(double));
+  g_sr_restarts = 0;
   double SS = 0.0, rr = 0.0;
   for (int32_t k = 0; k < K; ++k) {
     orc_spmv(nt, ny, BLK(AP, k), BLK(AE, k), BLK(AN, k), BLK(p, k), BLK(sv, k));
@@ -504,8 +551,8 @@ int orc_pcg_joint_sr(int32_t nt, int32_t ny, int32_t K,
       if (!(g2 > 0.0)) { status = ORC_E_BREAKDOWN; break; }
       beta = g2 / gam;
       const double den = d2 - beta * g2 / alpha;
-      if (den > 0.0) alpha = g2 / den;
-      else if (d2 > 0.0) { beta = 0.0; alpha = g2 / d2; }   /* restart along z (R-A32) */
+      if (den > g_sr_restart_thresh * d2) alpha = g2 / den;
+      else if (d2 > 0.0) { beta = 0.0; alpha = g2 / d2; ++g_sr_restarts; }   /* restart along z (R-A32) */
       else { status = ORC_E_BREAKDOWN; break; }
       gam = g2;
     } else {
@@ -515,8 +562,8 @@ int orc_pcg_joint_sr(int32_t nt, int32_t ny, int32_t K,
         if (g2 < 0.0) { status = ORC_E_BREAKDOWN; break; }
         bk[k] = g2 / gk[k];
         const double den = d2 - bk[k] * g2 / ak[k];
-        if (den > 0.0) ak[k] = (g2 == 0.0) ? 0.0 : g2 / den;
-        else if (d2 > 0.0) { bk[k] = 0.0; ak[k] = g2 / d2; }   /* restart along z (R-A32) */
+        if (den > g_sr_restart_thresh * d2) ak[k] = (g2 == 0.0) ? 0.0 : g2 / den;
+        else if (d2 > 0.0) { bk[k] = 0.0; ak[k] = g2 / d2; ++g_sr_restarts; }   /* restart along z (R-A32) */
         else { status = ORC_E_BREAKDOWN; break; }
         gk[k] = g2;
       }

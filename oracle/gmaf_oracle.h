@@ -3,7 +3,7 @@
  *
  * A plain, slow, single-threaded FP64 CPU oracle for the GMAF hot path
  * (arXiv 2511.06824): film thickness (Eq. 2.3), FVM assembly (Eqs. 2.4-2.7),
- * PCG (Table 1, sign fixed) with Jacobi (Eq. 2.8) / ASSOR-I (Eq. 3.2) /
+ * PCG (Table 1, sign fixed) with Jacobi (Eq. 2.8) / exact SSOR (Eq. 2.9) / ASSOR-I (Eq. 3.2) /
  * ASSOR-II (Eqs. 3.4-3.6) on the joint block-diagonal system (Eqs. 3.7-3.9),
  * a dense Cholesky reference, and the force/moment quadrature (Sec. 2.4-III).
  *
@@ -38,7 +38,8 @@ enum {
   ORC_E_NO_CONVERGENCE = -6       /* max_iter reached, best iterate kept */
 };
 
-enum { ORC_PRECOND_NONE = 0, ORC_PRECOND_JACOBI = 1, ORC_PRECOND_ASSOR2 = 2, ORC_PRECOND_ASSOR1 = 3 };
+enum { ORC_PRECOND_NONE = 0, ORC_PRECOND_JACOBI = 1, ORC_PRECOND_ASSOR2 = 2, ORC_PRECOND_ASSOR1 = 3,
+       ORC_PRECOND_SSOR = 4 /* exact SSOR, Eq. 2.9 (omega = 1) / Eq. 3.3 (omega != 1); oracle only */ };
 enum { ORC_COUPLED = 0, ORC_LOCKSTEP = 1 };
 
 typedef struct {
@@ -82,7 +83,8 @@ int  orc_assemble(const orc_grid* g, const orc_cond* c, double* AP, double* AE, 
 void orc_spmv(int32_t nt, int32_t ny, const double* AP, const double* AE, const double* AN,
               const double* x, double* y);
 
-/* z = M^{-1} r for one condition: precond NONE / JACOBI / ASSOR2 (two-step, O6) / ASSOR1. */
+/* z = M^{-1} r for one condition: precond NONE / JACOBI / ASSOR2 (two-step, O6) / ASSOR1 /
+ * SSOR (exact triangular solves, Eq. 2.9 at omega = 1). */
 void orc_precond_apply(int32_t nt, int32_t ny, const double* AP, const double* AE, const double* AN,
                        int32_t precond, double omega, const double* r, double* z);
 
@@ -117,6 +119,11 @@ int  orc_pcg_joint_sr(int32_t nt, int32_t ny, int32_t K,
                       const double* AP, const double* AE, const double* AN, const double* S,
                       double* p, double tol, double omega, int32_t precond, int32_t coupling,
                       int32_t max_iter, int32_t warm, orc_stats* st, double* history, double* cond_rel);
+
+/* Test hook of the R-A32 restart branch (see gmaf_oracle.c): restart when den <= thresh * delta'
+ * (default 0 = the method); orc_sr_restarts() = restarts taken by the last orc_pcg_joint_sr. */
+void orc_sr_set_restart_threshold(double thresh);
+int32_t orc_sr_restarts(void);
 
 /* Asynchronous strategy (Eq. 3.10, NEXT-2): per-block PCG, block frozen once
  * ||r_k||/||S_k|| <= tol.  iters_k (K) receives per-block iteration counts. */

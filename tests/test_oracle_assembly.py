@@ -158,3 +158,84 @@ def test_discrete_manufactured_solution(orc, gi):
     res = orc.pcg_joint(AP, AE, AN, S, tol=1e-12, precond="assor2", omega=1.6)
     assert res.converged
     assert np.linalg.norm(res.p - pstar) <= 1e-8 * np.linalg.norm(pstar)
+
+
+# ------------------------------------------------------ the source's motion terms
+def _source_mms(gi, orc, nt, ny):
+    """S of orc_assemble with ALL motion terms live (e, e-dot, U_theta, U_y non-zero) and
+    p_in = p_out = 0 (no Dirichlet folds), against the right-hand side of the Reynolds equation
+    (reading R-A1): S / (dx dy) = -[(U_theta/2) dh/dx + (U_y/2) dh/dy + dh/dt] with x = R_k theta,
+    h from Eq. 2.3 with e(t) = e + t e-dot, differentiated symbolically by sympy."""
+    import sympy as sp
+    th, y, t = sp.symbols("theta y t", real=True)
+    e0 = (1.2e-6, -0.7e-6, 0.9e-6, 1.5e-6)
+    ed = (3e-5, -2e-5, -4e-5, 1e-5)
+    g = gi.grid(nt, ny)
+    c = gi.condition().copy()
+    c[0:4], c[4:8] = e0, ed
+    c[9], c[10] = 0.37, 0.45          # U_theta, U_y
+    c[11] = c[12] = 0.0               # p_in = p_out = 0
+    L, Rk, Rc = c[8], g["R_k"], g["R_c"]
+    e = [e0[i] + ed[i] * t for i in range(4)]
+    a = Rc * sp.cos(th) - (e[2] - e[0]) / L * y - e[0]
+    b = Rc * sp.sin(th) - (e[3] - e[1]) / L * y - e[1]
+    h = sp.sqrt(a ** 2 + b ** 2) - Rk
+    rhs = (c[9] / 2) * sp.diff(h, th) / Rk + (c[10] / 2) * sp.diff(h, y) + sp.diff(h, t)
+    f = sp.lambdify((th, y), rhs.subs(t, 0), "numpy")
+    _, _, _, S = orc.assemble(g, c)
+    dth, dy = 2 * math.pi / nt, L / (ny + 1)
+    TH, Y = np.meshgrid(np.arange(nt) * dth, (np.arange(ny) + 1) * dy)
+    exact = -f(TH, Y)
+    return np.max(np.abs(S / ((Rk * dth) * dy) - exact)), np.max(np.abs(exact))
+
+
+def test_source_motion_terms_converge_to_the_reynolds_rhs(orc, gi):
+    """The wedge terms (central differences, R-A5) converge at O(h^2) to the symbolic
+    right-hand side and the squeeze term is exact: error ratio in [3.5, 4.5] over three
+    refinements, and small against the right-hand side.  A dropped term, a sign error or a
+    wrong factor in any of t1, t2, t3 (gmaf_oracle.c orc_assemble) leaves an O(1) error."""
+    errs = [_source_mms(gi, orc, nt, ny) for nt, ny in [(32, 15), (64, 31), (128, 63), (256, 127)]]
+    ratios = [errs[i][0] / errs[i + 1][0] for i in range(3)]
+    assert all(3.5 <= q <= 4.5 for q in ratios), (errs, ratios)
+    assert errs[-1][0] <= 2e-4 * errs[-1][1]
+
+
+def test_squeeze_film_sign_and_damping(orc, gi):
+    """Pure lateral translation e = 0, e-dot = (v, 0, v, 0), no sliding, p_in = p_out = 0:
+    h-dot = -v cos(theta) (a closing gap at theta = 0).  The squeeze film must push back: by the
+    maximum principle p = f(y) cos(theta) with f > 0, so sign(p) = sign(-h-dot) everywhere, and the
+    pressure force opposes the motion (F_x < 0, negative power)."""
+    g = gi.grid(64, 32)
+    v = 1e-4
+    c = gi.condition().copy()
+    c[0:4], c[4:8] = 0.0, (v, 0.0, v, 0.0)
+    c[9] = c[10] = 0.0
+    c[11] = c[12] = 0.0
+    AP, AE, AN, S = orc.assemble(g, c)
+    _, hd = orc.thickness(g, c)
+    p = orc.cholesky_solve(orc.expand_dense(AP, AE, AN), S.ravel()).reshape(32, 64)
+    hdi = hd[1:-1]
+    live = np.abs(hdi) > 0.05 * v
+    assert np.all(np.sign(p[live]) == np.sign(-hdi[live]))
+    assert p[16, 0] > 0 and p[16, 32] < 0
+    w = orc.wrench(g, c, p)
+    assert w[0] < 0 and abs(w[1]) <= 1e-9 * abs(w[0])
+
+
+def test_squeeze_damping_matrix_is_symmetric_negative_definite(orc, gi):
+    """J_e-dot (Eq. 2.14) from the 9-condition joint solve (Eq. 2.19): the
+    e-dot-perturbed conditions differ from the base ONLY through the squeeze term of S, so
+    J_e-dot = dF/d(e-dot) is the squeeze-film damping matrix.  The Reynolds operator is self-
+    adjoint and F is the virtual work conjugate to e (R-A28), so it must be symmetric
+    (reciprocity) and negative definite (dissipation) -- a sign or factor slip in the squeeze term
+    or in the generalized-force mapping breaks one of the two; and dF1/d(e-dot 1) < 0."""
+    import oracle.picard as OP
+    g = gi.grid(64, 32)
+    st = gi.condition()
+    res, W = orc.joint_step(g, gi.fd_conditions(st), tol=1e-12, omega=1.8)
+    assert res.converged
+    Fo = np.stack([OP.oil_force(W[k], st[8]) for k in range(9)])
+    _, Jv = OP.fd_jacobians(Fo, gi.DE, gi.DEDOT)
+    assert Jv[0, 0] < 0
+    assert np.max(np.abs(Jv - Jv.T)) <= 1e-8 * np.max(np.abs(Jv))
+    assert np.linalg.eigvalsh(0.5 * (Jv + Jv.T)).max() < 0

@@ -246,3 +246,120 @@ def test_single_reduction_schedule_equals_table1(orc, gi):
     for pc in ("jacobi", "none"):
         c = orc.pcg_joint(AP, AE, AN, S, tol=1e-10, omega=1.6, precond=pc, schedule="single")
         assert c.converged and np.linalg.norm(c.p - a.p) <= 1e-8 * np.linalg.norm(a.p)
+
+
+# ---------------------------------------------------------------- SSOR (Eq. 2.9), oracle only
+def test_ssor_apply_is_the_dense_eq_2_9_inverse(orc, gi):
+    """The oracle's SSOR (triangular solves) equals M^-1 r with M built densely from the
+    bands: M = (D + w L) D^-1 (D + w L)^T / (w (2 - w)) -- Eq. 2.9 at w = 1, Eq. 3.3 otherwise --
+    with D, L the diagonal and strict lower triangle of the dense A in the natural ordering
+    (Eq. 3.8; the periodic wraps fall where R-A12 puts them by construction)."""
+    g = gi.grid(16, 12, "short", tex_n_theta=4, tex_n_y=2, tex_band_rows=6)
+    AP, AE, AN, _ = orc.assemble(g, gi.random_conditions(3, 1)[0])
+    A = orc.expand_dense(AP, AE, AN)
+    D, L = np.diag(np.diag(A)), np.tril(A, -1)
+    rng = np.random.default_rng(7)
+    for w in (1.0, 1.5):
+        M = (D + w * L) @ np.linalg.inv(D) @ (D + w * L).T / (w * (2 - w))
+        for _ in range(3):
+            r = rng.standard_normal(AP.shape)
+            z = orc.precond_apply(AP, AE, AN, r, "ssor", w)
+            zr = np.linalg.solve(M, r.ravel())
+            assert np.linalg.norm(z.ravel() - zr) <= 1e-12 * np.linalg.norm(zr), w
+    # M^-1 is symmetric: <z(r1), r2> == <r1, z(r2)>
+    r1, r2 = rng.standard_normal(AP.shape), rng.standard_normal(AP.shape)
+    a = np.vdot(orc.precond_apply(AP, AE, AN, r1, "ssor", 1.0), r2)
+    b = np.vdot(r1, orc.precond_apply(AP, AE, AN, r2, "ssor", 1.0))
+    assert abs(a - b) <= 1e-12 * abs(a)
+
+
+def test_ssor_pcg_reaches_the_dense_solution(orc, c1):
+    cfg, (AP, AE, AN, S) = c1
+    x = orc.cholesky_solve(orc.expand_dense(AP[0], AE[0], AN[0]), S[0].ravel())
+    for w in (1.0, 1.8):
+        res = orc.pcg_joint(AP, AE, AN, S, tol=1e-10, omega=w, precond="ssor")
+        assert res.converged and np.linalg.norm(res.p[0].ravel() - x) <= 1e-8 * np.linalg.norm(x)
+
+
+def test_fig2a_preconditioner_ordering_with_ssor(orc, gi):
+    """Fig. 2(a) (smooth 2000x1600, rtol 1e-12, w = 1.8; Jacobi 6352, SSOR 6352,
+    ASSOR-I 6519, ASSOR-II 3738 iterations) at a mesh the oracle affords (smooth 200x160).
+    Reproduced: ASSOR-II needs the fewest of the parallel preconditioners and ASSOR-I about as
+    many as Jacobi.  NOT reproduced (reading R-A33): exact SSOR (Eq. 2.9, triangular solves) needs
+    about HALF of Jacobi's iterations here, not the same count -- the textbook behaviour of SSOR;
+    and exact SSOR at the same w beats its Neumann approximation ASSOR-II (Eq. 3.4 approximates
+    the inverse of Eq. 3.3's M)."""
+    g = gi.grid(200, 160)
+    AP, AE, AN, S = orc.assemble(g, gi.condition())
+    it = {}
+    for name, pc, w in (("jacobi", "jacobi", 1.8), ("ssor", "ssor", 1.0), ("ssor_w", "ssor", 1.8),
+                        ("assor1", "assor1", 1.8), ("assor2", "assor2", 1.8)):
+        res = orc.pcg_joint(AP, AE, AN, S, tol=1e-12, omega=w, precond=pc)
+        assert res.converged
+        it[name] = res.iterations
+    assert it["assor2"] < it["jacobi"] and it["assor2"] < it["assor1"]
+    assert 0.95 <= it["assor1"] / it["jacobi"] <= 1.2          # paper 6519 / 6352 = 1.03
+    assert it["assor2"] / it["jacobi"] <= 0.7                   # paper 0.59
+    assert it["ssor"] <= 0.6 * it["jacobi"]                     # R-A33 (paper: equal)
+    assert it["ssor_w"] <= it["assor2"]
+
+
+# ------------------------------------------------- the R-A32 restart of the single-reduction PCG
+def _psd(A, Minv, b, n_it):
+    """Preconditioned steepest descent written out: x += a z, a = (r.z)/(z.Az), z = M^-1 r."""
+    x = np.zeros_like(b)
+    r = b.copy()
+    out = []
+    for _ in range(n_it):
+        z = Minv @ r
+        a = (r @ z) / (z @ (A @ z))
+        x = x + a * z
+        r = r - a * (A @ z)
+        out.append(x.copy())
+    return out
+
+
+@pytest.mark.parametrize("coupling", ["coupled", "lockstep"])
+def test_restart_branch_is_preconditioned_steepest_descent(orc, gi, coupling):
+    """R-A32: on a non-positive Chronopoulos-Gear denominator the single-reduction PCG restarts
+    along z (beta = 0, alpha = gamma'/delta').  Forcing that branch at EVERY iteration (the
+    oracle's test hook, threshold 2) must reproduce preconditioned steepest descent -- written
+    out here densely with the dense Eq. 3.4 inverse -- iterate by iterate; coupled = one descent
+    on the joint system, lockstep = one per condition."""
+    g = gi.grid(12, 8, "smooth")
+    conds = gi.random_conditions(21, 2)
+    AP, AE, AN, S = orc.assemble_joint(g, conds)
+    n = 12 * 8
+    A = np.zeros((2 * n, 2 * n))
+    Minv = np.zeros((2 * n, 2 * n))
+    for k in range(2):
+        A[k * n:(k + 1) * n, k * n:(k + 1) * n] = orc.expand_dense(AP[k], AE[k], AN[k])
+        Minv[k * n:(k + 1) * n, k * n:(k + 1) * n] = orc.assor2_dense(AP[k], AE[k], AN[k], 1.6)
+    b = S.ravel()
+    if coupling == "coupled":
+        ref = _psd(A, Minv, b, 6)
+    else:
+        parts = [_psd(A[k * n:(k + 1) * n, k * n:(k + 1) * n], Minv[k * n:(k + 1) * n, k * n:(k + 1) * n],
+                      b[k * n:(k + 1) * n], 6) for k in range(2)]
+        ref = [np.concatenate([parts[0][j], parts[1][j]]) for j in range(6)]
+    try:
+        orc.sr_restart_threshold(2.0)
+        for j in (1, 2, 4, 6):
+            res = orc.pcg_joint(AP, AE, AN, S, tol=1e-30, omega=1.6, coupling=coupling, max_iter=j,
+                                schedule="single")
+            assert res.iterations == j
+            # iteration 1 uses the initial alpha (no recurrence); the scalars computed after each
+            # of the j iterations all take the restart branch (once per condition in lockstep)
+            assert orc.sr_restarts() == j * (1 if coupling == "coupled" else 2)
+            err = np.linalg.norm(res.p.ravel() - ref[j - 1]) / np.linalg.norm(ref[j - 1])
+            assert err <= 1e-11, (j, err)
+        # and the restarted iteration still converges to the direct solution
+        res = orc.pcg_joint(AP, AE, AN, S, tol=1e-10, omega=1.6, coupling=coupling, max_iter=20000,
+                            schedule="single")
+        x = np.linalg.solve(A, b)
+        assert res.converged and np.linalg.norm(res.p.ravel() - x) <= 1e-8 * np.linalg.norm(x)
+    finally:
+        orc.sr_restart_threshold(0.0)
+    # the method itself (threshold 0) never restarts on this well-conditioned case
+    res = orc.pcg_joint(AP, AE, AN, S, tol=1e-10, omega=1.6, coupling=coupling, schedule="single")
+    assert res.converged and orc.sr_restarts() == 0

@@ -112,49 +112,112 @@ def _dist():
     return world, rank, local
 
 
-def cpu_baseline(cfg, iters: int = 10):
-    """The oracle as it stands (single-threaded C, one core), on a bounded sample of the
-    same workload: assembly of all K conditions + `iters` PCG-ASSOR iterations."""
+def _host_info() -> dict:
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def _full_step_iterations(cfg) -> int | None:
+    """PCG iterations of one full step of this workload as the ORACLE counts them (its own Table-1
+    solve, tests/golden/<cfg>_oracle_samples.json, written by scripts/oracle_c3_reference.py)."""
+    path = os.path.join(ROOT, "tests", "golden", f"{cfg.name.lower()}_oracle_samples.json")
+    try:
+        with open(path) as f:
+            return int(json.load(f)["iterations"])
+    except Exception:
+        return None
+
+
+def _oracle_sample(cfg, iters: int):
+    """Time the oracle as it stands, pinned to ONE host core (sched_setaffinity = taskset -c 0;
+    the oracle is single-threaded): assembly of all K conditions, `iters` PCG-ASSOR iterations,
+    the K wrench quadratures."""
     import oracle
-    t0 = time.perf_counter()
-    AP, AE, AN, S = oracle.assemble_joint(cfg.grid, cfg.conds)
-    t1 = time.perf_counter()
-    res = oracle.pcg_joint(AP, AE, AN, S, tol=0.0, omega=cfg.omega, max_iter=iters)
-    t2 = time.perf_counter()
+    oracle.build()
+    old = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
+    pinned = False
+    try:
+        if old is not None:
+            os.sched_setaffinity(0, {min(old)})
+            pinned = True
+        t0 = time.perf_counter()
+        AP, AE, AN, S = oracle.assemble_joint(cfg.grid, cfg.conds)
+        t1 = time.perf_counter()
+        res = oracle.pcg_joint(AP, AE, AN, S, tol=0.0, omega=cfg.omega, max_iter=iters)
+        t2 = time.perf_counter()
+        for k in range(cfg.K):
+            oracle.wrench(cfg.grid, cfg.conds[k], res.p[k])
+        t3 = time.perf_counter()
+    finally:
+        if old is not None:
+            os.sched_setaffinity(0, old)
+    return {"assembly_s": t1 - t0, "iter_s": (t2 - t1) / max(res.iterations, 1), "quadrature_s": t3 - t2,
+            "iterations": res.iterations, "core": min(old) if pinned else None}
+
+
+def _full_step_rate(cfg, smp) -> tuple[float, float, int | None]:
+    """(full-step rate, per-iteration rate, I): the oracle's rate for the SAME workload the GPU arm
+    times -- a full step with I PCG iterations (the oracle's own count) -- from the timed pieces:
+    K n I / (t_assembly + t_quadrature + I t_iteration); the per-iteration rate beside it."""
     n = cfg.grid["n_theta"] * cfg.grid["n_y"]
-    value = cfg.K * n * res.iterations / (t2 - t1)
+    it_rate = cfg.K * n / smp["iter_s"]
+    I = _full_step_iterations(cfg)
+    if I is None:
+        return it_rate, it_rate, None
+    return cfg.K * n * I / (smp["assembly_s"] + smp["quadrature_s"] + I * smp["iter_s"]), it_rate, I
+
+
+def cpu_baseline(cfg, iters: int = 10):
+    """The oracle as it stands (single-threaded C, one core), on a bounded sample of the same
+    workload: assembly of all K conditions + `iters` PCG-ASSOR iterations + the quadrature."""
+    smp = _oracle_sample(cfg, iters)
+    value, it_rate, I = _full_step_rate(cfg, smp)
     return {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{cfg.name}: oracle assembly of K={cfg.K} ({t1 - t0:.2f} s) + "
-                      f"{res.iterations} PCG-ASSOR iterations ({t2 - t1:.2f} s) on 1 host core",
-            "assembly_s": t1 - t0, "iter_s": (t2 - t1) / max(res.iterations, 1)}
+            "sample": f"{cfg.name}: oracle on 1 host core (affinity core {smp['core']}, like taskset -c "
+                      f"{smp['core']}): assembly of K={cfg.K} ({smp['assembly_s']:.2f} s) + {smp['iterations']} "
+                      f"PCG-ASSOR iterations ({smp['iter_s'] * smp['iterations']:.2f} s) + K quadratures "
+                      f"({smp['quadrature_s']:.2f} s); value = the full step of {I} iterations (the oracle's own "
+                      f"count, tests/golden) from these pieces",
+            "per_iteration_rate": it_rate, "full_step_iterations": I,
+            "assembly_s": smp["assembly_s"], "iter_s": smp["iter_s"], "quadrature_s": smp["quadrature_s"],
+            **_host_info()}
 
 
 def run_reference(args, cfg):
     world, rank, _ = _dist()
     if rank != 0:
         return 0
-    import oracle
-    oracle.build()
     iters = args.ref_iters
-    n = cfg.grid["n_theta"] * cfg.grid["n_y"]
-    times = []
+    vals, its, steps_s = [], [], []
+    last = None
     for s in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        AP, AE, AN, S = oracle.assemble_joint(cfg.grid, cfg.conds)
-        res = oracle.pcg_joint(AP, AE, AN, S, tol=0.0, omega=cfg.omega, max_iter=iters)
-        W = [oracle.wrench(cfg.grid, cfg.conds[k], res.p[k]) for k in range(cfg.K)]
-        t1 = time.perf_counter()
+        smp = _oracle_sample(cfg, iters)
         if s >= args.warmup:
-            times.append(t1 - t0)
-    tot = sum(times)
-    value = cfg.K * n * iters * len(times) / tot
-    sample = (f"{cfg.name}: per step the oracle assembles K={cfg.K}, runs {iters} PCG-ASSOR "
-              f"iterations and integrates K wrenches, single-threaded on 1 host core")
+            v, itr, I = _full_step_rate(cfg, smp)
+            vals.append(v)
+            its.append(itr)
+            steps_s.append(smp["assembly_s"] + smp["quadrature_s"] + (I or iters) * smp["iter_s"])
+            last = (smp, I)
+    value = len(vals) / sum(1.0 / v for v in vals)          # the rate of the summed (equal-work) steps
+    smp, I = last
+    how = (f"value = the full step of {I} iterations (the oracle's own count, tests/golden) from the timed pieces"
+           if I else "value = the per-iteration rate of the sample (no oracle full-step count for this config)")
+    sample = (f"{cfg.name}: per step the oracle (1 host core, affinity core {smp['core']}) assembles K={cfg.K}, "
+              f"runs {iters} PCG-ASSOR iterations and integrates K wrenches; {how}")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(steps_s) / len(steps_s),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": _config_obj(cfg, args),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                             "per_iteration_rate": statistics.mean(its), "full_step_iterations": I,
+                             **_host_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -287,7 +350,9 @@ def run_gmaf(args, cfg):
         conds = conds_all
     else:
         conds = cfg.conds
-        S = P.JointSolver(cfg.grid, K, device=local)
+        # the FD conditions of Eqs. 2.17-2.19 need 5 distinct coefficient sets per 9 (Eq. 2.3 has
+        # no e-dot): the band storage is sized for exactly that
+        S = P.JointSolver(cfg.grid, K, device=local, max_matrices=5 * (K // 9) if K % 9 == 0 else None)
     stream = S.stream
 
     def one_step():

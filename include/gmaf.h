@@ -139,8 +139,14 @@ typedef struct {
 typedef struct gmaf_ctx gmaf_ctx;
 
 /* Device workspace bytes needed for this grid, K conditions and distribution.
- * Returns 0 on invalid arguments. */
+ * Returns 0 on invalid arguments.  The coefficient bands are stored once per DISTINCT matrix
+ * (conditions with bitwise-equal e and L_F share one: Eq. 2.3 has no e-dot, so the 9
+ * conditions of Eqs. 2.17-2.19 need 5): gmaf_workspace_bytes sizes them for K, the worst case;
+ * gmaf_workspace_bytes_m for at most max_matrices (<= 0 or > K: K).  gmaf_create derives the
+ * capacity from ws_bytes, and gmaf_thickness fails with GMAF_E_WORKSPACE if the conditions need
+ * more distinct sets than that. */
 size_t gmaf_workspace_bytes(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist);
+size_t gmaf_workspace_bytes_m(const gmaf_grid* grid, int32_t K, int32_t max_matrices, const gmaf_dist* dist);
 
 /* Create a context.  d_workspace: device pointer (256-byte aligned) of ws_bytes >=
  * gmaf_workspace_bytes(); cuda_stream: a cudaStream_t (NULL = legacy default stream).
@@ -296,6 +302,17 @@ gmaf_status gmaf_slab(const gmaf_ctx* ctx, int32_t* y0, int32_t* y1);
  * 0..world-1, or a slab thinner than 8 rows). */
 gmaf_status gmaf_slab_rows(int32_t n_y, int32_t world, int32_t rank, int32_t* y0, int32_t* y1,
                            int32_t* yb, int32_t* ye);
+
+/* Launch configuration of this context's iteration kernel, for tests and
+ * the benchmark: strip width tw (output columns per CTA), rows per chunk th, strips and chunks
+ * per condition, CTAs per launch (n_strips * n_chunks * K_local), the schedule that solves use
+ * (GMAF_SCHEDULE_*) and whether the single-pass solve runs as ONE persistent launch (1: all
+ * iterations in one cooperative kernel with a grid barrier per iteration; 0: one kernel per
+ * iteration inside the CUDA graph's WHILE loop).  Errors: INVALID_ARG (null pointer). */
+typedef struct {
+  int32_t tw, th, n_strips, n_chunks, n_ctas, schedule, persistent, pad;
+} gmaf_tiles;
+gmaf_status gmaf_tile_config(const gmaf_ctx* ctx, gmaf_tiles* out);
 
 /* Make a new ncclUniqueId (128 bytes) into out (NCCL is loaded at run time).  Errors: NCCL. */
 gmaf_status gmaf_nccl_unique_id(void* out);

@@ -19,7 +19,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("GMAF_LIB") or os.path.join(_HERE, "libgmaf.so")   # GMAF_LIB: A/B builds only
+LIB_PATH = os.path.join(_HERE, "libgmaf.so")   # the in-tree product library, nothing else
 
 STATUS = {0: "OK", -1: "INVALID_ARG", -2: "INVALID_MESH", -3: "MESH_TOO_COARSE",
           -4: "NONPOSITIVE_THICKNESS", -5: "BREAKDOWN", -6: "NO_CONVERGENCE", -7: "STATE",
@@ -59,6 +59,11 @@ class gmaf_kernel_timing(C.Structure):
                 ("bytes_per_launch", C.c_double)]
 
 
+class gmaf_tiles(C.Structure):
+    _fields_ = [("tw", C.c_int32), ("th", C.c_int32), ("n_strips", C.c_int32), ("n_chunks", C.c_int32),
+                ("n_ctas", C.c_int32), ("schedule", C.c_int32), ("persistent", C.c_int32), ("pad", C.c_int32)]
+
+
 class gmaf_pump(C.Structure):
     _fields_ = [("m_k", C.c_double), ("m_G", C.c_double), ("R_b", C.c_double), ("beta", C.c_double),
                 ("omega_s", C.c_double), ("R_k", C.c_double)]
@@ -95,6 +100,8 @@ def lib() -> C.CDLL:
         P = C.c_void_p
         L.gmaf_workspace_bytes.restype = C.c_size_t
         L.gmaf_workspace_bytes.argtypes = [C.POINTER(gmaf_grid), C.c_int32, C.POINTER(gmaf_dist)]
+        L.gmaf_workspace_bytes_m.restype = C.c_size_t
+        L.gmaf_workspace_bytes_m.argtypes = [C.POINTER(gmaf_grid), C.c_int32, C.c_int32, C.POINTER(gmaf_dist)]
         L.gmaf_create.argtypes = [C.POINTER(gmaf_grid), C.c_int32, C.POINTER(gmaf_dist), P, C.c_size_t, P,
                                   C.POINTER(P)]
         L.gmaf_destroy.argtypes = [P]
@@ -124,6 +131,7 @@ def lib() -> C.CDLL:
         L.gmaf_p2p_handle.argtypes = [P, P]
         L.gmaf_p2p_connect.argtypes = [P, P]
         L.gmaf_slab.argtypes = [P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+        L.gmaf_tile_config.argtypes = [P, C.POINTER(gmaf_tiles)]
         L.gmaf_slab_rows.argtypes = [C.c_int32, C.c_int32, C.c_int32] + [C.POINTER(C.c_int32)] * 4
         L.gmaf_last_error.restype = C.c_char_p
         L.gmaf_last_error.argtypes = [P]
@@ -133,17 +141,17 @@ def lib() -> C.CDLL:
                      "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_set_schedule",
                      "gmaf_nccl_unique_id", "gmaf_cond_iterations", "gmaf_general_forces",
                      "gmaf_picard_iteration", "gmaf_picard_step", "gmaf_p2p_handle", "gmaf_p2p_connect",
-                     "gmaf_slab", "gmaf_slab_rows"):
+                     "gmaf_slab", "gmaf_slab_rows", "gmaf_tile_config"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
 
 
-ABI_SYMBOLS = ("gmaf_workspace_bytes", "gmaf_create", "gmaf_destroy", "gmaf_thickness", "gmaf_assemble",
+ABI_SYMBOLS = ("gmaf_workspace_bytes", "gmaf_workspace_bytes_m", "gmaf_create", "gmaf_destroy", "gmaf_thickness", "gmaf_assemble",
                "gmaf_solve", "gmaf_solve_fixed", "gmaf_integrate", "gmaf_get", "gmaf_field_ptr",
                "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_set_schedule", "gmaf_nccl_unique_id",
                "gmaf_cond_iterations", "gmaf_general_forces", "gmaf_picard_iteration", "gmaf_picard_step",
-               "gmaf_p2p_handle", "gmaf_p2p_connect", "gmaf_slab", "gmaf_slab_rows",
+               "gmaf_p2p_handle", "gmaf_p2p_connect", "gmaf_slab", "gmaf_slab_rows", "gmaf_tile_config",
                "gmaf_last_error", "gmaf_version")
 SCHEDULE = {"table1": 0, "single": 1}
 
@@ -186,7 +194,7 @@ def general_forces(pump: dict, cond, phi: float, wrench12=None):
 
 def _check(ctx, code: int):
     if code != 0:
-        msg = lib().gmaf_last_error(ctx).decode() if ctx else ""
+        msg = lib().gmaf_last_error(ctx).decode()   # NULL ctx: the last failed create
         raise GmafError(code, msg)
 
 
@@ -220,6 +228,11 @@ def gmaf_slab_rows(n_y: int, world: int, rank: int) -> tuple[int, int, int, int]
 
 def gmaf_workspace_bytes(grid: gmaf_grid, K: int, dist: gmaf_dist | None = None) -> int:
     return int(lib().gmaf_workspace_bytes(C.byref(grid), int(K), C.byref(dist) if dist else None))
+
+
+def gmaf_workspace_bytes_m(grid: gmaf_grid, K: int, max_matrices: int, dist: gmaf_dist | None = None) -> int:
+    return int(lib().gmaf_workspace_bytes_m(C.byref(grid), int(K), int(max_matrices),
+                                            C.byref(dist) if dist else None))
 
 
 def gmaf_create(grid: gmaf_grid, K: int, d_workspace: int, ws_bytes: int, stream: int,
@@ -272,7 +285,8 @@ class JointSolver:
     """One context: K working conditions on one mesh (Eq. 3.7 joint system)."""
 
     def __init__(self, grid: dict, K: int, device: int | str = 0, stream=None, rank: int = 0,
-                 world: int = 1, nccl_uid: bytes | None = None, p2p: bool = False, shard: str = "conditions"):
+                 world: int = 1, nccl_uid: bytes | None = None, p2p: bool = False, shard: str = "conditions",
+                 max_matrices: int | None = None):
         """K = total conditions.  With nccl_uid the K conditions are sharded over `world` ranks
         (condition sharding with one NCCL allgather per iteration, include/gmaf.h gmaf_dist); with
         p2p=True they are sharded peer to peer (the gathers fused into the iteration kernel over
@@ -294,7 +308,10 @@ class JointSolver:
         self.shard = shard
         self.dist, self._uid_buf = make_dist(rank, world, nccl_uid, p2p=p2p and world >= 1, shard=shard)
         self.rank, self.world = int(rank), int(world)
-        nbytes = gmaf_workspace_bytes(self.grid, self.K, self.dist)
+        # max_matrices: distinct coefficient sets to store (the 9 FD conditions of one state need 5;
+        # None = K, the worst case)
+        nbytes = (gmaf_workspace_bytes(self.grid, self.K, self.dist) if max_matrices is None else
+                  gmaf_workspace_bytes_m(self.grid, self.K, int(max_matrices), self.dist))
         if nbytes == 0:
             raise GmafError(-1, "invalid grid for workspace sizing")
         with torch.cuda.device(self.device):
@@ -355,6 +372,13 @@ class JointSolver:
                                                  C.byref(st)))
         return SolveStats(_SCHED_NAME[st.schedule], st.iterations, bool(st.converged), st.status,
                           st.rel_residual, st.true_rel_residual, st.solve_ms, np.zeros(self.K))
+
+    def tile_config(self) -> dict:
+        """Launch configuration of the iteration kernel (include/gmaf.h gmaf_tile_config)."""
+        t = gmaf_tiles()
+        _check(self.ctx, lib().gmaf_tile_config(self.ctx, C.byref(t)))
+        return {"tw": t.tw, "th": t.th, "n_strips": t.n_strips, "n_chunks": t.n_chunks, "n_ctas": t.n_ctas,
+                "schedule": _SCHED_NAME[t.schedule], "persistent": bool(t.persistent)}
 
     def cond_iterations(self) -> np.ndarray:
         """Per-condition iteration counts of the last solve (the freeze iteration under 'async')."""

@@ -24,6 +24,9 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-fast-math",
           "-I" + os.path.join(ROOT, "include"), "-Xptxas", "-v"]
 UNITS = [("geometry.cu", ["--fmad=false"]), ("pcg.cu", []), ("sr.cu", []), ("gmaf_api.cu", []), ("picard.cu", [])]
+# GMAF_NVCC_EXTRA: extra nvcc flags for timing-only experiments (e.g. -DGMAF_EXPERIMENT_NOBAR);
+# never set for the product build
+EXTRA = os.environ.get("GMAF_NVCC_EXTRA", "").split()
 
 
 def _deps():
@@ -40,7 +43,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     for src, extra in UNITS:
         obj = os.path.join(BUILD, src.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *COMMON, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *ARCH, *COMMON, *extra, *EXTRA, "-c", os.path.join(CSRC, src), "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         log = os.path.join(BUILD, src + ".log")
         with open(log, "w") as f:

@@ -6,6 +6,29 @@
 
 namespace gmaf {
 
+// the device's opt-in maximum of dynamic shared memory per block (host)
+inline int smem_optin_max() {
+  static int v = -1;
+  if (v < 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+      v = 0;
+  }
+  return v;
+}
+
+// Raise a kernel's dynamic shared-memory cap to the device's opt-in maximum minus its static
+// shared memory (their sum may not exceed the opt-in limit).
+template <typename KernelT>
+inline cudaError_t raise_smem_cap(KernelT kern) {
+  cudaFuncAttributes a;
+  cudaError_t e = cudaFuncGetAttributes(&a, kern);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              smem_optin_max() - (int)a.sharedSizeBytes);
+}
+
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

@@ -167,15 +167,18 @@ int check_grid(const gmaf_grid* g) {
   return GMAF_OK;
 }
 
-Layout make_layout(const gmaf_grid* g, int K, int world = 0, int kmax = 0, int rows_stored = 0) {
+// Mcap = distinct coefficient sets the bands hold (<= K; conditions with equal (e, L_F) share
+// one, Eq. 2.3 has no e-dot: the 9 FD conditions of one state need 5).  The bands come LAST so
+// that gmaf_create can read Mcap back from the workspace size.
+Layout make_layout(const gmaf_grid* g, int K, int world = 0, int kmax = 0, int rows_stored = 0, int Mcap = 0) {
   Layout L{};
+  if (Mcap <= 0 || Mcap > K) Mcap = K;
   const size_t nt = (size_t)g->n_theta, ny = (size_t)g->n_y;
   const size_t n = nt * (size_t)(rows_stored > 0 ? rows_stored : g->n_y);   // per-condition field
   size_t o = 0;
   auto take = [&](size_t bytes) { size_t at = o; o = align_up(o + bytes); return at; };
   L.off_ct = take(nt * 8); L.off_st = take(nt * 8); L.off_cth = take(nt * 8); L.off_sth = take(nt * 8);
   L.off_cp = take((size_t)K * sizeof(CondParams));
-  L.off_AP = take((size_t)K * n * 8); L.off_AE = take((size_t)K * n * 8); L.off_AN = take((size_t)K * n * 8);
   L.off_S = take((size_t)K * n * 8); L.off_p = take((size_t)K * n * 8);
   L.off_r = take((size_t)K * n * 8); L.off_r2 = take((size_t)K * n * 8);
   L.off_u = take((size_t)K * n * 8); L.off_u2 = take((size_t)K * n * 8);
@@ -193,6 +196,7 @@ Layout make_layout(const gmaf_grid* g, int K, int world = 0, int kmax = 0, int r
   L.off_timing = take(sizeof(Timing));
   L.off_guard = take(4 * sizeof(unsigned long long));
   L.off_matrep = take((size_t)K * sizeof(int32_t));
+  L.off_AP = take((size_t)Mcap * n * 8); L.off_AE = take((size_t)Mcap * n * 8); L.off_AN = take((size_t)Mcap * n * 8);
   L.total = o;
   return L;
 }
@@ -214,6 +218,7 @@ struct gmaf_ctx {
   int schedule = GMAF_SCHEDULE_SINGLE;
   DevPtrs d{};
   int M = 0;
+  int Mcap = 0;          // distinct coefficient sets the band storage holds (<= K)
   std::vector<int32_t> mat_of, mat_rep;
   int state = ST_CREATED;
   std::string err;
@@ -231,6 +236,7 @@ struct gmaf_ctx {
   int last_coupling = 0;
   bool stream_mode = false;  // GMAF_LAUNCH_MODE=stream: no CUDA graph (for ncu)
   bool sr_k_ok = true;       // K fits the single-pass kernel's reduction scratch
+  bool persist_ok = false;   // the single-pass solve runs as one persistent launch (sr.cu k_srp)
   // multi-rank (condition sharding): this rank owns global conditions [kofs, kofs + K)
   bool distm = false;
   int world = 1, rank = 0, kofs = 0, Kglob = 0, kmax = 0;
@@ -248,6 +254,8 @@ struct gmaf_ctx {
 };
 
 namespace {
+
+thread_local std::string g_create_err;   // reason of the last failed gmaf_create on this thread
 
 gmaf_status fail(gmaf_ctx* c, gmaf_status code, const char* fmt, ...) {
   if (c) {
@@ -356,11 +364,38 @@ cudaError_t enqueue_final(gmaf_ctx* ctx, const GraphKey& key, cudaStream_t s) {
   return launch_true_scalar(ctx->d, ctx->world, s);
 }
 
+bool use_persistent(const gmaf_ctx* ctx, const GraphKey& key) {
+  return ctx->persist_ok && key.schedule == GMAF_SCHEDULE_SINGLE && !ctx->distm;
+}
+
+// Persistent solve: init -> ONE launch that runs every iteration (grid barrier per iteration,
+// no WHILE node) -> fix-up -> true residual.
+cudaError_t enqueue_persistent(gmaf_ctx* ctx, const GraphKey& key, cudaStream_t s) {
+  cudaError_t e = enqueue_init(ctx, key, 0ull, s);
+  if (e == cudaSuccess) e = launch_sr_persistent(ctx->gp, ctx->d, ctx->tiles_sr, ctx->K, key.precond, s);
+  if (e == cudaSuccess) e = enqueue_final(ctx, key, s);
+  return e;
+}
+
 gmaf_status build_graph(gmaf_ctx* ctx, const GraphKey& key, cudaGraphExec_t* out) {
   auto it = ctx->graphs.find(key);
   if (it != ctx->graphs.end()) { *out = it->second.second; return GMAF_OK; }
   cudaGraph_t graph = nullptr;
   CU(cudaGraphCreate(&graph, 0));
+  if (use_persistent(ctx, key)) {
+    cudaStream_t cs = ctx->cap_stream;
+    CU(cudaStreamBeginCaptureToGraph(cs, graph, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    cudaError_t le = enqueue_persistent(ctx, key, cs);
+    cudaGraph_t g2 = nullptr;
+    cudaError_t ee = cudaStreamEndCapture(cs, &g2);
+    CU(le);
+    CU(ee);
+    cudaGraphExec_t exec = nullptr;
+    CU(cudaGraphInstantiate(&exec, graph, 0));
+    ctx->graphs[key] = {graph, exec};
+    *out = exec;
+    return GMAF_OK;
+  }
   cudaGraphConditionalHandle handle;
   CU(cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
   cudaStream_t cs = ctx->cap_stream;
@@ -506,6 +541,10 @@ gmaf_status run_solve(gmaf_ctx* ctx, double tol, double omega, int precond, int 
     // Plain stream launches (profilers cannot replay kernel nodes of conditional graphs):
     // the host polls the device done-flag every kUnroll iterations.
     CU(cudaEventRecord(ctx->ev0, ctx->stream));
+    if (use_persistent(ctx, key)) {
+      CU(enqueue_persistent(ctx, key, ctx->stream));
+      CU(cudaEventRecord(ctx->ev1, ctx->stream));
+    } else {
     CU(enqueue_init(ctx, key, 0ull, ctx->stream));
     for (;;) {
       CU(cudaMemcpyAsync(hs, ctx->d.st_, sizeof(SolverState), cudaMemcpyDeviceToHost, ctx->stream));
@@ -515,6 +554,7 @@ gmaf_status run_solve(gmaf_ctx* ctx, double tol, double omega, int precond, int 
     }
     CU(enqueue_final(ctx, key, ctx->stream));
     CU(cudaEventRecord(ctx->ev1, ctx->stream));
+    }
   } else {
     cudaGraphExec_t exec = nullptr;
     gmaf_status gs = build_graph(ctx, key, &exec);
@@ -581,21 +621,25 @@ extern "C" {
 
 const char* gmaf_version(void) { return "gmaf-b200 0.1 (sm_100a)"; }
 
-size_t gmaf_workspace_bytes(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist) {
+size_t gmaf_workspace_bytes_m(const gmaf_grid* grid, int32_t K, int32_t max_matrices, const gmaf_dist* dist) {
   if (check_grid(grid) != GMAF_OK || K < 1) return 0;
   if (dist && (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)) return 0;
   if (rows_mode(dist)) {
     if (dist->world > kMaxP2P || grid->n_y < 2 * SLAB_HALO * dist->world) return 0;
     const Slab sl = slab_of(grid->n_y, dist->world, dist->rank);
-    return make_layout(grid, K, dist->world, K, sl.ye - sl.yb).total;
+    return make_layout(grid, K, dist->world, K, sl.ye - sl.yb, max_matrices).total;
   }
   if (dist_mode(dist)) {
     if (dist->world > K) return 0;
     int lo, hi;
     shard(K, dist->world, dist->rank, &lo, &hi);
-    return make_layout(grid, hi - lo, dist->world, (K + dist->world - 1) / dist->world).total;
+    return make_layout(grid, hi - lo, dist->world, (K + dist->world - 1) / dist->world, 0, max_matrices).total;
   }
-  return make_layout(grid, K).total;
+  return make_layout(grid, K, 0, 0, 0, max_matrices).total;
+}
+
+size_t gmaf_workspace_bytes(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist) {
+  return gmaf_workspace_bytes_m(grid, K, 0, dist);
 }
 
 gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist, void* d_workspace,
@@ -634,8 +678,14 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
   // multi-rank contexts run the single-pass kernel, whose reduction scratch (the dead rings,
   // 48 (tw + 8) doubles) must hold the 4 K per-condition sums
   if (dm && 4 * K > 48 * (tw_single(grid->n_theta) + 2 * SR_HALO_COLS)) return GMAF_E_INVALID_ARG;
-  const Layout L = rm ? make_layout(grid, K, world, kmax, sl.ye - sl.yb)
-                 : dm ? make_layout(grid, K, world, kmax) : make_layout(grid, K);
+  // the band storage the caller's workspace holds: the most distinct coefficient sets that fit
+  auto layout_m = [&](int Mc) {
+    return rm ? make_layout(grid, K, world, kmax, sl.ye - sl.yb, Mc)
+         : dm ? make_layout(grid, K, world, kmax, 0, Mc) : make_layout(grid, K, 0, 0, 0, Mc);
+  };
+  int Mcap = K;
+  while (Mcap > 1 && layout_m(Mcap).total > ws_bytes) --Mcap;
+  const Layout L = layout_m(Mcap);
   if (!d_workspace || ws_bytes < L.total || (reinterpret_cast<uintptr_t>(d_workspace) % kAlign) != 0)
     return GMAF_E_WORKSPACE;
   gmaf_ctx* ctx = new (std::nothrow) gmaf_ctx();
@@ -654,6 +704,7 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
   ctx->ws = reinterpret_cast<char*>(d_workspace);
   ctx->ws_bytes = ws_bytes;
   ctx->L = L;
+  ctx->Mcap = Mcap;
   GridParams& gp = ctx->gp;
   gp.nt = grid->n_theta; gp.ny = grid->n_y; gp.Rk = grid->R_k; gp.Rc = grid->R_c; gp.mu = grid->mu;
   gp.hmin = grid->h_min;
@@ -693,7 +744,14 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
   d.dist.packed_local = at<double>(ctx, L.off_plocal);
   d.dist.packed_all = at<double>(ctx, L.off_pall);
 
-  auto cleanup_fail = [&](gmaf_status s) { gmaf_destroy(ctx); return s; };
+  auto cleanup_fail = [&](gmaf_status s) {
+    const cudaError_t ce = cudaGetLastError();
+    char buf[256];
+    std::snprintf(buf, sizeof(buf), "create: status %d (last CUDA error: %s)", (int)s, cudaGetErrorString(ce));
+    g_create_err = buf;
+    gmaf_destroy(ctx);
+    return s;
+  };
   if (cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess ||
       cudaMallocHost((void**)&ctx->h_state, sizeof(SolverState)) != cudaSuccess ||
@@ -741,7 +799,7 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
     if (configure_pcg_kernels(ctx->tiles, K) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
     // single-pass kernel: its own tiles (wider halo, TMA ring) and occupancy
     TileCfg sprobe = make_tiles(grid->n_theta, sl.y1 - sl.y0, K, 1, tw_single(grid->n_theta));
-    if (configure_sr_kernels(sprobe) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
+    if (configure_sr_kernels(sprobe, K) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
     const int socc = sr_ctas_per_sm(sprobe);
     ctx->tiles_sr = make_tiles(grid->n_theta, sl.y1 - sl.y0, K, sms * (socc > 0 ? socc : 1), tw_single(grid->n_theta));
     if (ctx->tiles_sr.n_tiles > kMaxTilesPerCondition) return cleanup_fail(GMAF_E_INVALID_MESH);
@@ -755,6 +813,13 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
     ctx->schedule = single_ok(grid->n_theta) && ctx->sr_k_ok ? GMAF_SCHEDULE_SINGLE : GMAF_SCHEDULE_TABLE1;
     const char* sch = std::getenv("GMAF_SCHEDULE");
     if (sch && std::strcmp(sch, "table1") == 0) ctx->schedule = GMAF_SCHEDULE_TABLE1;
+    // persistent single-pass solve (one rank): needs every CTA of the one-wave grid resident
+    // with the persistent kernel's extra shared memory (GMAF_PERSIST=0 selects the per-iteration
+    // kernels inside the graph's WHILE loop)
+    const char* pe = std::getenv("GMAF_PERSIST");
+    const bool want = !(pe && std::strcmp(pe, "0") == 0);
+    ctx->persist_ok = want && !dm && single_ok(grid->n_theta) && ctx->sr_k_ok && srp_fits(ctx->tiles_sr, K) &&
+                      (long long)srp_ctas_per_sm(ctx->tiles_sr, K) * sms >= (long long)ctx->tiles_sr.n_tiles * K;
   }
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
   ctx->quad_ctas = quad_ctas_per_condition(gp, K);
@@ -854,6 +919,9 @@ gmaf_status gmaf_thickness(gmaf_ctx* ctx, const gmaf_condition* conds_all) {
   }
   ctx->M = (int)ctx->mat_rep.size();
   ctx->state = ST_CREATED;
+  if (ctx->M > ctx->Mcap)
+    return fail(ctx, GMAF_E_WORKSPACE, "thickness: %d distinct coefficient sets (distinct (e, L_F)), the workspace "
+                "holds %d (gmaf_workspace_bytes_m)", ctx->M, ctx->Mcap);
   CU(cudaMemcpyAsync((void*)ctx->d.cp, ctx->h_cp, (size_t)K * sizeof(CondParams), cudaMemcpyHostToDevice,
                      ctx->stream));
   CU(cudaMemcpyAsync(ctx->d.mat_rep, ctx->mat_rep.data(), (size_t)ctx->M * sizeof(int32_t),
@@ -992,7 +1060,7 @@ gmaf_status gmaf_kernel_times(gmaf_ctx* ctx, gmaf_kernel_timing* out, int32_t n,
   CU(cudaStreamSynchronize(ctx->stream));
   static const char* names[KK_COUNT] = {"thickness_guard", "assemble", "pcg_init", "pcg_phase_a",
                                         "pcg_phase_b", "true_residual", "quadrature", "sr_init", "sr_iter",
-                                        "tail_of_sr_iter"};
+                                        "tail_of_sr_iter", "gridbar_wait"};
   const double rows = (double)(ctx->gp.y1 - ctx->gp.y0);   // own rows (all n_y on one rank)
   const double n_nodes = (double)ctx->grid.n_theta * rows * ctx->K;
   const double nM = (double)ctx->grid.n_theta * rows * (ctx->M > 0 ? ctx->M : ctx->K);
@@ -1008,7 +1076,8 @@ gmaf_status gmaf_kernel_times(gmaf_ctx* ctx, gmaf_kernel_timing* out, int32_t n,
       8.0 * n_nodes,                        // quadrature: read p
       8.0 * (2.0 * n_nodes + 3.0 * nM),     // sr_init: read S, write r (x zeroed: +1)
       8.0 * (5.0 * n_nodes + 3.0 * nM),     // sr_iter: r RW, pd RW, x RW every other; 3 bands
-      0.0};                                 // serial tail of sr_iter (inside its time)
+      0.0,                                  // serial tail of sr_iter (inside its time)
+      0.0};                                 // persistent: CTA 0's wait at the grid barrier
   int c = 0;
   for (int q = 0; q < KK_COUNT && c < n; ++q, ++c) {
     std::memset(&out[c], 0, sizeof(gmaf_kernel_timing));
@@ -1073,6 +1142,16 @@ gmaf_status gmaf_p2p_connect(gmaf_ctx* ctx, const void* handles) {
     void* p = nullptr;
     CU(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
     ctx->peer_bufs[r] = p;
+    // the kernels load and store this buffer directly (NVLink peer memory): refuse loudly if the
+    // owning GPU is not peer-accessible from this one (same GPU: always accessible)
+    cudaPointerAttributes pa;
+    CU(cudaPointerGetAttributes(&pa, p));
+    int mydev = 0, can = 1;
+    CU(cudaGetDevice(&mydev));
+    if (pa.device != mydev) CU(cudaDeviceCanAccessPeer(&can, mydev, pa.device));
+    if (!can)
+      return fail(ctx, GMAF_E_CUDA, "p2p_connect: GPU %d cannot access rank %d's GPU %d peer to peer (NVLink/P2P "
+                  "required by the peer-to-peer exchange)", mydev, r, pa.device);
     ctx->d.dist.peer[r] = static_cast<char*>(p);
     if (ctx->rows) ctx->d.dist.halo_in[r] = reinterpret_cast<double*>(static_cast<char*>(p) + ctx->inbox_off);
   }
@@ -1100,17 +1179,15 @@ gmaf_status gmaf_slab_rows(int32_t n_y, int32_t world, int32_t rank, int32_t* y0
   return GMAF_OK;
 }
 
-// Debugging aid (not part of include/gmaf.h): copy this rank's halo inbox
-// [2 slots][2 sides][2 vectors][K][4][nt] and the gather counter to the host.
-gmaf_status gmaf_debug_inbox(gmaf_ctx* ctx, double* host_out, unsigned long long* seq) {
-  if (!ctx || !host_out || !seq || !ctx->rows) return GMAF_E_INVALID_ARG;
-  const size_t n = (size_t)8 * SLAB_HALO * ctx->K * ctx->grid.n_theta;
-  CU(cudaMemcpy(host_out, ctx->p2p_buf + ctx->inbox_off, n * 8, cudaMemcpyDeviceToHost));
-  // then u[0], u[1] (all stored rows of all K) right after the inbox
-  const size_t nf = (size_t)ctx->K * ctx->gp.ns;
-  CU(cudaMemcpy(host_out + n, ctx->d.u[0], nf * 8, cudaMemcpyDeviceToHost));
-  CU(cudaMemcpy(host_out + n + nf, ctx->d.u[1], nf * 8, cudaMemcpyDeviceToHost));
-  CU(cudaMemcpy(seq, ctx->d.dist.seq, 8, cudaMemcpyDeviceToHost));
+gmaf_status gmaf_tile_config(const gmaf_ctx* ctx, gmaf_tiles* out) {
+  if (!ctx || !out) return GMAF_E_INVALID_ARG;
+  const bool single = ctx->schedule == GMAF_SCHEDULE_SINGLE;
+  const TileCfg& t = single ? ctx->tiles_sr : ctx->tiles;
+  out->tw = t.tw; out->th = t.th; out->n_strips = t.n_strips; out->n_chunks = t.n_chunks;
+  out->n_ctas = t.n_tiles * ctx->K;
+  out->schedule = ctx->schedule;
+  out->persistent = (single && ctx->persist_ok && !ctx->distm) ? 1 : 0;
+  out->pad = 0;
   return GMAF_OK;
 }
 
@@ -1121,6 +1198,8 @@ gmaf_status gmaf_slab(const gmaf_ctx* ctx, int32_t* y0, int32_t* y1) {
   return GMAF_OK;
 }
 
-const char* gmaf_last_error(const gmaf_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+const char* gmaf_last_error(const gmaf_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : (g_create_err.empty() ? "null context" : g_create_err.c_str());
+}
 
 }  // extern "C"

@@ -44,7 +44,9 @@ __host__ __device__ __forceinline__ long long fofs(const GridParams& g, int k) {
 // Kernel kinds for the in-kernel %globaltimer accounting.
 enum KernelKind { KK_THICK = 0, KK_ASSEMBLE, KK_INIT, KK_PHASE_A, KK_PHASE_B, KK_TRUERES, KK_QUAD,
                   KK_SR_INIT, KK_SR_ITER,
-                  KK_SR_TAIL,   // serial tail of k_sr ITER (last CTA: reduction + scalar stage), inside KK_SR_ITER
+                  KK_SR_TAIL,   // serial tail of k_sr ITER (last CTA: reduction + scalar stage), inside KK_SR_ITER;
+                                // persistent k_srp: grid barrier complete -> scalars ready (CTA 0)
+                  KK_SR_WAIT,   // persistent k_srp: CTA 0's arrival at the grid barrier -> barrier complete
                   KK_COUNT };
 
 struct Timing {
@@ -172,8 +174,14 @@ cudaError_t launch_sr_fixup(const GridParams& g, const DevPtrs& d, int K, cudaSt
 // multi-rank: scalars from the gathered per-condition sums (one CTA)
 cudaError_t launch_sr_scalar(const DevPtrs& d, bool init, int Kglob, int Klocal, int kofs, int world,
                              cudaStream_t s);
-cudaError_t configure_sr_kernels(const TileCfg& t);
+cudaError_t configure_sr_kernels(const TileCfg& t, int K);
 int sr_ctas_per_sm(const TileCfg& t);
+// persistent single-pass solve (one rank): every iteration in one cooperative launch with a grid
+// barrier per iteration and the scalar stage evaluated redundantly in every CTA (sr.cu k_srp)
+cudaError_t launch_sr_persistent(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,
+                                 cudaStream_t s);
+int srp_ctas_per_sm(const TileCfg& t, int K);
+bool srp_fits(const TileCfg& t, int K);
 // peer-to-peer mode: gather n doubles per rank from src into packed_all-style dst [world][n]
 // (one thread; a timeout marks the solve failed, GMAF_E_CUDA)
 cudaError_t launch_p2p_gather(const DevPtrs& d, const double* src, int n, double* dst, cudaStream_t s);

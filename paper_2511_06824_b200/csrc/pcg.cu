@@ -400,13 +400,19 @@ static cudaError_t launch_tiles(KernelT kern, const GridParams& g, const DevPtrs
 }
 
 template <typename KernelT>
-static cudaError_t set_smem(KernelT kern, int bytes) {
-  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+static cudaError_t set_smem(KernelT kern, int) {
+  return raise_smem_cap(kern);
 }
 
 // Called once per context, outside any stream capture.
 cudaError_t configure_pcg_kernels(const TileCfg& t, int K) {
-  const int sm = (int)tile_smem(t, K);
+  // raised once to the device's opt-in maximum (see configure_sr_kernels)
+  const int sm = smem_optin_max();
+  if (sm <= 0 || (long long)tile_smem(t, K) > sm) return cudaErrorInvalidValue;
+  static unsigned done = 0u;   // once per device
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cudaErrorInvalidValue;
+  if (done & (1u << dev)) return cudaSuccess;
   cudaError_t e = cudaSuccess;
 #define GMAF_SET(...) if (e == cudaSuccess) e = set_smem(__VA_ARGS__, sm)
   GMAF_SET(k_phase_a<PC_ASSOR2>); GMAF_SET(k_phase_a<PC_JACOBI>); GMAF_SET(k_phase_a<PC_NONE>);
@@ -418,6 +424,7 @@ cudaError_t configure_pcg_kernels(const TileCfg& t, int K) {
   GMAF_SET(k_phase_b<PC_NONE, MODE_INIT_WARM>);
   GMAF_SET(k_phase_b<PC_NONE, MODE_TRUERES>);
 #undef GMAF_SET
+  if (e == cudaSuccess) done |= 1u << dev;
   return e;
 }
 

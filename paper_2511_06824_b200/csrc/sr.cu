@@ -51,336 +51,652 @@ __host__ __device__ inline size_t sr_smem_bytes(int nl) {
          (SR_CSLOTS + SR_VSLOTS + SR_CSLOTS) * sizeof(uint64_t) + 64;
 }
 
+// Per-thread geometry of one (strip, row chunk, condition) tile, recomputed by each role.
+struct SrGeo {
+  int NTC, NCT, NL, tid, tl, k, i0, j0, j1, gl, gr, im, ip, jbase, nsteps, m;
+  bool is_producer, out, seamL, seamR, seamWarp, lcoef;
+  long long fk;
+};
+
+__device__ __forceinline__ SrGeo sr_geo(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K) {
+  SrGeo q;
+  // warps 0 .. NCT/32-1 compute (one thread per column pair); the last warp streams rows (TMA)
+  q.NTC = t.tw / 2 + SR_HALO;             // column pairs
+  q.NCT = (q.NTC + 31) & ~31;             // compute threads (whole warps; idle lanes alias the last pair)
+  q.NL = 2 * q.NTC;                       // loaded columns = tw + 2*HALO
+  q.tid = threadIdx.x;
+  q.is_producer = q.tid >= q.NCT;
+  q.tl = min(q.tid, q.NTC - 1);
+  q.k = blockIdx.x % K;
+  const int tile = blockIdx.x / K;
+  const int strip = tile % t.n_strips, chunk = tile / t.n_strips;
+  const int nt = g.nt;
+  q.i0 = strip * t.tw - t.tw / 2;                   // first output column (may be negative: mod nt)
+  q.j0 = g.y0 + chunk * t.th;
+  q.j1 = min(q.j0 + t.th, g.y1);                    // own rows [y0, y1)
+  const int cl = 2 * q.tl;
+  int gl = (q.i0 - SR_HALO + cl) % nt;
+  if (gl < 0) gl += nt;
+  q.gl = gl;
+  q.gr = gl + 1;                           // gl is even and nt is even: the pair never wraps
+  // output pair: inside [HALO, HALO + TW) and, for the last (ragged) strip, before column
+  // tw/2 + n_strips*tw - tw/2 ... i.e. its global output index i0 + cl - HALO < nt - tw/2
+  const int o = q.i0 + cl - SR_HALO + t.tw / 2;     // output index counted from strip 0's start
+  q.out = (q.tid < q.NTC) && (cl >= SR_HALO) && (cl < SR_HALO + t.tw) && (o < nt);
+  // ASSOR split on the periodic ring (R-A12): only a pair holding column 0 on its left or
+  // column nt-1 on its right sees the wraps; every other pair uses the plain formulas.
+  q.seamL = (q.gl == 0);
+  q.seamR = (q.gr == nt - 1);
+  q.seamWarp = false;                      // set by the compute role (warp vote)
+  q.im = max(cl - 1, 0);                   // scalar index of the left neighbour of the pair
+  q.ip = min(cl + 2, q.NL - 1);            // scalar index of the right neighbour of the pair
+  // the left neighbour's A_E comes by shuffle, except in lane 0 and in idle lanes (which must
+  // reproduce the last real pair exactly, since they write the same ring slots)
+  q.lcoef = (q.tid & 31) == 0 || q.tid >= q.NTC;
+  q.fk = fofs(g, q.k);                     // field base of condition k (global row indexing)
+  q.m = d.cp[q.k].mat;
+  q.jbase = q.j0 - SR_YLO;
+  // steps jl = jbase .. jbase + nsteps - 1; the real ones end at j1 + LAG - 1, the rest pad to
+  // a whole number of unrolled blocks (their rows read as zero rows)
+  q.nsteps = ((q.j1 + SR_LAG - q.jbase) + SR_UNROLL - 1) & ~(SR_UNROLL - 1);
+  return q;
+}
+
+// Shared-memory carve-up of the single-pass kernels (NL doubles per row).
+struct SrSmem {
+  double *vstage, *cring, *ringW, *ringV, *ringP, *ringW2, *ringV2, *ringU2;
+  uint32_t full0, emptyv0, emptyc0;
+};
+__device__ __forceinline__ SrSmem sr_smem(double* smem_raw, int NL) {
+  SrSmem s;
+  s.vstage = smem_raw;                               // [4][3][NL]  r, pd, x rows
+  s.cring = s.vstage + SR_VSLOTS * 3 * NL;           // [8][3][NL]  AP, AE, AN rows
+  s.ringW = s.cring + SR_CSLOTS * 3 * NL;            // [2][NL] each
+  s.ringV = s.ringW + 2 * NL;
+  s.ringP = s.ringV + 2 * NL;
+  s.ringW2 = s.ringP + 2 * NL;
+  s.ringV2 = s.ringW2 + 2 * NL;
+  s.ringU2 = s.ringV2 + 2 * NL;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s.ringU2 + 2 * NL);
+  s.full0 = smem_addr(bars);                         // [8] one per step mod 8
+  s.emptyv0 = s.full0 + 8 * SR_CSLOTS;               // [4]
+  s.emptyc0 = s.emptyv0 + 8 * SR_VSLOTS;             // [8]
+  return s;
+}
+
+__device__ __forceinline__ void sr_init_barriers(const SrGeo& q, const SrSmem& s) {
+  if (q.tid == 0) {
+    for (int b = 0; b < SR_CSLOTS; ++b) mbar_init(s.full0 + 8 * b, 1);
+    for (int b = 0; b < SR_VSLOTS; ++b) mbar_init(s.emptyv0 + 8 * b, q.NCT / 32);
+    for (int b = 0; b < SR_CSLOTS; ++b) mbar_init(s.emptyc0 + 8 * b, q.NCT / 32);
+    mbar_fence_init();
+  }
+  for (int i = q.tid; i < 12 * q.NL; i += blockDim.x) s.ringW[i] = 0.0;
+}
+
+// ------------------------------------------------------------------ TMA producer warp
+// Streams steps [s_lo, s_hi) of one tile pass.  gstep0 = steps this CTA streamed in earlier
+// passes (a multiple of 8): the ring slots and mbarrier phases continue across the passes of the
+// persistent kernel.  Lane a < 6 streams array a: 0 r, 1 pd_{i-1}, 2 x (or S), 3 AP, 4 AE, 5 AN.
+template <int MODE>
+__device__ __forceinline__ void sr_produce(const GridParams& g, const DevPtrs& d, const SrGeo& q,
+                                           const SrSmem& s, int K, int parity, uint32_t gstep0, int s_lo,
+                                           int s_hi) {
+  constexpr bool ITER = (MODE == SR_ITER_EVEN || MODE == SR_ITER_ODD);
+  constexpr bool XUPD = (MODE == SR_ITER_ODD);
+  constexpr bool USE_PD = ITER;
+  constexpr bool USE_X = XUPD || (MODE == SR_INIT_WARM);
+  const int nt = g.nt, ny = g.ny, NL = q.NL;
+  const long long fk = q.fk;
+  // ITER: r_i = R[parity], pd_{i-1} = PD[1-parity].  INIT: r_0 = S (cold) or R[1] (warm).
+  const double* rin = ITER ? d.r[parity] + fk : (MODE == SR_INIT_COLD ? d.S + fk : d.r[1] + fk);
+  const int lane = q.tid - q.NCT;
+  const bool vec = lane < 3;
+  const double* srcp = lane == 0 ? rin
+                     : lane == 1 ? d.u[1 - parity] + fk
+                     : lane == 2 ? ((MODE == SR_INIT_WARM) ? d.S + fk : d.p + fk)
+                     : lane == 3 ? d.AP + fofs(g, q.m)
+                     : lane == 4 ? d.AE + fofs(g, q.m)
+                                 : d.AN + fofs(g, q.m);
+  const double* constrow = lane == 3 ? d.one_row : d.zero_row;
+  const bool used = lane < 6 && (lane != 1 || USE_PD) && (lane != 2 || USE_X);
+  const int lag = lane == 1 ? 1 : (lane == 2 ? 2 : 0);
+  const int j0 = q.j0, j1 = q.j1, jbase = q.jbase;
+  int lo = jbase, hi = min(j1 + SR_YHI, ny);                         // rows really read
+  if (lane == 1) { lo = j0 - SR_YLO + 1; hi = min(j1 + SR_YHI - 1, ny); }
+  if (lane == 2) { lo = j0; hi = j1; }
+  if (lo < 0) lo = 0;
+  int g0 = (q.i0 - SR_HALO) % nt;
+  if (g0 < 0) g0 += nt;
+  const int len0 = min(NL, nt - g0);                  // first segment (the seam splits a row)
+  const uint32_t bytes = (uint32_t)NL * 8u * (uint32_t)(4 + (USE_PD ? 1 : 0) + (USE_X ? 1 : 0));
+  const uint32_t dst0 = smem_addr(vec ? s.vstage + lane * NL : s.cring + (lane - 3) * NL);
+  const uint32_t dstride = (uint32_t)(3 * NL * 8);    // bytes between slots
+  // row-slab mode: an iteration's r and pd rows outside the own slab come from the inbox the
+  // neighbours pushed them into (slot = parity of the last gather stamp)
+  const bool inbox = ITER && lane < 2 && d.dist.rows == 1;
+  const double* ibase = inbox ? d.dist.halo_in[d.dist.rank] : nullptr;
+  const int islot = inbox ? (int)(*d.dist.seq & 1ull) : 0;
+  for (int step = s_lo; step < s_hi; ++step) {
+    const uint32_t gs = gstep0 + (uint32_t)step;
+    const int sv = (int)(gs & (SR_VSLOTS - 1)), sc = (int)(gs & (SR_CSLOTS - 1));
+    if (gs >= SR_VSLOTS) mbar_wait_sleep(s.emptyv0 + 8 * sv, ((gs / SR_VSLOTS) - 1) & 1);
+    if (gs >= SR_CSLOTS) mbar_wait_sleep(s.emptyc0 + 8 * sc, ((gs / SR_CSLOTS) - 1) & 1);
+    const uint32_t bar = s.full0 + 8 * sc;
+    if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
+    __syncwarp();
+    if (used) {
+      const int row = jbase + step - lag;
+      const uint32_t dst = dst0 + (uint32_t)(vec ? sv : sc) * dstride;
+      if (row >= lo && row < hi) {
+        const double* rowp = srcp + (long long)row * nt;
+        if (inbox && (row < g.y0 || row >= g.y1)) {
+          const int side = row < g.y0 ? 0 : 1;
+          rowp = ibase + halo_ofs(islot, side, lane, K, q.k, side ? row - g.y1 : row - (g.y0 - SLAB_HALO), nt);
+        }
+        bulk_g2s(dst, rowp + g0, (uint32_t)len0 * 8u, bar);
+        int done = len0;
+        while (done < NL) {                              // wrapped remainder (small n_theta loops)
+          const int len = min(NL - done, nt);
+          bulk_g2s(dst + (uint32_t)done * 8u, rowp, (uint32_t)len * 8u, bar);
+          done += len;
+        }
+      } else {
+        bulk_g2s(dst, constrow, (uint32_t)NL * 8u, bar);
+      }
+    }
+  }
+}
+
+// -------------------------------------------------------------------- compute warps
+// One pass of the 7-stage row pipeline over the tile (all nsteps steps).  Accumulates the
+// per-thread gamma, delta, r.r and S.S partials into acc.
+template <int PC, int MODE>
+__device__ __forceinline__ void sr_compute(const GridParams& g, const DevPtrs& d, const SrGeo& q, const SrSmem& s,
+                                           int parity, double alpha, double alpha_prev, double beta, double omega,
+                                           uint32_t gstep0, double& acc_rr, double& acc_g, double& acc_d,
+                                           double& acc_s) {
+  constexpr bool ITER = (MODE == SR_ITER_EVEN || MODE == SR_ITER_ODD);
+  constexpr bool XUPD = (MODE == SR_ITER_ODD);         // x += a_{i-1} pd_{i-1} + a_i pd_i
+  constexpr bool USE_PD = ITER;                         // pd_{-1} = 0 is stored by the init
+  constexpr bool USE_X = XUPD || (MODE == SR_INIT_WARM);  // a warm init streams S in the x slot
+  const int nt = g.nt, NL = q.NL, NTC = q.NTC, NCT = q.NCT, tl = q.tl, im = q.im, ip = q.ip;
+  const int j0 = q.j0, j1 = q.j1, jbase = q.jbase, gl = q.gl;
+  const bool out = q.out, seamL = q.seamL, seamR = q.seamR, lcoef = q.lcoef;
+  // warp-uniform guard: only the warp holding a seam pair runs the wrap corrections
+  const bool seamWarp = __any_sync(0xffffffffu, (seamL || seamR) && q.tid < NCT);
+  double* rout = (ITER ? d.r[1 - parity] : d.r[0]) + q.fk;
+  double* pdout = (ITER ? d.u[parity] : d.u[1]) + q.fk;
+  double* x = d.p + q.fk;
+  const double c2 = (2.0 - omega) * omega;
+  const double romega = 1.0 / omega;
+  const double* vstage = s.vstage;
+  const double* cring = s.cring;
+
+  // own-column history in registers (suffix = lag in rows behind the load row);
+  // coefficient rows are read from the 8-slot ring at their lag
+  D2 oD1{0, 0}, oD2{0, 0}, oD3{0, 0};
+  D2 r1{0, 0}, r2{0, 0}, pdo2{0, 0}, pd2{0, 0}, pd3{0, 0}, rn3{0, 0}, u2_4{0, 0};
+  const bool lane0 = (q.tid & 31) == 0;
+  for (int blk = 0; blk < q.nsteps; blk += SR_UNROLL) {
+    const uint32_t gblk = gstep0 + (uint32_t)blk;
+    const uint32_t cpar = (gblk / SR_UNROLL) & 1u;                   // phase of the per-step barriers
+#pragma unroll
+    for (int u = 0; u < SR_UNROLL; ++u) {
+      const int jl = jbase + blk + u;
+      const int sv = u & (SR_VSLOTS - 1);
+      // coefficient rows at lag L live in slot (u - L) & 7; arrays AP=0, AE=1, AN=2
+      const double* c0 = cring + (((u + 8) & 7) * 3) * NL;
+      const double* c1 = cring + (((u + 7) & 7) * 3) * NL;
+      const double* c2r = cring + (((u + 6) & 7) * 3) * NL;
+      const double* c3 = cring + (((u + 5) & 7) * 3) * NL;
+      const double* c4 = cring + (((u + 4) & 7) * 3) * NL;
+      double* w_0 = s.ringW + (u & 1) * NL;
+      const double* w_1 = s.ringW + ((u + 1) & 1) * NL;
+      double* v_0 = s.ringV + (u & 1) * NL;
+      const double* v_1 = s.ringV + ((u + 1) & 1) * NL;
+      double* p_1 = s.ringP + ((u + 1) & 1) * NL;
+      const double* p_2 = s.ringP + (u & 1) * NL;
+      double* w2_2 = s.ringW2 + (u & 1) * NL;
+      const double* w2_3 = s.ringW2 + ((u + 1) & 1) * NL;
+      double* v2_2 = s.ringV2 + (u & 1) * NL;
+      const double* v2_3 = s.ringV2 + ((u + 1) & 1) * NL;
+      double* u2_3r = s.ringU2 + ((u + 1) & 1) * NL;
+      const double* u2_4r = s.ringU2 + (u & 1) * NL;
+
+      // ---- (A) row jl: streamed data, D^-1, w = D^-1 r
+      mbar_wait(s.full0 + 8 * u, cpar);
+      const double* vs = vstage + sv * 3 * NL;
+      const D2 r0 = ld2(vs, tl);
+      const D2 pdo1 = USE_PD ? ld2(vs + NL, tl) : D2{0, 0};
+      const D2 x2 = USE_X ? ld2(vs + 2 * NL, tl) : D2{0, 0};
+      __syncwarp();
+      if (lane0) mbar_arrive(s.emptyv0 + 8 * sv);            // this warp is done with vector slot sv
+      const D2 AP0 = ld2(c0, tl);
+      const D2 AE0 = ld2(c0 + NL, tl);
+      const D2 AN1 = ld2(c1 + 2 * NL, tl);
+      const D2 w1 = rld(w_1, tl, NTC);
+      D2 iD0{fast_rcp(AP0.l), fast_rcp(AP0.r)};
+      if constexpr (PC == SPC_ASSOR1) {
+        // ASSOR-I (Eq. 3.2): the preconditioner is the diagonal c / Dt with
+        // Dt_i = D_i + omega^2 sum_{k in L(i)} L_ik^2 / D_k, L = {W, E-wrap at n_theta-1, S}
+        // (R-A12); it enters the pipeline exactly like Jacobi's D^-1
+        const D2 AP1 = ld2(c1, tl);
+        const double apl = left_of(AP0.r, c0, im, lcoef), ael = left_of(AE0.r, c0 + NL, im, lcoef);
+        double sl = (ael * ael) * fast_rcp(apl);
+        double sr = (AE0.l * AE0.l) * iD0.l;
+        if (seamWarp) {
+          if (seamL) sl = 0.0;                                           // column 0: no W in L
+          if (seamR) sr += (AE0.r * AE0.r) * fast_rcp(c0[ip]);           // column nt-1: E-wrap
+        }
+        sl += (AN1.l * AN1.l) * fast_rcp(AP1.l);
+        sr += (AN1.r * AN1.r) * fast_rcp(AP1.r);
+        iD0 = {c2 * fast_rcp(AP0.l + (omega * omega) * sl), c2 * fast_rcp(AP0.r + (omega * omega) * sr)};
+      }
+      const D2 oD0{omega * iD0.l, omega * iD0.r};
+      D2 w0;
+      if constexpr (PC == SPC_NONE) w0 = r0; else w0 = {r0.l * iD0.l, r0.r * iD0.r};
+      rst(w_0, tl, NTC, w0);
+      row_bar(NCT);                                         // barrier 1: w(jl) complete
+
+      // ---- (B) v1(jl) = w - (omega/D) sum_L A w  (Eq. 3.5);  (C) z(jl-1), pd(jl-1)
+      D2 z1;
+      if constexpr (PC == SPC_ASSOR2) {
+        const double w0m = rleft(w_0, tl, NTC), ae0m = left_of(AE0.r, c0 + NL, im, lcoef);
+        const D2 v11 = rld(v_1, tl, NTC);
+        const double v1p = rright(v_1, tl);
+        const D2 AEm1 = ld2(c1 + NL, tl);
+        // plain pair: L = {W, S}, U = {E, N}
+        D2 sL{AN1.l * w1.l + ae0m * w0m, AN1.r * w1.r + AE0.l * w0.l};
+        if (seamWarp) {
+          if (seamL) sL.l -= ae0m * w0m;                        // column 0: W is the wrap (in U)
+          if (seamR) sL.r += AE0.r * rright(w_0, tl);           // column nt-1: E-wrap is in L
+        }
+        const D2 v10{w0.l - oD0.l * sL.l, w0.r - oD0.r * sL.r};
+        rst(v_0, tl, NTC, v10);
+        D2 sU{AN1.l * v10.l + AEm1.l * v11.r, AN1.r * v10.r + AEm1.r * v1p};
+        if (seamWarp) {
+          if (seamL) sU.l += c1[NL + im] * rleft(v_1, tl, NTC); // column 0: W-wrap
+          if (seamR) sU.r -= AEm1.r * v1p;                      // column nt-1: no E in U
+        }
+        z1 = {c2 * (v11.l - oD1.l * sU.l), c2 * (v11.r - oD1.r * sU.r)};
+      } else {
+        z1 = w1;                                            // D^-1 r (Jacobi) or r (none)
+      }
+      const D2 pd1 = USE_PD ? D2{z1.l + beta * pdo1.l, z1.r + beta * pdo1.r} : z1;   // step 9
+      rst(p_1, tl, NTC, pd1);
+      if (out && jl - 1 >= j0 && jl - 1 < j1)
+        stg2(pdout + (long long)(jl - 1) * nt + gl, ITER ? pd1 : D2{0, 0});   // INIT: pd_{-1} = 0
+      // ---- (D) s(jl-2) = A pd, r_{i+1} = r_i - alpha s, x, w2 = D^-1 r_{i+1}
+      D2 rn2;
+      const D2 AEm2 = ld2(c2r + NL, tl);
+      const D2 AN3 = ld2(c3 + 2 * NL, tl);
+      const double ae2m = left_of(AEm2.r, c2r + NL, im, lcoef);
+      {
+        const D2 AP2 = ld2(c2r, tl);
+        const D2 AN2 = ld2(c2r + 2 * NL, tl);
+        D2 sv{AP2.l * pd2.l + ae2m * rleft(p_2, tl, NTC), AP2.r * pd2.r + AEm2.l * pd2.l};
+        sv.l += AEm2.l * pd2.r + AN3.l * pd3.l + AN2.l * pd1.l;
+        sv.r += AEm2.r * rright(p_2, tl) + AN3.r * pd3.r + AN2.r * pd1.r;
+        rn2 = {r2.l - alpha * sv.l, r2.r - alpha * sv.r};  // step 5 (INIT: alpha = 0)
+      }
+      if (out && jl - 2 >= j0 && jl - 2 < j1) {
+        const long long q2 = (long long)(jl - 2) * nt + gl;
+        stg2(rout + q2, rn2);
+        acc_rr += rn2.l * rn2.l + rn2.r * rn2.r;
+        if (XUPD) stg2(x + q2, D2{x2.l + (alpha_prev * pdo2.l + alpha * pd2.l),      // step 4
+                                  x2.r + (alpha_prev * pdo2.r + alpha * pd2.r)});
+        if (MODE == SR_INIT_COLD) { stg2(x + q2, D2{0, 0}); acc_s += r2.l * r2.l + r2.r * r2.r; }
+        if (MODE == SR_INIT_WARM) acc_s += x2.l * x2.l + x2.r * x2.r;   // x2 holds S here
+      }
+      D2 wz;
+      if constexpr (PC == SPC_NONE) wz = rn2;
+      else wz = {(rn2.l * oD2.l) * romega, (rn2.r * oD2.r) * romega};
+      rst(w2_2, tl, NTC, wz);
+      row_bar(NCT);                                         // barrier 2: w2(jl-2) complete
+
+      // ---- (E) v2(jl-2)   (F) z2(jl-3), gamma   (G) A z2 at jl-4, delta
+      D2 u2_3;
+      if constexpr (PC == SPC_ASSOR2) {
+        const D2 w23 = rld(w2_3, tl, NTC);
+        const double wz2m = rleft(w2_2, tl, NTC);
+        const D2 v23 = rld(v2_3, tl, NTC);
+        const double v23p = rright(v2_3, tl);
+        const D2 AEm3 = ld2(c3 + NL, tl);
+        D2 sL{AN3.l * w23.l + ae2m * wz2m, AN3.r * w23.r + AEm2.l * wz.l};
+        if (seamWarp) {
+          if (seamL) sL.l -= ae2m * wz2m;
+          if (seamR) sL.r += AEm2.r * rright(w2_2, tl);
+        }
+        const D2 v22{wz.l - oD2.l * sL.l, wz.r - oD2.r * sL.r};
+        rst(v2_2, tl, NTC, v22);
+        D2 sU{AN3.l * v22.l + AEm3.l * v23.r, AN3.r * v22.r + AEm3.r * v23p};
+        if (seamWarp) {
+          if (seamL) sU.l += c3[NL + im] * rleft(v2_3, tl, NTC);
+          if (seamR) sU.r -= AEm3.r * v23p;
+        }
+        u2_3 = {c2 * (v23.l - oD3.l * sU.l), c2 * (v23.r - oD3.r * sU.r)};
+      } else {
+        u2_3 = rld(w2_3, tl, NTC);
+      }
+      u2_3r[tl] = u2_3.l;                                  // only the right-neighbour read (delta) remains
+      if (out && jl - 3 >= j0 && jl - 3 < j1) acc_g += rn3.l * u2_3.l + rn3.r * u2_3.r;   // gamma
+      {
+        // delta = z2' A z2 as the quadratic form (A symmetric): each owned row j adds its
+        // diagonal term and its east and north couplings, i.e. every edge once, at its
+        // west / south end -- no w = A z2 vector, one coefficient row (lag 4)
+        const D2 AP4 = ld2(c4, tl);
+        const D2 AEm4 = ld2(c4 + NL, tl);
+        const D2 AN4 = ld2(c4 + 2 * NL, tl);
+        if (out && jl - 4 >= j0 && jl - 4 < j1) {
+          const double ql = AP4.l * u2_4.l + 2.0 * (AEm4.l * u2_4.r + AN4.l * u2_3.l);
+          const double qr = AP4.r * u2_4.r + 2.0 * (AEm4.r * rright(u2_4r, tl) + AN4.r * u2_3.r);
+          acc_d += u2_4.l * ql + u2_4.r * qr;
+        }
+      }
+      __syncwarp();
+      // coefficient row jl-4 done (in the persistent kernel the first 4 steps of a pass release
+      // the last 4 rows of the previous pass)
+      if (lane0 && gblk + (uint32_t)u >= 4u) mbar_arrive(s.emptyc0 + 8 * ((u + 4) & 7));
+      // rotate the histories (register renaming across the unrolled steps)
+      u2_4 = u2_3;
+      rn3 = rn2;
+      pd3 = pd2; pd2 = pd1;
+      pdo2 = pdo1;
+      r2 = r1; r1 = r0;
+      oD3 = oD2; oD2 = oD1; oD1 = oD0;
+    }
+  }
+}
+
 template <int PC, int MODE>
 __global__ void __maxnreg__(168)
 k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long hcond, int use_cond) {
   extern __shared__ __align__(128) double smem_raw[];
   constexpr bool ITER = (MODE == SR_ITER_EVEN || MODE == SR_ITER_ODD);
-  constexpr bool XUPD = (MODE == SR_ITER_ODD);         // x += a_{i-1} pd_{i-1} + a_i pd_i
   constexpr bool INIT = !ITER;
-  constexpr bool USE_PD = ITER;                         // pd_{-1} = 0 is stored by the init
-  constexpr bool USE_X = XUPD || (MODE == SR_INIT_WARM);  // a warm init streams S in the x slot
   SolverState* st = d.st_;
   if (ITER && st->done) return;
   timing_begin(d.timing, ITER ? KK_SR_ITER : KK_SR_INIT);
-
-  // warps 0 .. NCT/32-1 compute (one thread per column pair); the last warp streams rows (TMA)
-  const int NTC = t.tw / 2 + SR_HALO;     // column pairs
-  const int NCT = (NTC + 31) & ~31;       // compute threads (whole warps; idle lanes alias the last pair)
-  const int NL = 2 * NTC;                 // loaded columns = tw + 2*HALO
-  const int tid = threadIdx.x;
-  const bool is_producer = tid >= NCT;
-  const int tl = min(tid, NTC - 1);
-  const int k = blockIdx.x % K;
-  const int tile = blockIdx.x / K;
-  const int strip = tile % t.n_strips, chunk = tile / t.n_strips;
-  const int nt = g.nt, ny = g.ny;
-  const int i0 = strip * t.tw - t.tw / 2;           // first output column (may be negative: mod nt)
-  const int j0 = g.y0 + chunk * t.th, j1 = min(j0 + t.th, g.y1);   // own rows [y0, y1)
-  const int cl = 2 * tl;
-  int gl = (i0 - SR_HALO + cl) % nt;
-  if (gl < 0) gl += nt;
-  const int gr = gl + 1;                   // gl is even and nt is even: the pair never wraps
-  // output pair: inside [HALO, HALO + TW) and, for the last (ragged) strip, before column
-  // tw/2 + n_strips*tw - tw/2 ... i.e. its global output index i0 + cl - HALO < nt - tw/2
-  const int o = i0 + cl - SR_HALO + t.tw / 2;       // output index counted from strip 0's start
-  const bool out = (tid < NTC) && (cl >= SR_HALO) && (cl < SR_HALO + t.tw) && (o < nt);
-  // ASSOR split on the periodic ring (R-A12): only a pair holding column 0 on its left or
-  // column nt-1 on its right sees the wraps; every other pair uses the plain formulas.
-  const bool seamL = (gl == 0), seamR = (gr == nt - 1);
-  // warp-uniform guard: only the warp holding a seam pair runs the wrap corrections
-  const bool seamWarp = __any_sync(0xffffffffu, (seamL || seamR) && tid < NCT);
-  const int im = max(cl - 1, 0);           // scalar index of the left neighbour of the pair
-  const int ip = min(cl + 2, NL - 1);      // scalar index of the right neighbour of the pair
-  // the left neighbour's A_E comes by shuffle, except in lane 0 and in idle lanes (which must
-  // reproduce the last real pair exactly, since they write the same ring slots)
-  const bool lcoef = (tid & 31) == 0 || tid >= NTC;
-
-  double* vstage = smem_raw;                                 // [4][3][NL]  r, pd, x rows
-  double* cring = vstage + SR_VSLOTS * 3 * NL;               // [8][3][NL]  AP, AE, AN rows
-  double* ringW = cring + SR_CSLOTS * 3 * NL;                // [2][NL] each
-  double* ringV = ringW + 2 * NL;
-  double* ringP = ringV + 2 * NL;
-  double* ringW2 = ringP + 2 * NL;
-  double* ringV2 = ringW2 + 2 * NL;
-  double* ringU2 = ringV2 + 2 * NL;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ringU2 + 2 * NL);
-  const uint32_t full0 = smem_addr(bars);                     // [8] one per step mod 8
-  const uint32_t emptyv0 = full0 + 8 * SR_CSLOTS;             // [4]
-  const uint32_t emptyc0 = emptyv0 + 8 * SR_VSLOTS;           // [8]
-
-  const long long fk = fofs(g, k);        // field base of condition k (global row indexing)
-  const int m = d.cp[k].mat;
-  // ITER: r_i = R[parity], pd_{i-1} = PD[1-parity]; writes R[1-parity], PD[parity].
-  // INIT: r_0 = S (cold) or R[1] (warm: = S - A x0 from the residual pre-pass); writes R[0]
-  //       and pd_{-1} = 0 into PD[1].
-  const double* rin = ITER ? d.r[parity] + fk : (MODE == SR_INIT_COLD ? d.S + fk : d.r[1] + fk);
-  double* rout = (ITER ? d.r[1 - parity] : d.r[0]) + fk;
-  double* pdout = (ITER ? d.u[parity] : d.u[1]) + fk;
-  double* x = d.p + fk;
-
-  const double alpha = ITER ? d.cs.alpha[k] : 0.0;
-  const double alpha_prev = ITER ? d.cs.uvk[k] : 0.0;   // uvk holds alpha_{i-1} here
-  const double beta = ITER ? d.cs.beta[k] : 0.0;
-  const double omega = st->omega;
-  const double c2 = (2.0 - omega) * omega;
-  const double romega = 1.0 / omega;
-
-  const int jbase = j0 - SR_YLO;
-  // steps jl = jbase .. jbase + nsteps - 1; the real ones end at j1 + LAG - 1, the rest pad to
-  // a whole number of unrolled blocks (their rows read as zero rows)
-  const int nsteps = ((j1 + SR_LAG - jbase) + SR_UNROLL - 1) & ~(SR_UNROLL - 1);
-
-  if (tid == 0) {
-    for (int s = 0; s < SR_CSLOTS; ++s) mbar_init(full0 + 8 * s, 1);
-    for (int s = 0; s < SR_VSLOTS; ++s) mbar_init(emptyv0 + 8 * s, NCT / 32);
-    for (int s = 0; s < SR_CSLOTS; ++s) mbar_init(emptyc0 + 8 * s, NCT / 32);
-    mbar_fence_init();
-  }
-  for (int q = tid; q < 12 * NL; q += blockDim.x) ringW[q] = 0.0;
+  const SrGeo q = sr_geo(g, d, t, K);
+  const SrSmem s = sr_smem(smem_raw, q.NL);
+  sr_init_barriers(q, s);
   __syncthreads();
 
   double acc_rr = 0, acc_g = 0, acc_d = 0, acc_s = 0;
   // asynchronous strategy: a frozen condition's CTAs only join the reduction
-  const bool frozen = ITER && st->coupling == 2 && d.cs.frz[k] != 0;
+  const bool frozen = ITER && st->coupling == 2 && d.cs.frz[q.k] != 0;
   if (frozen) {
-  } else if (is_producer) {
-    // ------------------------------------------------------------- TMA producer warp
-    // lane a < 6 streams array a: 0 r, 1 pd_{i-1}, 2 x (or S), 3 AP, 4 AE, 5 AN
-    const int lane = tid - NCT;
-    const bool vec = lane < 3;
-    const double* srcp = lane == 0 ? rin
-                       : lane == 1 ? d.u[1 - parity] + fk
-                       : lane == 2 ? ((MODE == SR_INIT_WARM) ? d.S + fk : x)
-                       : lane == 3 ? d.AP + fofs(g, m)
-                       : lane == 4 ? d.AE + fofs(g, m)
-                                   : d.AN + fofs(g, m);
-    const double* constrow = lane == 3 ? d.one_row : d.zero_row;
-    const bool used = lane < 6 && (lane != 1 || USE_PD) && (lane != 2 || USE_X);
-    const int lag = lane == 1 ? 1 : (lane == 2 ? 2 : 0);
-    int lo = jbase, hi = min(j1 + SR_YHI, ny);                         // rows really read
-    if (lane == 1) { lo = j0 - SR_YLO + 1; hi = min(j1 + SR_YHI - 1, ny); }
-    if (lane == 2) { lo = j0; hi = j1; }
-    if (lo < 0) lo = 0;
-    int g0 = (i0 - SR_HALO) % nt;
-    if (g0 < 0) g0 += nt;
-    const int len0 = min(NL, nt - g0);                  // first segment (the seam splits a row)
-    const uint32_t bytes = (uint32_t)NL * 8u * (uint32_t)(4 + (USE_PD ? 1 : 0) + (USE_X ? 1 : 0));
-    const uint32_t dst0 = smem_addr(vec ? vstage + lane * NL : cring + (lane - 3) * NL);
-    const uint32_t dstride = (uint32_t)(3 * NL * 8);    // bytes between slots
-    // row-slab mode: an iteration's r and pd rows outside the own slab come from the inbox the
-    // neighbours pushed them into (slot = parity of the last gather stamp)
-    const bool inbox = ITER && lane < 2 && d.dist.rows == 1;
-    const double* ibase = inbox ? d.dist.halo_in[d.dist.rank] : nullptr;
-    const int islot = inbox ? (int)(*d.dist.seq & 1ull) : 0;
-    for (int step = 0; step < nsteps; ++step) {
-      const int sv = step & (SR_VSLOTS - 1), sc = step & (SR_CSLOTS - 1);
-      if (step >= SR_VSLOTS) mbar_wait_sleep(emptyv0 + 8 * sv, (uint32_t)(((step / SR_VSLOTS) - 1) & 1));
-      if (step >= SR_CSLOTS) mbar_wait_sleep(emptyc0 + 8 * sc, (uint32_t)(((step / SR_CSLOTS) - 1) & 1));
-      const uint32_t bar = full0 + 8 * sc;
-      if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
-      __syncwarp();
-      if (used) {
-        const int row = jbase + step - lag;
-        const uint32_t dst = dst0 + (uint32_t)(vec ? sv : sc) * dstride;
-        if (row >= lo && row < hi) {
-          const double* rowp = srcp + (long long)row * nt;
-          if (inbox && (row < g.y0 || row >= g.y1)) {
-            const int side = row < g.y0 ? 0 : 1;
-            rowp = ibase + halo_ofs(islot, side, lane, K, k, side ? row - g.y1 : row - (g.y0 - SLAB_HALO), nt);
-          }
-          bulk_g2s(dst, rowp + g0, (uint32_t)len0 * 8u, bar);
-          int done = len0;
-          while (done < NL) {                              // wrapped remainder (small n_theta loops)
-            const int len = min(NL - done, nt);
-            bulk_g2s(dst + (uint32_t)done * 8u, rowp, (uint32_t)len * 8u, bar);
-            done += len;
-          }
-        } else {
-          bulk_g2s(dst, constrow, (uint32_t)NL * 8u, bar);
-        }
-      }
-    }
+  } else if (q.is_producer) {
+    sr_produce<MODE>(g, d, q, s, K, parity, 0u, 0, q.nsteps);
   } else {
-    // -------------------------------------------------------------- compute warps
-    // own-column history in registers (suffix = lag in rows behind the load row);
-    // coefficient rows are read from the 8-slot ring at their lag
-    D2 oD1{0, 0}, oD2{0, 0}, oD3{0, 0};
-    D2 r1{0, 0}, r2{0, 0}, pdo2{0, 0}, pd2{0, 0}, pd3{0, 0}, rn3{0, 0}, u2_4{0, 0};
-    const bool lane0 = (tid & 31) == 0;
-    for (int blk = 0; blk < nsteps; blk += SR_UNROLL) {
-      const uint32_t cpar = (uint32_t)((blk / SR_UNROLL) & 1);       // phase of the per-step barriers
-#pragma unroll
-      for (int u = 0; u < SR_UNROLL; ++u) {
-        const int jl = jbase + blk + u;
-        const int sv = u & (SR_VSLOTS - 1);
-        // coefficient rows at lag L live in slot (u - L) & 7; arrays AP=0, AE=1, AN=2
-        const double* c0 = cring + (((u + 8) & 7) * 3) * NL;
-        const double* c1 = cring + (((u + 7) & 7) * 3) * NL;
-        const double* c2r = cring + (((u + 6) & 7) * 3) * NL;
-        const double* c3 = cring + (((u + 5) & 7) * 3) * NL;
-        const double* c4 = cring + (((u + 4) & 7) * 3) * NL;
-        double* w_0 = ringW + (u & 1) * NL;
-        const double* w_1 = ringW + ((u + 1) & 1) * NL;
-        double* v_0 = ringV + (u & 1) * NL;
-        const double* v_1 = ringV + ((u + 1) & 1) * NL;
-        double* p_1 = ringP + ((u + 1) & 1) * NL;
-        const double* p_2 = ringP + (u & 1) * NL;
-        double* w2_2 = ringW2 + (u & 1) * NL;
-        const double* w2_3 = ringW2 + ((u + 1) & 1) * NL;
-        double* v2_2 = ringV2 + (u & 1) * NL;
-        const double* v2_3 = ringV2 + ((u + 1) & 1) * NL;
-        double* u2_3r = ringU2 + ((u + 1) & 1) * NL;
-        const double* u2_4r = ringU2 + (u & 1) * NL;
-
-        // ---- (A) row jl: streamed data, D^-1, w = D^-1 r
-        mbar_wait(full0 + 8 * u, cpar);
-        const double* vs = vstage + sv * 3 * NL;
-        const D2 r0 = ld2(vs, tl);
-        const D2 pdo1 = USE_PD ? ld2(vs + NL, tl) : D2{0, 0};
-        const D2 x2 = USE_X ? ld2(vs + 2 * NL, tl) : D2{0, 0};
-        __syncwarp();
-        if (lane0) mbar_arrive(emptyv0 + 8 * sv);            // this warp is done with vector slot sv
-        const D2 AP0 = ld2(c0, tl);
-        const D2 AE0 = ld2(c0 + NL, tl);
-        const D2 AN1 = ld2(c1 + 2 * NL, tl);
-        const D2 w1 = rld(w_1, tl, NTC);
-        D2 iD0{fast_rcp(AP0.l), fast_rcp(AP0.r)};
-        if constexpr (PC == SPC_ASSOR1) {
-          // ASSOR-I (Eq. 3.2): the preconditioner is the diagonal c / Dt with
-          // Dt_i = D_i + omega^2 sum_{k in L(i)} L_ik^2 / D_k, L = {W, E-wrap at n_theta-1, S}
-          // (R-A12); it enters the pipeline exactly like Jacobi's D^-1
-          const D2 AP1 = ld2(c1, tl);
-          const double apl = left_of(AP0.r, c0, im, lcoef), ael = left_of(AE0.r, c0 + NL, im, lcoef);
-          double sl = (ael * ael) * fast_rcp(apl);
-          double sr = (AE0.l * AE0.l) * iD0.l;
-          if (seamWarp) {
-            if (seamL) sl = 0.0;                                           // column 0: no W in L
-            if (seamR) sr += (AE0.r * AE0.r) * fast_rcp(c0[ip]);           // column nt-1: E-wrap
-          }
-          sl += (AN1.l * AN1.l) * fast_rcp(AP1.l);
-          sr += (AN1.r * AN1.r) * fast_rcp(AP1.r);
-          iD0 = {c2 * fast_rcp(AP0.l + (omega * omega) * sl), c2 * fast_rcp(AP0.r + (omega * omega) * sr)};
-        }
-        const D2 oD0{omega * iD0.l, omega * iD0.r};
-        D2 w0;
-        if constexpr (PC == SPC_NONE) w0 = r0; else w0 = {r0.l * iD0.l, r0.r * iD0.r};
-        rst(w_0, tl, NTC, w0);
-        compute_bar(NCT);                                     // barrier 1: w(jl) complete
-
-        // ---- (B) v1(jl) = w - (omega/D) sum_L A w  (Eq. 3.5);  (C) z(jl-1), pd(jl-1)
-        D2 z1;
-        if constexpr (PC == SPC_ASSOR2) {
-          const double w0m = rleft(w_0, tl, NTC), ae0m = left_of(AE0.r, c0 + NL, im, lcoef);
-          const D2 v11 = rld(v_1, tl, NTC);
-          const double v1p = rright(v_1, tl);
-          const D2 AEm1 = ld2(c1 + NL, tl);
-          // plain pair: L = {W, S}, U = {E, N}
-          D2 sL{AN1.l * w1.l + ae0m * w0m, AN1.r * w1.r + AE0.l * w0.l};
-          if (seamWarp) {
-            if (seamL) sL.l -= ae0m * w0m;                        // column 0: W is the wrap (in U)
-            if (seamR) sL.r += AE0.r * rright(w_0, tl);           // column nt-1: E-wrap is in L
-          }
-          const D2 v10{w0.l - oD0.l * sL.l, w0.r - oD0.r * sL.r};
-          rst(v_0, tl, NTC, v10);
-          D2 sU{AN1.l * v10.l + AEm1.l * v11.r, AN1.r * v10.r + AEm1.r * v1p};
-          if (seamWarp) {
-            if (seamL) sU.l += c1[NL + im] * rleft(v_1, tl, NTC); // column 0: W-wrap
-            if (seamR) sU.r -= AEm1.r * v1p;                      // column nt-1: no E in U
-          }
-          z1 = {c2 * (v11.l - oD1.l * sU.l), c2 * (v11.r - oD1.r * sU.r)};
-        } else {
-          z1 = w1;                                            // D^-1 r (Jacobi) or r (none)
-        }
-        const D2 pd1 = USE_PD ? D2{z1.l + beta * pdo1.l, z1.r + beta * pdo1.r} : z1;   // step 9
-        rst(p_1, tl, NTC, pd1);
-        if (out && jl - 1 >= j0 && jl - 1 < j1)
-          stg2(pdout + (long long)(jl - 1) * nt + gl, ITER ? pd1 : D2{0, 0});   // INIT: pd_{-1} = 0
-        // ---- (D) s(jl-2) = A pd, r_{i+1} = r_i - alpha s, x, w2 = D^-1 r_{i+1}
-        D2 rn2;
-        const D2 AEm2 = ld2(c2r + NL, tl);
-        const D2 AN3 = ld2(c3 + 2 * NL, tl);
-        const double ae2m = left_of(AEm2.r, c2r + NL, im, lcoef);
-        {
-          const D2 AP2 = ld2(c2r, tl);
-          const D2 AN2 = ld2(c2r + 2 * NL, tl);
-          D2 sv{AP2.l * pd2.l + ae2m * rleft(p_2, tl, NTC), AP2.r * pd2.r + AEm2.l * pd2.l};
-          sv.l += AEm2.l * pd2.r + AN3.l * pd3.l + AN2.l * pd1.l;
-          sv.r += AEm2.r * rright(p_2, tl) + AN3.r * pd3.r + AN2.r * pd1.r;
-          rn2 = {r2.l - alpha * sv.l, r2.r - alpha * sv.r};  // step 5 (INIT: alpha = 0)
-        }
-        if (out && jl - 2 >= j0 && jl - 2 < j1) {
-          const long long q2 = (long long)(jl - 2) * nt + gl;
-          stg2(rout + q2, rn2);
-          acc_rr += rn2.l * rn2.l + rn2.r * rn2.r;
-          if (XUPD) stg2(x + q2, D2{x2.l + (alpha_prev * pdo2.l + alpha * pd2.l),      // step 4
-                                    x2.r + (alpha_prev * pdo2.r + alpha * pd2.r)});
-          if (MODE == SR_INIT_COLD) { stg2(x + q2, D2{0, 0}); acc_s += r2.l * r2.l + r2.r * r2.r; }
-          if (MODE == SR_INIT_WARM) acc_s += x2.l * x2.l + x2.r * x2.r;   // x2 holds S here
-        }
-        D2 wz;
-        if constexpr (PC == SPC_NONE) wz = rn2;
-        else wz = {(rn2.l * oD2.l) * romega, (rn2.r * oD2.r) * romega};
-        rst(w2_2, tl, NTC, wz);
-        compute_bar(NCT);                                     // barrier 2: w2(jl-2) complete
-
-        // ---- (E) v2(jl-2)   (F) z2(jl-3), gamma   (G) A z2 at jl-4, delta
-        D2 u2_3;
-        if constexpr (PC == SPC_ASSOR2) {
-          const D2 w23 = rld(w2_3, tl, NTC);
-          const double wz2m = rleft(w2_2, tl, NTC);
-          const D2 v23 = rld(v2_3, tl, NTC);
-          const double v23p = rright(v2_3, tl);
-          const D2 AEm3 = ld2(c3 + NL, tl);
-          D2 sL{AN3.l * w23.l + ae2m * wz2m, AN3.r * w23.r + AEm2.l * wz.l};
-          if (seamWarp) {
-            if (seamL) sL.l -= ae2m * wz2m;
-            if (seamR) sL.r += AEm2.r * rright(w2_2, tl);
-          }
-          const D2 v22{wz.l - oD2.l * sL.l, wz.r - oD2.r * sL.r};
-          rst(v2_2, tl, NTC, v22);
-          D2 sU{AN3.l * v22.l + AEm3.l * v23.r, AN3.r * v22.r + AEm3.r * v23p};
-          if (seamWarp) {
-            if (seamL) sU.l += c3[NL + im] * rleft(v2_3, tl, NTC);
-            if (seamR) sU.r -= AEm3.r * v23p;
-          }
-          u2_3 = {c2 * (v23.l - oD3.l * sU.l), c2 * (v23.r - oD3.r * sU.r)};
-        } else {
-          u2_3 = rld(w2_3, tl, NTC);
-        }
-        u2_3r[tl] = u2_3.l;                                  // only the right-neighbour read (delta) remains
-        if (out && jl - 3 >= j0 && jl - 3 < j1) acc_g += rn3.l * u2_3.l + rn3.r * u2_3.r;   // gamma
-        {
-          // delta = z2' A z2 as the quadratic form (A symmetric): each owned row j adds its
-          // diagonal term and its east and north couplings, i.e. every edge once, at its
-          // west / south end -- no w = A z2 vector, one coefficient row (lag 4)
-          const D2 AP4 = ld2(c4, tl);
-          const D2 AEm4 = ld2(c4 + NL, tl);
-          const D2 AN4 = ld2(c4 + 2 * NL, tl);
-          if (out && jl - 4 >= j0 && jl - 4 < j1) {
-            const double ql = AP4.l * u2_4.l + 2.0 * (AEm4.l * u2_4.r + AN4.l * u2_3.l);
-            const double qr = AP4.r * u2_4.r + 2.0 * (AEm4.r * rright(u2_4r, tl) + AN4.r * u2_3.r);
-            acc_d += u2_4.l * ql + u2_4.r * qr;
-          }
-        }
-        __syncwarp();
-        if (lane0 && blk + u >= 4) mbar_arrive(emptyc0 + 8 * ((u + 4) & 7));   // coefficient row jl-4 done
-        // rotate the histories (register renaming across the unrolled steps)
-        u2_4 = u2_3;
-        rn3 = rn2;
-        pd3 = pd2; pd2 = pd1;
-        pdo2 = pdo1;
-        r2 = r1; r1 = r0;
-        oD3 = oD2; oD2 = oD1; oD1 = oD0;
-      }
-    }
+    const double alpha = ITER ? d.cs.alpha[q.k] : 0.0;
+    const double alpha_prev = ITER ? d.cs.uvk[q.k] : 0.0;   // uvk holds alpha_{i-1} here
+    const double beta = ITER ? d.cs.beta[q.k] : 0.0;
+    sr_compute<PC, MODE>(g, d, q, s, parity, alpha, alpha_prev, beta, st->omega, 0u, acc_rr, acc_g, acc_d, acc_s);
   }
 
   // ---- per-CTA partials, then the scalar stage (last CTA, fixed order)
   double v[4] = {acc_rr, acc_g, acc_d, acc_s};
   // the whole dynamic shared memory (48 NL doubles) is dead now: the reduction scratch needs
   // 4 (blockDim + 32) and 4 K doubles (the host keeps K <= 12 NL on this schedule)
-  sr_finish<ITER, INIT>(d, v, smem_raw, K, k, t.n_tiles, blockIdx.x / K, hcond, use_cond);
+  sr_finish<ITER, INIT>(d, v, smem_raw, K, q.k, t.n_tiles, blockIdx.x / K, hcond, use_cond, q.NCT / 32);
+}
+
+static int sr_pairs(const TileCfg& t) { return t.tw / 2 + SR_HALO; }
+// compute warps (column pairs rounded up to whole warps) + one TMA producer warp
+static int sr_threads(const TileCfg& t) { return ((sr_pairs(t) + 31) & ~31) + 32; }
+
+// ------------------------------------------------------------ persistent iteration kernel
+// k_srp runs ALL iterations of a solve in one launch (one CTA per tile, every CTA resident: a
+// cooperative launch).  Per iteration the CTA runs the same row pipeline as k_sr, then
+//   * its per-thread partials are reduced by a fixed warp-shuffle tree + warps in order,
+//   * thread 0 publishes them and arrives on a grid barrier (a monotonically increasing
+//     counter: release add, acquire spin),
+//   * EVERY CTA sums the per-CTA partials of every condition in CTA order (the same loads in the
+//     same order everywhere) and runs the scalar stage (Eq. 3.9, alpha, beta; R-A24, R-A32) on its
+//     own shared-memory copy of the solver state -- so every CTA holds bitwise the same scalars
+//     and no CTA waits for a serial last-CTA tail or a kernel boundary;
+//   * meanwhile the producer warp, released by the same grid barrier, already streams the first
+//     rows of the next iteration (their data does not depend on the scalars).
+// CTA 0 writes the state and the per-condition scalars back to global memory at exit.
+// One rank only (row slabs / condition sharding keep the per-launch kernels + exchange kernels).
+constexpr int kCtrGridBar = 14;   // d.counters slot of the grid barrier (zeroed before the launch)
+
+__host__ __device__ inline size_t srp_align(size_t x) { return (x + 15) & ~(size_t)15; }
+// extra dynamic shared memory after the rings: state copy, [4K] sums, [4][32] warp partials,
+// [4][nblk] per-CTA partials, 7 K doubles + 2 K ints of per-condition scalars, the ready flags
+__host__ __device__ inline size_t srp_extra_bytes(int K, int nblk) {
+  return srp_align(sizeof(SolverState)) + srp_align((size_t)4 * K * 8) + 4 * 32 * 8 + srp_align((size_t)4 * nblk * 8) +
+         srp_align((size_t)7 * K * 8) + srp_align((size_t)2 * K * 4) + 16 + 32;
+}
+__host__ __device__ inline size_t srp_smem_bytes(int nl, int K, int nblk) {
+  return srp_align(sr_smem_bytes(nl)) + srp_extra_bytes(K, nblk);
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(unsigned int* p, unsigned int v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+constexpr long long kGridBarTimeoutNs = 20000000000ll;   // 20 s: a CTA that never arrives fails the solve
+// spin until the grid barrier counter reaches target; false on timeout
+__device__ __forceinline__ bool grid_wait(const unsigned int* ctr, unsigned int target) {
+  if (ld_acquire_u32(ctr) >= target) return true;
+  const unsigned long long t0 = globaltimer();
+  while (ld_acquire_u32(ctr) < target)
+    if ((long long)(globaltimer() - t0) > kGridBarTimeoutNs) return false;
+  return true;
+}
+
+struct SrpShared {
+  SolverState* st;
+  double* red;      // [4K] per-condition sums [rr | gamma | delta | S.S]
+  double* wpart;    // [4][32] per-warp partials
+  double* pbuf;     // [4K][ncta] the per-CTA partials of one iteration
+  CondScalars cs;   // CTA-private per-condition scalars
+  volatile int* ready;   // [0]: iterations whose scalars are ready; [1]: failure flag
+  unsigned long long* tim;   // [4] CTA 0's timing accumulators
+};
+__device__ __forceinline__ SrpShared srp_shared(double* smem_raw, int NL, int K, int nblk) {
+  char* b = reinterpret_cast<char*>(smem_raw) + srp_align(sr_smem_bytes(NL));
+  SrpShared x;
+  x.st = reinterpret_cast<SolverState*>(b);
+  b += srp_align(sizeof(SolverState));
+  x.red = reinterpret_cast<double*>(b);
+  b += srp_align((size_t)4 * K * 8);
+  x.wpart = reinterpret_cast<double*>(b);
+  b += 4 * 32 * 8;
+  x.pbuf = reinterpret_cast<double*>(b);
+  b += srp_align((size_t)4 * nblk * 8);
+  double* a = reinterpret_cast<double*>(b);
+  x.cs.alpha = a; x.cs.beta = a + K; x.cs.dk = a + 2 * K; x.cs.Sk = a + 3 * K; x.cs.rrk = a + 4 * K;
+  x.cs.uvk = a + 5 * K; x.cs.ttk = a + 6 * K;
+  b += srp_align((size_t)7 * K * 8);
+  x.cs.itk = reinterpret_cast<int32_t*>(b); x.cs.frz = x.cs.itk + K;
+  b += srp_align((size_t)2 * K * 4);
+  x.ready = reinterpret_cast<volatile int*>(b);
+  x.tim = reinterpret_cast<unsigned long long*>(b + 16);
+  return x;
+}
+
+template <int PC>
+__global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K) {
+  extern __shared__ __align__(128) double smem_raw[];
+  if (d.st_->done) return;                   // the init already converged (or failed)
+  const SrGeo q = sr_geo(g, d, t, K);
+  const SrSmem s = sr_smem(smem_raw, q.NL);
+  const SrpShared x = srp_shared(smem_raw, q.NL, K, (int)gridDim.x);
+  sr_init_barriers(q, s);
+  // CTA-private copies of the solver state and of the per-condition scalars
+  for (int i = q.tid; i < K; i += blockDim.x) {
+    x.cs.alpha[i] = d.cs.alpha[i]; x.cs.beta[i] = d.cs.beta[i]; x.cs.dk[i] = d.cs.dk[i];
+    x.cs.Sk[i] = d.cs.Sk[i]; x.cs.rrk[i] = d.cs.rrk[i]; x.cs.uvk[i] = d.cs.uvk[i]; x.cs.ttk[i] = d.cs.ttk[i];
+    x.cs.itk[i] = d.cs.itk[i]; x.cs.frz[i] = d.cs.frz[i];
+  }
+  if (q.tid == 0) { *x.st = *d.st_; x.ready[0] = 0; x.ready[1] = 0; }
+  __syncthreads();
+  const int it0 = x.st->iter;                // iteration count at entry (0 after the init)
+  const bool async = x.st->coupling == 2;
+  const int nblk = gridDim.x, ncta = t.n_tiles, cta = blockIdx.x / K;
+  unsigned int* gbar = d.counters + kCtrGridBar;
+  uint32_t gstep = 0;                        // row steps this CTA streamed / consumed so far
+
+  if (q.is_producer) {
+    // ------------------------------------------------ producer: stream every iteration
+    const int lane = q.tid - q.NCT;
+    for (int it = 0;; ++it) {
+      const int parity = (it0 + it) & 1;
+      int pre = 0;
+      if (it > 0) {
+        // the rows of iteration it were written by all CTAs in iteration it-1
+        bool ok = true;
+        if (lane == 0) ok = grid_wait(gbar, (unsigned)(it * nblk));
+        ok = __shfl_sync(0xffffffffu, ok, 0);
+        if (!ok) break;
+        fence_proxy_async_global();          // generic-proxy stores -> TMA (async-proxy) reads
+        if (!async) {                        // prefetch 4 steps while the scalars are computed
+          pre = 4;
+          if (parity) sr_produce<SR_ITER_ODD>(g, d, q, s, K, 1, gstep, 0, pre);
+          else sr_produce<SR_ITER_EVEN>(g, d, q, s, K, 0, gstep, 0, pre);
+        }
+        while (x.ready[0] < it && x.ready[1] == 0) __nanosleep(32);
+      }
+      __syncwarp();
+      const bool stop = x.ready[1] != 0 || x.st->done;
+      if (stop) {
+        // drain the prefetched steps (TMA writes into this CTA's shared memory) before exiting
+        if (lane == 0)
+          for (int b = 0; b < pre; ++b) mbar_wait(s.full0 + 8 * ((gstep + b) & 7), (gstep / SR_UNROLL) & 1u);
+        break;
+      }
+      if (async && x.cs.frz[q.k]) continue;  // frozen condition: no rows this iteration
+      if (parity) sr_produce<SR_ITER_ODD>(g, d, q, s, K, 1, gstep, pre, q.nsteps);
+      else sr_produce<SR_ITER_EVEN>(g, d, q, s, K, 0, gstep, pre, q.nsteps);
+      gstep += (uint32_t)q.nsteps;
+    }
+    return;
+  }
+
+  // ------------------------------------------------------ compute warps
+  const int NCT = q.NCT, nw = NCT >> 5;
+  const bool timed = blockIdx.x == 0 && q.tid == 0;
+  // CTA 0's timing accumulators live in shared memory (registers are the hot loop's)
+  volatile unsigned long long* tim = x.tim;   // [0] start, [1] tail, [2] wait, [3] arrival
+  if (timed) { tim[0] = globaltimer(); tim[1] = 0ull; tim[2] = 0ull; }
+  const double omega = x.st->omega;
+  for (int it = 0;; ++it) {
+    const int parity = (it0 + it) & 1;
+    double a_rr = 0.0, a_g = 0.0, a_d = 0.0, a_s = 0.0;
+    if (!(async && x.cs.frz[q.k])) {
+      const double alpha = x.cs.alpha[q.k], alpha_prev = x.cs.uvk[q.k], beta = x.cs.beta[q.k];
+      if (parity) sr_compute<PC, SR_ITER_ODD>(g, d, q, s, 1, alpha, alpha_prev, beta, omega, gstep, a_rr, a_g, a_d, a_s);
+      else sr_compute<PC, SR_ITER_EVEN>(g, d, q, s, 0, alpha, alpha_prev, beta, omega, gstep, a_rr, a_g, a_d, a_s);
+      gstep += (uint32_t)q.nsteps;
+    }
+    // field stores of this iteration -> visible to the other CTAs' TMA reads after the barrier
+    fence_proxy_async_global();
+    __threadfence();
+    // fixed-order block reduction (the same as k_sr's, so both give bitwise the same partials)
+    double v[3] = {a_rr, a_g, a_d};
+    warp_tree_sum<3>(v, x.wpart);
+    compute_bar(NCT);
+    const unsigned int target = (unsigned)((it + 1) * nblk);
+    double* part = d.partials + (size_t)(it & 1) * 4 * K * ncta;   // parity buffers
+    if (q.tid == 0) {
+      if (timed) tim[3] = globaltimer();
+      warps_in_order<3>(v, x.wpart, nw);
+      for (int c = 0; c < 3; ++c) part[(size_t)(c * K + q.k) * ncta + cta] = v[c];
+      part[(size_t)(3 * K + q.k) * ncta + cta] = 0.0;
+      __threadfence();
+      red_release_add(gbar, 1u);
+      if (!grid_wait(gbar, target)) x.ready[1] = 1;
+      __threadfence();
+    }
+    compute_bar(NCT);
+    if (x.ready[1]) break;
+    const unsigned long long t_bar = timed ? globaltimer() : 0ull;
+    if (timed) tim[2] = tim[2] + (t_bar - tim[3]);
+    // per-condition sums over the CTAs in CTA order (identical in every CTA): every partial is
+    // loaded at once (one L2 round trip), then each (q, k) row is summed in CTA order
+    {
+      const int np = 4 * K * ncta;
+#pragma unroll 4
+      for (int i = q.tid; i < np; i += NCT) x.pbuf[i] = __ldcg(part + i);
+    }
+    compute_bar(NCT);
+    for (int i = q.tid; i < 4 * K; i += NCT) {
+      const double* src = x.pbuf + (size_t)i * ncta;
+      double a = 0.0;
+      for (int b = 0; b < ncta; ++b) a += src[b];
+      x.red[i] = a;
+    }
+    compute_bar(NCT);
+    if (q.tid == 0) {
+      sr_scalar_stage<false>(x.cs, x.st, x.red, K, K, 0, 0, 0ull, stage_prefetch(x.cs, x.st));
+      __threadfence_block();
+      x.ready[0] = it + 1;                  // the producer may go on (or stop)
+    }
+    compute_bar(NCT);
+    if (timed) tim[1] = tim[1] + (globaltimer() - t_bar);
+    if (x.st->done) break;
+  }
+  // CTA 0 writes the solver state and the per-condition scalars back
+  if (blockIdx.x == 0) {
+    for (int i = q.tid; i < K; i += NCT) {
+      d.cs.alpha[i] = x.cs.alpha[i]; d.cs.beta[i] = x.cs.beta[i]; d.cs.dk[i] = x.cs.dk[i];
+      d.cs.Sk[i] = x.cs.Sk[i]; d.cs.rrk[i] = x.cs.rrk[i]; d.cs.uvk[i] = x.cs.uvk[i];
+      d.cs.itk[i] = x.cs.itk[i]; d.cs.frz[i] = x.cs.frz[i];
+    }
+    if (q.tid == 0) {
+      SolverState st = *x.st;
+      if (x.ready[1]) { st.done = 1; st.status = -9; }   // GMAF_E_CUDA: grid barrier timeout
+      *d.st_ = st;
+      const unsigned long long t1 = globaltimer();
+      const int iters = st.iter - it0;
+      atomicAdd(&d.timing->total_ns[KK_SR_ITER], t1 - tim[0]);
+      atomicAdd(&d.timing->launches[KK_SR_ITER], (unsigned long long)(iters > 0 ? iters : 0));
+      atomicAdd(&d.timing->total_ns[KK_SR_TAIL], (unsigned long long)tim[1]);
+      atomicAdd(&d.timing->launches[KK_SR_TAIL], (unsigned long long)(iters > 0 ? iters : 0));
+      atomicAdd(&d.timing->total_ns[KK_SR_WAIT], (unsigned long long)tim[2]);
+      atomicAdd(&d.timing->launches[KK_SR_WAIT], (unsigned long long)(iters > 0 ? iters : 0));
+    }
+  }
+}
+
+cudaError_t launch_sr_persistent(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,
+                                 cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(d.counters + kCtrGridBar, 0, sizeof(unsigned int), s);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(t.n_tiles * K);
+  cfg.blockDim = dim3(sr_threads(t));
+  cfg.dynamicSmemBytes = srp_smem_bytes(2 * sr_pairs(t), K, t.n_tiles * K);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;   // every CTA resident (the grid barrier needs it)
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  switch (precond) {
+    case SPC_ASSOR2: return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2>, g, d, t, K);
+    case SPC_ASSOR1: return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR1>, g, d, t, K);
+    case SPC_JACOBI: return cudaLaunchKernelEx(&cfg, k_srp<SPC_JACOBI>, g, d, t, K);
+    default: return cudaLaunchKernelEx(&cfg, k_srp<SPC_NONE>, g, d, t, K);
+  }
+}
+
+// resident CTAs per SM of the persistent kernel with K conditions (0: it does not fit)
+int srp_ctas_per_sm(const TileCfg& t, int K) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_srp<SPC_ASSOR2>, sr_threads(t),
+                                                    srp_smem_bytes(2 * sr_pairs(t), K, t.n_tiles * K)) != cudaSuccess)
+    return 0;
+  return n;
 }
 
 // Multi-rank scalar stage: one CTA, after the allgather of every rank's packed sums
@@ -427,9 +743,6 @@ __global__ void k_sr_fixup(GridParams g, DevPtrs d, int K) {   // K = local cond
 }
 
 // --------------------------------------------------------------------- launchers
-static int sr_pairs(const TileCfg& t) { return t.tw / 2 + SR_HALO; }
-// compute warps (column pairs rounded up to whole warps) + one TMA producer warp
-static int sr_threads(const TileCfg& t) { return ((sr_pairs(t) + 31) & ~31) + 32; }
 
 template <typename KernelT>
 static cudaError_t sr_launch(KernelT kern, const GridParams& g, const DevPtrs& d, const TileCfg& t, int K,
@@ -671,8 +984,8 @@ cudaError_t launch_sr_scalar(const DevPtrs& d, bool init, int Kglob, int Klocal,
 }
 
 template <typename KernelT>
-static cudaError_t sr_set(KernelT kern, int bytes) {
-  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+static cudaError_t sr_set(KernelT kern, int) {
+  return raise_smem_cap(kern);
 }
 
 template <int MODE>
@@ -684,13 +997,35 @@ static cudaError_t sr_set_modes(int bytes) {
   return e;
 }
 
-cudaError_t configure_sr_kernels(const TileCfg& t) {
-  const int bytes = (int)sr_smem_bytes(2 * sr_pairs(t));
-  cudaError_t e = sr_set_modes<SR_ITER_EVEN>(bytes);
-  if (e == cudaSuccess) e = sr_set_modes<SR_ITER_ODD>(bytes);
-  if (e == cudaSuccess) e = sr_set_modes<SR_INIT_COLD>(bytes);
-  if (e == cudaSuccess) e = sr_set_modes<SR_INIT_WARM>(bytes);
+// The dynamic shared-memory cap is a process-wide attribute of each kernel while the sizes differ
+// per context (strip width, K): every kernel is raised once to the device's opt-in maximum (the
+// cap only bounds a launch; occupancy follows the bytes actually requested), so a context created
+// later can never lower the cap under an earlier one.  Fails if this context needs
+// more than the device offers.
+cudaError_t configure_sr_kernels(const TileCfg& t, int K) {
+  const int cap = smem_optin_max();
+  if (cap <= 0) return cudaErrorInvalidValue;
+  if ((long long)sr_smem_bytes(2 * sr_pairs(t)) > cap - 1024) return cudaErrorInvalidValue;
+  static unsigned done = 0u;   // host-side, once per device (the attribute is process-global)
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cudaErrorInvalidValue;
+  if (done & (1u << dev)) return cudaSuccess;
+  cudaError_t e = sr_set_modes<SR_ITER_EVEN>(cap);
+  if (e == cudaSuccess) e = sr_set_modes<SR_ITER_ODD>(cap);
+  if (e == cudaSuccess) e = sr_set_modes<SR_INIT_COLD>(cap);
+  if (e == cudaSuccess) e = sr_set_modes<SR_INIT_WARM>(cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR1>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_JACOBI>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_NONE>, cap);
+  (void)K;
+  if (e == cudaSuccess) done |= 1u << dev;
   return e;
+}
+
+// whether the persistent kernel fits this context (its extra shared memory grows with K)
+bool srp_fits(const TileCfg& t, int K) {
+  return (long long)srp_smem_bytes(2 * sr_pairs(t), K, t.n_tiles * K) <= smem_optin_max() - 1024;
 }
 
 int sr_ctas_per_sm(const TileCfg& t) {

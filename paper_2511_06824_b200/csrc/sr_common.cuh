@@ -59,6 +59,12 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 __device__ __forceinline__ void compute_bar(int nthreads) {
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
+// timing-only experiment (wrong results): the row pipeline's two barriers per row compiled out
+#ifdef GMAF_EXPERIMENT_NOBAR
+__device__ __forceinline__ void row_bar(int) { __syncwarp(); }
+#else
+__device__ __forceinline__ void row_bar(int nthreads) { compute_bar(nthreads); }
+#endif
 // 1/a to full double precision without the IEEE-division slow path: rcp.approx (MUFU)
 // + one third-order Newton step (the solve does not need a correctly rounded D^-1).
 __device__ __forceinline__ double fast_rcp(double a) {
@@ -97,14 +103,13 @@ __device__ __forceinline__ void stg2(double* p, D2 v) {   // 16-byte global stor
 // Table-1 scalars from the per-condition sums (fixed k order): convergence test (Eq. 3.9),
 // alpha/beta of the single-reduction recurrence (coupled: global; lockstep: per condition).
 // red = [rr | gamma | delta | S.S] x Kall.  Local conditions kofs .. kofs+Klocal-1 receive their
-// alpha/beta in d.cs (indexed locally).  One thread.
+// alpha/beta in cs (indexed locally).  One thread.
 // Asynchronous strategy (Eq. 3.10): every condition is its own Krylov process
 // (per-condition alpha_k, beta_k) frozen at its own test ||r_k||/||S_k|| <= tol; the solve ends
 // when all are frozen.  A frozen condition's CTAs no longer stream or compute (device mask, no
 // host round trip -- the cost the paper's implementation paid).  One rank (Kall == Klocal).
 template <bool INIT>
-__device__ void sr_scalar_async(const DevPtrs& d, const double* red, int K) {
-  SolverState* st = d.st_;
+__device__ void sr_scalar_async(const CondScalars& cs, SolverState* st, const double* red, int K) {
   const double* rrk = red;
   const double* gk = red + K;
   const double* dk = red + 2 * K;
@@ -116,23 +121,23 @@ __device__ void sr_scalar_async(const DevPtrs& d, const double* red, int K) {
     st->nS = sqrt(SS);
     st->iter = 0; st->status = 0; st->converged = 0; st->done = 0; st->zero_p = (st->nS == 0.0);
     for (int k = 0; k < K; ++k) {
-      d.cs.Sk[k] = ssk[k]; d.cs.rrk[k] = rrk[k]; d.cs.itk[k] = 0;
+      cs.Sk[k] = ssk[k]; cs.rrk[k] = rrk[k]; cs.itk[k] = 0;
       const double relk = ssk[k] > 0.0 ? sqrt(rrk[k]) / sqrt(ssk[k]) : 0.0;
-      d.cs.frz[k] = (ssk[k] == 0.0 || relk <= st->tol) ? 1 : 0;
+      cs.frz[k] = (ssk[k] == 0.0 || relk <= st->tol) ? 1 : 0;
       double a0 = 0.0;
-      if (!d.cs.frz[k] && gk[k] != 0.0) { if (!(dk[k] > 0.0)) bad = true; a0 = gk[k] / dk[k]; }
-      d.cs.alpha[k] = a0; d.cs.beta[k] = 0.0; d.cs.uvk[k] = 0.0; d.cs.dk[k] = gk[k];
+      if (!cs.frz[k] && gk[k] != 0.0) { if (!(dk[k] > 0.0)) bad = true; a0 = gk[k] / dk[k]; }
+      cs.alpha[k] = a0; cs.beta[k] = 0.0; cs.uvk[k] = 0.0; cs.dk[k] = gk[k];
     }
   } else {
     st->iter += 1;
     for (int k = 0; k < K; ++k) {
-      if (d.cs.frz[k]) continue;
-      d.cs.itk[k] += 1;
-      d.cs.rrk[k] = rrk[k];
-      d.cs.uvk[k] = d.cs.alpha[k];                       // alpha used this iteration
-      const double relk = d.cs.Sk[k] > 0.0 ? sqrt(rrk[k]) / sqrt(d.cs.Sk[k]) : 0.0;
-      if (relk <= st->tol) { d.cs.frz[k] = 1; continue; }
-      const double aold = d.cs.alpha[k], gold = d.cs.dk[k];
+      if (cs.frz[k]) continue;
+      cs.itk[k] += 1;
+      cs.rrk[k] = rrk[k];
+      cs.uvk[k] = cs.alpha[k];                       // alpha used this iteration
+      const double relk = cs.Sk[k] > 0.0 ? sqrt(rrk[k]) / sqrt(cs.Sk[k]) : 0.0;
+      if (relk <= st->tol) { cs.frz[k] = 1; continue; }
+      const double aold = cs.alpha[k], gold = cs.dk[k];
       double a = 0.0, b = 0.0;
       if (gold != 0.0 && aold != 0.0) {
         if (gk[k] < 0.0) bad = true;
@@ -142,12 +147,12 @@ __device__ void sr_scalar_async(const DevPtrs& d, const double* red, int K) {
         else if (dk[k] > 0.0) { b = 0.0; a = gk[k] / dk[k]; }   // restart (R-A32)
         else bad = true;
       }
-      d.cs.alpha[k] = a; d.cs.beta[k] = b; d.cs.dk[k] = gk[k];
+      cs.alpha[k] = a; cs.beta[k] = b; cs.dk[k] = gk[k];
     }
   }
   double rr = 0.0;
   int live = 0;
-  for (int k = 0; k < K; ++k) { rr += d.cs.rrk[k]; live += d.cs.frz[k] ? 0 : 1; }
+  for (int k = 0; k < K; ++k) { rr += cs.rrk[k]; live += cs.frz[k] ? 0 : 1; }
   st->rel = st->nS > 0.0 ? sqrt(rr) / st->nS : 0.0;
   if (live == 0) { st->done = 1; st->converged = 1; }
   else if (st->iter >= st->max_iter) { st->done = 1; st->status = -6; }
@@ -157,28 +162,30 @@ __device__ void sr_scalar_async(const DevPtrs& d, const double* red, int K) {
 // Solver-state snapshot for the scalar stage, loaded early (overlapped with the partial-sum loads
 // of the serial tail): the stage itself then makes no dependent global round trip.
 struct StageIn { SolverState s; double aold0; };
-__device__ __forceinline__ StageIn stage_prefetch(const DevPtrs& d) {
+__device__ __forceinline__ StageIn stage_prefetch(const CondScalars& cs, const SolverState* st) {
   StageIn in;
-  in.s = *d.st_;
-  in.aold0 = d.cs.alpha[0];
+  in.s = *st;
+  in.aold0 = cs.alpha[0];
   return in;
 }
+__device__ __forceinline__ StageIn stage_prefetch(const DevPtrs& d) { return stage_prefetch(d.cs, d.st_); }
 
-// Executed by ONE WARP (all 32 lanes; red in shared memory is read by broadcast): every lane
-// evaluates the scalars redundantly -- the same arithmetic in the same order, so all agree -- and
-// the per-condition arrays are written lane-parallel (one store instruction for up to 32
-// conditions instead of a serial chain of single-thread stores on the iteration's critical path);
-// lane 0 writes the state back.
+// Executed by ONE THREAD on the critical path of every iteration (a warp-parallel version, with
+// lanes evaluating the scalars redundantly and storing the per-condition arrays lane-parallel,
+// was reverted: lanes read alpha[0] and the state while lane 0 was writing them, which corrupted
+// the lockstep scalars for K = 2, 3 -- DESIGN.md sec. 9).  cs / st are the per-condition arrays
+// and the solver state: global memory (d.cs, d.st_) for the per-launch kernels, CTA-private
+// shared-memory copies in the persistent kernel.
 template <bool INIT>
-__device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, int Klocal, int kofs,
-                                int use_cond, unsigned long long hcond, const StageIn& in) {
+__device__ void sr_scalar_stage(const CondScalars& cs, SolverState* st, const double* red, int Kall, int Klocal,
+                                int kofs, int use_cond, unsigned long long hcond, const StageIn& in) {
   // one thread on the critical path of every iteration: work on the register snapshot, write the
   // state back once
   SolverState s = in.s;
   const double aold0 = in.aold0;
   if (s.coupling == 2) {
-    sr_scalar_async<INIT>(d, red, Kall);
-    if (use_cond && d.st_->done) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, 0u);
+    sr_scalar_async<INIT>(cs, st, red, Kall);
+    if (use_cond && st->done) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, 0u);
     return;
   }
   const double* rrk = red;
@@ -187,12 +194,12 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
   const double* ssk = red + 3 * Kall;
   double rr = 0.0;
   for (int kk = 0; kk < Kall; ++kk) rr += rrk[kk];
-  for (int kl = 0; kl < Klocal; ++kl) d.cs.rrk[kl] = rrk[kofs + kl];
+  for (int kl = 0; kl < Klocal; ++kl) cs.rrk[kl] = rrk[kofs + kl];
   bool bad = false;
   if (INIT) {
     double SS = 0.0;
     for (int kk = 0; kk < Kall; ++kk) SS += ssk[kk];
-    for (int kl = 0; kl < Klocal; ++kl) d.cs.Sk[kl] = ssk[kofs + kl];
+    for (int kl = 0; kl < Klocal; ++kl) cs.Sk[kl] = ssk[kofs + kl];
     s.nS = sqrt(SS);
     s.iter = 0; s.status = 0; s.converged = 0; s.done = 0; s.zero_p = 0;
     if (s.nS == 0.0) {
@@ -208,15 +215,15 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
         for (int kk = 0; kk < Kall; ++kk) { gg += gk[kk]; dd += dk[kk]; }
         if (!(dd > 0.0)) bad = true;
         const double a0 = gg / dd;
-        for (int kl = 0; kl < Klocal; ++kl) { d.cs.alpha[kl] = a0; d.cs.beta[kl] = 0.0; d.cs.uvk[kl] = 0.0; }
+        for (int kl = 0; kl < Klocal; ++kl) { cs.alpha[kl] = a0; cs.beta[kl] = 0.0; cs.uvk[kl] = 0.0; }
         s.d = gg;
       } else {
         for (int kk = 0; kk < Kall; ++kk)
           if (gk[kk] != 0.0 && !(dk[kk] > 0.0)) bad = true;
         for (int kl = 0; kl < Klocal; ++kl) {
           const int kk = kofs + kl;
-          d.cs.alpha[kl] = gk[kk] != 0.0 ? gk[kk] / dk[kk] : 0.0;
-          d.cs.beta[kl] = 0.0; d.cs.uvk[kl] = 0.0; d.cs.dk[kl] = gk[kk];
+          cs.alpha[kl] = gk[kk] != 0.0 ? gk[kk] / dk[kk] : 0.0;
+          cs.beta[kl] = 0.0; cs.uvk[kl] = 0.0; cs.dk[kl] = gk[kk];
         }
       }
       if (bad) { s.done = 1; s.status = -5; }
@@ -244,15 +251,15 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
         else if (den > 0.0) a = g2 / den;
         else if (d2 > 0.0) { b = 0.0; a = g2 / d2; }
         else bad = true;
-        for (int kl = 0; kl < Klocal; ++kl) { d.cs.uvk[kl] = aold0; d.cs.alpha[kl] = a; d.cs.beta[kl] = b; }
+        for (int kl = 0; kl < Klocal; ++kl) { cs.uvk[kl] = aold0; cs.alpha[kl] = a; cs.beta[kl] = b; }
         s.d = g2;
       } else {
         for (int kk = 0; kk < Kall; ++kk)
           if (gk[kk] < 0.0) bad = true;
         for (int kl = 0; kl < Klocal; ++kl) {
           const int kk = kofs + kl;
-          const double aold = d.cs.alpha[kl], gold = d.cs.dk[kl];
-          d.cs.uvk[kl] = aold;                                   // alpha used this iteration
+          const double aold = cs.alpha[kl], gold = cs.dk[kl];
+          cs.uvk[kl] = aold;                                   // alpha used this iteration
           double a = 0.0, b = 0.0;
           if (gold != 0.0 && aold != 0.0) {
             b = gk[kk] / gold;
@@ -261,23 +268,28 @@ __device__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, i
             else if (dk[kk] > 0.0) { b = 0.0; a = gk[kk] / dk[kk]; }   // restart (R-A32)
             else bad = true;
           }
-          d.cs.alpha[kl] = a; d.cs.beta[kl] = b; d.cs.dk[kl] = gk[kk];
+          cs.alpha[kl] = a; cs.beta[kl] = b; cs.dk[kl] = gk[kk];
         }
       }
       if (bad && !s.done) { s.done = 1; s.status = -5; }
     } else {
-      for (int kl = 0; kl < Klocal; ++kl) d.cs.uvk[kl] = d.cs.alpha[kl];   // alpha used this iteration
+      for (int kl = 0; kl < Klocal; ++kl) cs.uvk[kl] = cs.alpha[kl];   // alpha used this iteration
     }
   }
-  *d.st_ = s;
+  *st = s;
   // the WHILE handle defaults to 1 at every graph launch: write it only to stop the loop
   if (use_cond && s.done) cudaGraphSetConditional((cudaGraphConditionalHandle)hcond, 0u);
 }
 
 template <bool INIT>
 __device__ __forceinline__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, int Klocal,
+                                                int kofs, int use_cond, unsigned long long hcond, const StageIn& in) {
+  sr_scalar_stage<INIT>(d.cs, d.st_, red, Kall, Klocal, kofs, use_cond, hcond, in);
+}
+template <bool INIT>
+__device__ __forceinline__ void sr_scalar_stage(const DevPtrs& d, const double* red, int Kall, int Klocal,
                                                 int kofs, int use_cond, unsigned long long hcond) {
-  sr_scalar_stage<INIT>(d, red, Kall, Klocal, kofs, use_cond, hcond, stage_prefetch(d));
+  sr_scalar_stage<INIT>(d.cs, d.st_, red, Kall, Klocal, kofs, use_cond, hcond, stage_prefetch(d));
 }
 
 
@@ -329,6 +341,11 @@ __device__ __forceinline__ bool p2p_gather(const DistPtrs& dd, const double* src
       if ((long long)(globaltimer() - t0) > kP2PTimeoutNs) { ok = false; break; }
     }
   }
+  // lane x reads every rank's block, but only lane r acquired rank r's stamp: the warp barrier
+  // (bar.warp.sync orders memory among its lanes) plus a system-scope acquire-release fence by
+  // every lane orders all the data reads below after all the stamp acquires
+  __syncwarp();
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
   if (!__all_sync(0xffffffffu, ok)) return false;
   const volatile double* data = reinterpret_cast<const volatile double*>(dd.peer[dd.rank] + 2 * W * 8);
   for (int i = lane; i < W * n; i += 32) {
@@ -339,14 +356,43 @@ __device__ __forceinline__ bool p2p_gather(const DistPtrs& dd, const double* src
   return true;
 }
 
+// Fixed-order CTA sum of NV per-thread values over the first nw warps (the compute warps): an
+// xor butterfly in every warp (every lane ends with bitwise the same warp sum: each level adds
+// the same two partial sums), lane 0 parks it in wbuf[q*32 + warp], then thread 0 adds the warps
+// in order.  The per-launch k_sr and the persistent k_srp both use it, so their per-CTA partials
+// -- and hence their scalars -- are bitwise identical.  Warps >= nw must not call it; the caller
+// separates the wbuf write from the read with a barrier over the nw warps.
+template <int NV>
+__device__ __forceinline__ void warp_tree_sum(double (&v)[NV], double* wbuf) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1)
+#pragma unroll
+    for (int c = 0; c < NV; ++c) v[c] += __shfl_xor_sync(0xffffffffu, v[c], m);
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int c = 0; c < NV; ++c) wbuf[c * 32 + (threadIdx.x >> 5)] = v[c];
+}
+template <int NV>
+__device__ __forceinline__ void warps_in_order(double (&v)[NV], const double* wbuf, int nw) {
+#pragma unroll
+  for (int c = 0; c < NV; ++c) {
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += wbuf[c * 32 + w];
+    v[c] = s;
+  }
+}
+
 // Per-CTA partials -> fixed-order per-condition sums in the last CTA -> the scalar stage
 // (multi-rank: the packed sums for the allgather).  Every thread of the CTA calls it; `red`
 // is dead shared memory of >= max(4 * (blockDim + 32), 4 * K) doubles.
 template <bool ITER, bool INIT>
 __device__ void sr_finish(const DevPtrs& d, double (&v)[4], double* red, int K, int k, int ncta, int cta,
-                          unsigned long long hcond, int use_cond) {
+                          unsigned long long hcond, int use_cond, int ncompute_warps) {
   const int tid = threadIdx.x;
-  block_sum<4>(v, red);
+  __syncthreads();                                   // the rings are dead: red may alias them
+  if ((tid >> 5) < ncompute_warps) warp_tree_sum<4>(v, red);
+  __syncthreads();
+  if (tid == 0) warps_in_order<4>(v, red, ncompute_warps);
   if (tid == 0) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) d.partials[(long long)(q * K + k) * ncta + cta] = v[q];

@@ -62,7 +62,19 @@ def aggregate(device_ms: float, wall_ms: float, dof_iters: float, group=None, de
 def connect_p2p(solver, group=None) -> None:
     """Exchange the solvers' CUDA IPC handles over torch.distributed (any backend, e.g. gloo) and
     connect the peer-to-peer context (include/gmaf.h gmaf_p2p_handle / gmaf_p2p_connect)."""
+    import torch
     import torch.distributed as dist
+    # every rank's GPU must be peer-accessible from this one (the exchange kernels load and store
+    # the peers' buffers over NVLink); fail loudly before connecting otherwise
+    devs = [None] * solver.world
+    dist.all_gather_object(devs, (torch.cuda.get_device_properties(solver.device).uuid.hex
+                                  if hasattr(torch.cuda.get_device_properties(solver.device), "uuid") else None,
+                                  solver.device.index), group=group)
+    mine = solver.device.index
+    for r, (_, d) in enumerate(devs):
+        if d is not None and d != mine and not torch.cuda.can_device_access_peer(mine, d):
+            raise RuntimeError(f"rank {solver.rank}: GPU {mine} cannot access rank {r}'s GPU {d} peer to peer "
+                               "(NVLink/P2P required by the peer-to-peer exchange)")
     handles = [None] * solver.world
     dist.all_gather_object(handles, solver.p2p_handle(), group=group)
     solver.p2p_connect(handles)

@@ -202,6 +202,29 @@ def test_matrix_dedup(P, orc, gi):
     S.close()
 
 
+def test_band_storage_sized_by_distinct_matrices(P, orc, gi):
+    """Bands are stored once per distinct (e, L_F) (Eq. 2.3 has no e-dot): a workspace sized for 5
+    coefficient sets runs the 9 FD conditions of one state bitwise like a full-size one, and refuses
+    (GMAF_E_WORKSPACE at thickness, nothing downstream) 9 conditions with 9 distinct e."""
+    g = gi.grid(96, 40, "short", tex_n_theta=8, tex_n_y=2, tex_band_rows=8)
+    conds = gi.fd_conditions(gi.condition())
+    full = P.gmaf_workspace_bytes(P.make_grid(g), 9)
+    small = P.gmaf_workspace_bytes_m(P.make_grid(g), 9, 5)
+    assert small == full - 4 * 3 * 96 * 40 * 8
+    S5 = P.JointSolver(g, 9, max_matrices=5)
+    st5, W5 = S5.step(conds, omega=1.6)
+    S9 = P.JointSolver(g, 9)
+    st9, W9 = S9.step(conds, omega=1.6)
+    assert st5.iterations == st9.iterations and np.array_equal(W5, W9)
+    with pytest.raises(P.GmafError) as ei:
+        S5.thickness(gi.random_conditions(3, 9))
+    assert ei.value.code == -8
+    with pytest.raises(P.GmafError):
+        S5.assemble()
+    S5.close()
+    S9.close()
+
+
 def test_c2_parity(P, orc, gi):
     cfg = gi.config("C2")
     st, ref = full_parity(P, orc, cfg.grid, cfg.conds, cfg.omega)
@@ -271,7 +294,7 @@ def test_c5_full_size_lockstep_iterates(P, orc, gi):
     cfg = gi.config("C5")
     K = cfg.conds.shape[0]
     assert K == 72
-    S = P.JointSolver(cfg.grid, K)
+    S = P.JointSolver(cfg.grid, K, max_matrices=40)    # 8 operating points x 5 distinct (e, L_F)
     S.thickness(cfg.conds)
     S.assemble()
     st = S.solve(tol=1e-30, omega=cfg.omega, coupling="lockstep", max_iter=3, raise_on_error=False)
@@ -527,3 +550,51 @@ def test_random_meshes_and_textures(P, orc, gi, case):
     g = gi.grid(nt, ny, tex, **over)
     conds = gi.random_conditions(s % 1000, K)
     full_parity(P, orc, g, conds, 1.6 if tex == "short" else 1.8)
+
+
+PERSIST_CASES = {
+    "c2": ("C2", {}),
+    "ragged_textured": (None, {}),
+    "lockstep": ("C2", {"coupling": "lockstep"}),
+    "async": (None, {"coupling": "async"}),
+    "jacobi": (None, {"precond": "jacobi"}),
+    "assor1": (None, {"precond": "assor1"}),
+}
+
+
+@pytest.mark.parametrize("case", sorted(PERSIST_CASES))
+def test_persistent_equals_per_launch_kernels(P, gi, monkeypatch, case):
+    """The persistent solve (sr.cu k_srp: all iterations in one cooperative launch, a grid barrier
+    and a redundant scalar stage per iteration) runs the same row pipeline, the same fixed-order
+    block reduction, the same CTA-order sums and the same scalar stage as the per-iteration
+    kernels of the graph's WHILE loop: the two are bitwise identical."""
+    name, kw = PERSIST_CASES[case]
+    if name:
+        cfg = gi.config(name)
+        g, conds, omega = cfg.grid, cfg.conds, cfg.omega
+    else:
+        g = gi.grid(300, 70, "short", tex_n_theta=30, tex_n_y=3, tex_band_rows=20)
+        conds, omega = gi.random_conditions(11, 9), 1.6
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("GMAF_PERSIST", mode)
+        S = P.JointSolver(g, len(conds))
+        assert S.tile_config()["persistent"] == (mode == "1")
+        S.thickness(conds)
+        S.assemble()
+        S.solve(tol=1e-30, omega=omega, max_iter=7, raise_on_error=False, **kw)
+        p7 = np.stack([S.get("p", k) for k in range(len(conds))])
+        st = S.solve(tol=1e-10, omega=omega, **kw)
+        p = np.stack([S.get("p", k) for k in range(len(conds))])
+        its = S.cond_iterations()
+        fx = S.solve_fixed(9, omega=omega, precond=kw.get("precond", "assor2"))
+        out[mode] = (p7, st, p, its, fx, S.integrate())
+        S.close()
+    (p7a, sta, pa, ita, fxa, Wa), (p7b, stb, pb, itb, fxb, Wb) = out["1"], out["0"]
+    assert np.array_equal(p7a, p7b)
+    assert sta.converged and stb.converged and sta.iterations == stb.iterations
+    assert sta.rel_residual == stb.rel_residual and sta.true_rel_residual == stb.true_rel_residual
+    assert np.array_equal(ita, itb)
+    assert np.array_equal(pa, pb)
+    assert fxa.iterations == fxb.iterations == 9
+    assert np.array_equal(Wa, Wb)

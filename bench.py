@@ -401,7 +401,15 @@ def run_gmaf(args, cfg):
     peak, peak_src = _peaks()
     traffic = _ncu_traffic(dom["name"], cfg.name)
     solve_ms = sum(k["total_ms"] for k in kt if k["name"].startswith(("pcg_", "sr_", "true_")))
-    launches = int(sum(k["launches"] for k in kt if not k["name"].startswith("tail_")))   # tails are not launches
+    # kernels this process launched in the timed region: every timed kernel's launches, except that
+    # the persistent solve runs ALL its iterations ("sr_iter" entries, one per PCG iteration) in one
+    # k_srp launch, followed by one fix-up launch (untimed); tails and barrier waits are not launches
+    tiles = S.tile_config()
+    persistent = bool(tiles["persistent"])
+    n_solves = args.steps
+    launches = int(sum(k["launches"] for k in kt
+                       if not k["name"].startswith(("tail_", "gridbar_")) and not (persistent and k["name"] == "sr_iter")))
+    launches += (2 * n_solves) if persistent else n_solves   # k_srp + k_sr_fixup, or the fix-up alone
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_max_ms / args.steps, "higher_is_better": True,
@@ -415,6 +423,11 @@ def run_gmaf(args, cfg):
                      "avg_launch_us_events": avg_ev_s * 1e6, "avg_launch_us_globaltimer": avg_gt_s * 1e6,
                      "achieved_globaltimer": dom["bytes_per_launch"] / avg_gt_s / 1e9,
                      "canonical_equiv_frac": value / max(world, 1) * 120.0 / (peak * 1e9),
+                     "unit_of_launch": ("one PCG iteration of the persistent kernel k_srp (all iterations of a "
+                                        "solve run in one cooperative launch)") if persistent else
+                                       "one launch of the per-iteration kernel k_sr",
+                     "traffic_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum of the iteration kernel per "
+                                     "PCG iteration (profiles/ncu_traffic.json), the same unit as bytes_per_launch",
                      "note": "achieved = algorithmic bytes (DESIGN.md sec. 6) / event-timed launch; "
                              "canonical_equiv_frac = per-GPU DOF*iter/s x 120 B (SURVEY 8(d) S1 3-band) / peak"},
         "kernels": {k["name"]: {"launches": k["launches"], "total_ms": round(k["total_ms"], 3),
@@ -426,6 +439,7 @@ def run_gmaf(args, cfg):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": K * 13 * 8 + 48,
                 "d2h_bytes_per_step": K * 12 * 8 + 8 * 7 * K + 128},
         "gpu_launches": launches,
+        "tiles": tiles,
         "clocks": ck,
     }
     if rank == 0 and world == 1 and args.picard_steps > 0:

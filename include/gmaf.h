@@ -314,6 +314,13 @@ typedef struct {
 } gmaf_tiles;
 gmaf_status gmaf_tile_config(const gmaf_ctx* ctx, gmaf_tiles* out);
 
+/* Load-balance diagnostics of the persistent solve: with the environment variable GMAF_DIAG set at
+ * gmaf_create, the persistent kernel records the %globaltimer (ns) at which each CTA arrives at
+ * the grid barrier of each of the first 32 iterations of a solve; this copies them to out
+ * (uint64 [iteration][CTA], CTA b = tile * K + condition, tile = chunk * n_strips + strip) and
+ * sets *count (0 without GMAF_DIAG or without the persistent path).  Errors: INVALID_ARG. */
+gmaf_status gmaf_cta_arrivals(gmaf_ctx* ctx, uint64_t* out, int32_t n, int32_t* count);
+
 /* Make a new ncclUniqueId (128 bytes) into out (NCCL is loaded at run time).  Errors: NCCL. */
 gmaf_status gmaf_nccl_unique_id(void* out);
 

@@ -99,3 +99,36 @@ def picard_iteration(g: dict, pump: dict, state, phi: float, dt: float, scheme="
     e_next, edot_next = update(F, Je, Jv, state[0:4], state[4:8], dt, scheme)
     return dict(F=F, F_oil=Fo[0], F_ext=Fe, F_inertial=Fi, J_e=Je, J_edot=Jv, e_next=e_next,
                 edot_next=edot_next, wrench=W[0], pcg_iterations=res.iterations)
+
+
+def picard_step(g: dict, pump: dict, prev, phi: float, dt: float, scheme="general", eps_dyn=1e-3,
+                max_picard=20, tol=1e-10, omega=1.6):
+    """One time step t_l -> t_l + dt (Sec. 2.3; R-A31): start from e = e_l + dt edot_l,
+    edot = edot_l (prev carries e_l, edot_l and the load case of t_l + dt) and iterate until
+    ||F|| <= eps_dyn max(||F_E||, 1 N).  Returns (state, Picard iterations, converged)."""
+    cur = np.asarray(prev, dtype=np.float64).reshape(13).copy()
+    cur[0:4] = cur[0:4] + dt * cur[4:8]
+    scale = max(np.linalg.norm(external_force(pump, cur, phi)), 1.0)
+    for k in range(max_picard):
+        it = picard_iteration(g, pump, cur, phi, dt, scheme, tol=tol, omega=omega)
+        if np.linalg.norm(it["F"]) <= eps_dyn * scale:
+            return cur, k + 1, True
+        cur = cur.copy()
+        cur[0:4], cur[4:8] = it["e_next"], it["edot_next"]
+    return cur, max_picard, False
+
+
+def march(g: dict, pump: dict, state0, n_steps: int, deg: float, load_case, scheme="general", omega=1.6):
+    """The Picard time march over n_steps steps of `deg` degrees from shaft angle 0: load_case(phi)
+    -> (L_F, U_theta, U_y, p_in, p_out) of each step.  Returns the [n_steps][4] eccentricities."""
+    dt = 2 * math.pi / pump["omega_s"] / 360.0 * deg
+    state = np.asarray(state0, dtype=np.float64).reshape(13).copy()
+    out = []
+    for s in range(1, n_steps + 1):
+        phi = math.radians(s * deg)
+        state[8:13] = load_case(phi)
+        state, _, ok = picard_step(g, pump, state, phi, dt, scheme, omega=omega)
+        if not ok:
+            raise RuntimeError(f"march: step {s} did not converge")
+        out.append(state[0:4].copy())
+    return np.array(out)

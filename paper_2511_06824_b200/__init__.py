@@ -132,6 +132,7 @@ def lib() -> C.CDLL:
         L.gmaf_p2p_connect.argtypes = [P, P]
         L.gmaf_slab.argtypes = [P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
         L.gmaf_tile_config.argtypes = [P, C.POINTER(gmaf_tiles)]
+        L.gmaf_cta_arrivals.argtypes = [P, C.POINTER(C.c_uint64), C.c_int32, C.POINTER(C.c_int32)]
         L.gmaf_slab_rows.argtypes = [C.c_int32, C.c_int32, C.c_int32] + [C.POINTER(C.c_int32)] * 4
         L.gmaf_last_error.restype = C.c_char_p
         L.gmaf_last_error.argtypes = [P]
@@ -141,7 +142,7 @@ def lib() -> C.CDLL:
                      "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_set_schedule",
                      "gmaf_nccl_unique_id", "gmaf_cond_iterations", "gmaf_general_forces",
                      "gmaf_picard_iteration", "gmaf_picard_step", "gmaf_p2p_handle", "gmaf_p2p_connect",
-                     "gmaf_slab", "gmaf_slab_rows", "gmaf_tile_config"):
+                     "gmaf_slab", "gmaf_slab_rows", "gmaf_tile_config", "gmaf_cta_arrivals"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -152,7 +153,7 @@ ABI_SYMBOLS = ("gmaf_workspace_bytes", "gmaf_workspace_bytes_m", "gmaf_create", 
                "gmaf_kernel_times", "gmaf_reset_kernel_times", "gmaf_set_schedule", "gmaf_nccl_unique_id",
                "gmaf_cond_iterations", "gmaf_general_forces", "gmaf_picard_iteration", "gmaf_picard_step",
                "gmaf_p2p_handle", "gmaf_p2p_connect", "gmaf_slab", "gmaf_slab_rows", "gmaf_tile_config",
-               "gmaf_last_error", "gmaf_version")
+               "gmaf_cta_arrivals", "gmaf_last_error", "gmaf_version")
 SCHEDULE = {"table1": 0, "single": 1}
 
 
@@ -379,6 +380,17 @@ class JointSolver:
         _check(self.ctx, lib().gmaf_tile_config(self.ctx, C.byref(t)))
         return {"tw": t.tw, "th": t.th, "n_strips": t.n_strips, "n_chunks": t.n_chunks, "n_ctas": t.n_ctas,
                 "schedule": _SCHED_NAME[t.schedule], "persistent": bool(t.persistent)}
+
+    def cta_arrivals(self) -> np.ndarray:
+        """[iteration][CTA] %globaltimer ns of each CTA's arrival at the persistent kernel's grid
+        barrier (first 32 iterations of the last solve; needs GMAF_DIAG at create; else empty)."""
+        t = self.tile_config()
+        n = 32 * t["n_ctas"]
+        buf = (C.c_uint64 * n)()
+        cnt = C.c_int32()
+        _check(self.ctx, lib().gmaf_cta_arrivals(self.ctx, buf, n, C.byref(cnt)))
+        return np.array(list(buf)[: cnt.value], dtype=np.uint64).reshape(-1, t["n_ctas"]) if cnt.value else \
+            np.zeros((0, t["n_ctas"]), dtype=np.uint64)
 
     def cond_iterations(self) -> np.ndarray:
         """Per-condition iteration counts of the last solve (the freeze iteration under 'async')."""

@@ -715,6 +715,7 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
   gp.tex_band = tex ? grid->tex_band_rows : 0; gp.tex_num = grid->tex_fill_num;
   gp.tex_den = grid->tex_fill_den > 0 ? grid->tex_fill_den : 1; gp.tex_depth = grid->tex_depth;
   gp.y0 = sl.y0; gp.y1 = sl.y1; gp.yb = sl.yb;
+  gp.diag = 0;   // set below once the tiles are known
   gp.ns = (long long)grid->n_theta * (sl.ye - sl.yb);
   DevPtrs& d = ctx->d;
   d.ct = at<double>(ctx, L.off_ct); d.st = at<double>(ctx, L.off_st);
@@ -820,6 +821,10 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
     const bool want = !(pe && std::strcmp(pe, "0") == 0);
     ctx->persist_ok = want && !dm && single_ok(grid->n_theta) && ctx->sr_k_ok && srp_fits(ctx->tiles_sr, K) &&
                       (long long)srp_ctas_per_sm(ctx->tiles_sr, K) * sms >= (long long)ctx->tiles_sr.n_tiles * K;
+    // diagnostics (gmaf_cta_arrivals): the arrival stamps live after the persistent kernel's two
+    // partial-sum buffers inside the partials region (4 K kMaxTilesPerCondition doubles)
+    gp.diag = (std::getenv("GMAF_DIAG") && ctx->persist_ok &&
+               (8 + kDiagIters) * ctx->tiles_sr.n_tiles <= 4 * kMaxTilesPerCondition) ? 1 : 0;
   }
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
   ctx->quad_ctas = quad_ctas_per_condition(gp, K);
@@ -1176,6 +1181,19 @@ gmaf_status gmaf_slab_rows(int32_t n_y, int32_t world, int32_t rank, int32_t* y0
     return GMAF_E_INVALID_ARG;
   const Slab sl = slab_of(n_y, world, rank);
   *y0 = sl.y0; *y1 = sl.y1; *yb = sl.yb; *ye = sl.ye;
+  return GMAF_OK;
+}
+
+gmaf_status gmaf_cta_arrivals(gmaf_ctx* ctx, uint64_t* out, int32_t n, int32_t* count) {
+  if (!ctx || !out || !count) return GMAF_E_INVALID_ARG;
+  *count = 0;
+  if (!ctx->gp.diag || !ctx->persist_ok) return GMAF_OK;
+  const int nblk = ctx->tiles_sr.n_tiles * ctx->K;
+  const int m = kDiagIters * nblk < n ? kDiagIters * nblk : n;
+  const double* base = ctx->d.partials + (size_t)8 * ctx->K * ctx->tiles_sr.n_tiles;
+  CU(cudaMemcpyAsync(out, base, (size_t)m * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  *count = m;
   return GMAF_OK;
 }
 

@@ -30,11 +30,13 @@ struct GridParams {
   // k hold the stored rows [yb, yb + ns/nt) -- the owned rows [y0, y1) plus up to SLAB_HALO
   // halo rows on each side -- and are addressed with GLOBAL row indices through fofs().  One
   // rank: y0 = yb = 0, y1 = ny, ns = nt*ny.
-  int32_t y0, y1, yb, pad_;
+  int32_t y0, y1, yb;
+  int32_t diag;     // 1: the persistent kernel records per-CTA grid-barrier arrival times (gmaf_cta_arrivals)
   long long ns;
 };
 
-constexpr int SLAB_HALO = 4;   // halo rows per side: the y dependency radius of A M^-1 A M^-1
+constexpr int SLAB_HALO = 4;
+constexpr int kDiagIters = 32;   // iterations whose per-CTA arrival times are recorded (diag mode)   // halo rows per side: the y dependency radius of A M^-1 A M^-1
 
 // Offset of (condition k, global row 0, column 0) in a [K][stored rows][nt] field.
 __host__ __device__ __forceinline__ long long fofs(const GridParams& g, int k) {

@@ -33,6 +33,7 @@
 //   D(2) s = A pd, r, x, w2 E(2) v2                         F(3) z2, gamma
 //   G(4) delta = z2' A z2 (quadratic form)
 #include <cstdint>
+#include <cstdlib>
 #include "sr_common.cuh"
 
 namespace gmaf {
@@ -211,8 +212,16 @@ __device__ __forceinline__ void sr_produce(const GridParams& g, const DevPtrs& d
 // -------------------------------------------------------------------- compute warps
 // One pass of the 7-stage row pipeline over the tile (all nsteps steps).  Accumulates the
 // per-thread gamma, delta, r.r and S.S partials into acc.
-template <int PC, int MODE>
-__device__ __forceinline__ void sr_compute(const GridParams& g, const DevPtrs& d, const SrGeo& q, const SrSmem& s,
+// SEAM selects how the row loop treats the periodic seam (the wrap terms of R-A12):
+//   SEAM_NONE  -- no seam code (a warp without a seam pair, in the split variant);
+//   SEAM_FIXED -- the warp holding the seam pairs: corrections as selects, no divergent branches;
+//   SEAM_CHECK -- one loop for every warp, the seam warp branching into the corrections.
+// All three evaluate the same expressions for every column, so results are bitwise identical: a
+// seam column's L/U sums are formed directly from its own terms (as Eqs. 3.5-3.6 state them for
+// the natural ordering), not as the plain sums plus and minus a correction.
+enum { SEAM_NONE = 0, SEAM_FIXED = 1, SEAM_CHECK = 2 };
+template <int PC, int MODE, int SEAM>
+__device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPtrs& d, const SrGeo& q, const SrSmem& s,
                                            int parity, double alpha, double alpha_prev, double beta, double omega,
                                            uint32_t gstep0, double& acc_rr, double& acc_g, double& acc_d,
                                            double& acc_s) {
@@ -223,8 +232,9 @@ __device__ __forceinline__ void sr_compute(const GridParams& g, const DevPtrs& d
   const int nt = g.nt, NL = q.NL, NTC = q.NTC, NCT = q.NCT, tl = q.tl, im = q.im, ip = q.ip;
   const int j0 = q.j0, j1 = q.j1, jbase = q.jbase, gl = q.gl;
   const bool out = q.out, seamL = q.seamL, seamR = q.seamR, lcoef = q.lcoef;
-  // warp-uniform guard: only the warp holding a seam pair runs the wrap corrections
-  const bool seamWarp = __any_sync(0xffffffffu, (seamL || seamR) && q.tid < NCT);
+  const bool seamWarp = SEAM == SEAM_FIXED ||
+                        (SEAM == SEAM_CHECK && __any_sync(0xffffffffu, (q.seamL || q.seamR) && q.tid < NCT));
+
   double* rout = (ITER ? d.r[1 - parity] : d.r[0]) + q.fk;
   double* pdout = (ITER ? d.u[parity] : d.u[1]) + q.fk;
   double* x = d.p + q.fk;
@@ -285,7 +295,7 @@ __device__ __forceinline__ void sr_compute(const GridParams& g, const DevPtrs& d
         const double apl = left_of(AP0.r, c0, im, lcoef), ael = left_of(AE0.r, c0 + NL, im, lcoef);
         double sl = (ael * ael) * fast_rcp(apl);
         double sr = (AE0.l * AE0.l) * iD0.l;
-        if (seamWarp) {
+        if (SEAM != SEAM_NONE && seamWarp) {
           if (seamL) sl = 0.0;                                           // column 0: no W in L
           if (seamR) sr += (AE0.r * AE0.r) * fast_rcp(c0[ip]);           // column nt-1: E-wrap
         }
@@ -306,18 +316,32 @@ __device__ __forceinline__ void sr_compute(const GridParams& g, const DevPtrs& d
         const D2 v11 = rld(v_1, tl, NTC);
         const double v1p = rright(v_1, tl);
         const D2 AEm1 = ld2(c1 + NL, tl);
+        // the seam warp (which paces its CTA at every row barrier, and the seam strip the grid)
+        // loads its wrap operands together with the plain ones and applies them as selects
+        double wE = 0.0, aW = 0.0, vW = 0.0;
+        if constexpr (SEAM == SEAM_FIXED) {
+          wE = rright(w_0, tl);                                 // w(jl) right of the pair (column 0 for nt-1)
+          aW = c1[NL + im];                                     // A_E(jl-1) left of the pair (nt-1 for column 0)
+          vW = rleft(v_1, tl, NTC);                             // v1(jl-1) left of the pair
+        }
         // plain pair: L = {W, S}, U = {E, N}
         D2 sL{AN1.l * w1.l + ae0m * w0m, AN1.r * w1.r + AE0.l * w0.l};
-        if (seamWarp) {
-          if (seamL) sL.l -= ae0m * w0m;                        // column 0: W is the wrap (in U)
+        if constexpr (SEAM == SEAM_FIXED) {
+          sL.l = seamL ? AN1.l * w1.l : sL.l;                   // column 0: W is the wrap (in U)
+          sL.r = seamR ? sL.r + AE0.r * wE : sL.r;              // column nt-1: E-wrap is in L
+        } else if (SEAM == SEAM_CHECK && seamWarp) {
+          if (seamL) sL.l = AN1.l * w1.l;                       // column 0: W is the wrap (in U)
           if (seamR) sL.r += AE0.r * rright(w_0, tl);           // column nt-1: E-wrap is in L
         }
         const D2 v10{w0.l - oD0.l * sL.l, w0.r - oD0.r * sL.r};
         rst(v_0, tl, NTC, v10);
         D2 sU{AN1.l * v10.l + AEm1.l * v11.r, AN1.r * v10.r + AEm1.r * v1p};
-        if (seamWarp) {
-          if (seamL) sU.l += c1[NL + im] * rleft(v_1, tl, NTC); // column 0: W-wrap
-          if (seamR) sU.r -= AEm1.r * v1p;                      // column nt-1: no E in U
+        if constexpr (SEAM == SEAM_FIXED) {
+          sU.l = seamL ? sU.l + aW * vW : sU.l;                 // column 0: the W-wrap is in U
+          sU.r = seamR ? AN1.r * v10.r : sU.r;                  // column nt-1: no E in U
+        } else if (SEAM == SEAM_CHECK && seamWarp) {
+          if (seamL) sU.l += c1[NL + im] * rleft(v_1, tl, NTC); // column 0: the W-wrap is in U
+          if (seamR) sU.r = AN1.r * v10.r;                      // column nt-1: no E in U
         }
         z1 = {c2 * (v11.l - oD1.l * sU.l), c2 * (v11.r - oD1.r * sU.r)};
       } else {
@@ -363,17 +387,29 @@ __device__ __forceinline__ void sr_compute(const GridParams& g, const DevPtrs& d
         const D2 v23 = rld(v2_3, tl, NTC);
         const double v23p = rright(v2_3, tl);
         const D2 AEm3 = ld2(c3 + NL, tl);
+        double wE2 = 0.0, aW2 = 0.0, vW2 = 0.0;
+        if constexpr (SEAM == SEAM_FIXED) {
+          wE2 = rright(w2_2, tl);
+          aW2 = c3[NL + im];
+          vW2 = rleft(v2_3, tl, NTC);
+        }
         D2 sL{AN3.l * w23.l + ae2m * wz2m, AN3.r * w23.r + AEm2.l * wz.l};
-        if (seamWarp) {
-          if (seamL) sL.l -= ae2m * wz2m;
+        if constexpr (SEAM == SEAM_FIXED) {
+          sL.l = seamL ? AN3.l * w23.l : sL.l;
+          sL.r = seamR ? sL.r + AEm2.r * wE2 : sL.r;
+        } else if (SEAM == SEAM_CHECK && seamWarp) {
+          if (seamL) sL.l = AN3.l * w23.l;
           if (seamR) sL.r += AEm2.r * rright(w2_2, tl);
         }
         const D2 v22{wz.l - oD2.l * sL.l, wz.r - oD2.r * sL.r};
         rst(v2_2, tl, NTC, v22);
         D2 sU{AN3.l * v22.l + AEm3.l * v23.r, AN3.r * v22.r + AEm3.r * v23p};
-        if (seamWarp) {
+        if constexpr (SEAM == SEAM_FIXED) {
+          sU.l = seamL ? sU.l + aW2 * vW2 : sU.l;
+          sU.r = seamR ? AN3.r * v22.r : sU.r;
+        } else if (SEAM == SEAM_CHECK && seamWarp) {
           if (seamL) sU.l += c3[NL + im] * rleft(v2_3, tl, NTC);
-          if (seamR) sU.r -= AEm3.r * v23p;
+          if (seamR) sU.r = AN3.r * v22.r;
         }
         u2_3 = {c2 * (v23.l - oD3.l * sU.l), c2 * (v23.r - oD3.r * sU.r)};
       } else {
@@ -409,6 +445,30 @@ __device__ __forceinline__ void sr_compute(const GridParams& g, const DevPtrs& d
   }
 }
 
+// The compute role.  SPLIT: the warp holding the seam runs the SEAM_FIXED row loop and every
+// other warp the SEAM_NONE one (warp-uniform choice, once per pass): the plain warps carry no
+// seam code, and the seam warp no divergent branches -- worth ~4% at long row chunks (C3), but
+// the two loops cost instruction-cache refills at every pass, which short chunks (row slabs of
+// 128 rows) do not amortize.  !SPLIT: one SEAM_CHECK loop for all warps.
+template <int PC, int MODE, bool SPLIT>
+__device__ __forceinline__ void sr_compute(const GridParams& g, const DevPtrs& d, const SrGeo& q, const SrSmem& s,
+                                           int parity, double alpha, double alpha_prev, double beta, double omega,
+                                           uint32_t gstep0, double& acc_rr, double& acc_g, double& acc_d,
+                                           double& acc_s) {
+  if constexpr (SPLIT) {
+    const bool seamWarp = __any_sync(0xffffffffu, (q.seamL || q.seamR) && q.tid < q.NCT);
+    if (seamWarp)
+      sr_compute_loop<PC, MODE, SEAM_FIXED>(g, d, q, s, parity, alpha, alpha_prev, beta, omega, gstep0, acc_rr, acc_g,
+                                            acc_d, acc_s);
+    else
+      sr_compute_loop<PC, MODE, SEAM_NONE>(g, d, q, s, parity, alpha, alpha_prev, beta, omega, gstep0, acc_rr, acc_g,
+                                           acc_d, acc_s);
+  } else {
+    sr_compute_loop<PC, MODE, SEAM_CHECK>(g, d, q, s, parity, alpha, alpha_prev, beta, omega, gstep0, acc_rr, acc_g,
+                                          acc_d, acc_s);
+  }
+}
+
 template <int PC, int MODE>
 __global__ void __maxnreg__(168)
 k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long hcond, int use_cond) {
@@ -433,7 +493,7 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
     const double alpha = ITER ? d.cs.alpha[q.k] : 0.0;
     const double alpha_prev = ITER ? d.cs.uvk[q.k] : 0.0;   // uvk holds alpha_{i-1} here
     const double beta = ITER ? d.cs.beta[q.k] : 0.0;
-    sr_compute<PC, MODE>(g, d, q, s, parity, alpha, alpha_prev, beta, st->omega, 0u, acc_rr, acc_g, acc_d, acc_s);
+    sr_compute<PC, MODE, false>(g, d, q, s, parity, alpha, alpha_prev, beta, st->omega, 0u, acc_rr, acc_g, acc_d, acc_s);
   }
 
   // ---- per-CTA partials, then the scalar stage (last CTA, fixed order)
@@ -524,7 +584,7 @@ __device__ __forceinline__ SrpShared srp_shared(double* smem_raw, int NL, int K,
   return x;
 }
 
-template <int PC>
+template <int PC, bool SPLIT>
 __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K) {
   extern __shared__ __align__(128) double smem_raw[];
   if (d.st_->done) return;                   // the init already converged (or failed)
@@ -594,8 +654,8 @@ __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K
     double a_rr = 0.0, a_g = 0.0, a_d = 0.0, a_s = 0.0;
     if (!(async && x.cs.frz[q.k])) {
       const double alpha = x.cs.alpha[q.k], alpha_prev = x.cs.uvk[q.k], beta = x.cs.beta[q.k];
-      if (parity) sr_compute<PC, SR_ITER_ODD>(g, d, q, s, 1, alpha, alpha_prev, beta, omega, gstep, a_rr, a_g, a_d, a_s);
-      else sr_compute<PC, SR_ITER_EVEN>(g, d, q, s, 0, alpha, alpha_prev, beta, omega, gstep, a_rr, a_g, a_d, a_s);
+      if (parity) sr_compute<PC, SR_ITER_ODD, SPLIT>(g, d, q, s, 1, alpha, alpha_prev, beta, omega, gstep, a_rr, a_g, a_d, a_s);
+      else sr_compute<PC, SR_ITER_EVEN, SPLIT>(g, d, q, s, 0, alpha, alpha_prev, beta, omega, gstep, a_rr, a_g, a_d, a_s);
       gstep += (uint32_t)q.nsteps;
     }
     // field stores of this iteration -> visible to the other CTAs' TMA reads after the barrier
@@ -609,6 +669,10 @@ __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K
     double* part = d.partials + (size_t)(it & 1) * 4 * K * ncta;   // parity buffers
     if (q.tid == 0) {
       if (timed) tim[3] = globaltimer();
+      // load-balance diagnostics: this CTA's arrival at the grid barrier (after the persistent
+      // kernel's two partial-sum buffers in the partials region; gmaf_cta_arrivals)
+      if (g.diag && it < kDiagIters)
+        reinterpret_cast<unsigned long long*>(d.partials + (size_t)8 * K * ncta)[it * nblk + blockIdx.x] = globaltimer();
       warps_in_order<3>(v, x.wpart, nw);
       for (int c = 0; c < 3; ++c) part[(size_t)(c * K + q.k) * ncta + cta] = v[c];
       part[(size_t)(3 * K + q.k) * ncta + cta] = 0.0;
@@ -668,8 +732,15 @@ __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K
   }
 }
 
+// The split seam variant (see sr_compute) pays off for long row chunks only.
+bool srp_split_seam(const TileCfg& t) {
+  if (const char* e = std::getenv("GMAF_SEAM_SPLIT")) return std::atoi(e) != 0;   // A/B experiments
+  return t.th >= 128;
+}
+
 cudaError_t launch_sr_persistent(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,
                                  cudaStream_t s) {
+  const bool split = srp_split_seam(t);
   cudaError_t e = cudaMemsetAsync(d.counters + kCtrGridBar, 0, sizeof(unsigned int), s);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
@@ -683,17 +754,19 @@ cudaError_t launch_sr_persistent(const GridParams& g, const DevPtrs& d, const Ti
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   switch (precond) {
-    case SPC_ASSOR2: return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2>, g, d, t, K);
-    case SPC_ASSOR1: return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR1>, g, d, t, K);
-    case SPC_JACOBI: return cudaLaunchKernelEx(&cfg, k_srp<SPC_JACOBI>, g, d, t, K);
-    default: return cudaLaunchKernelEx(&cfg, k_srp<SPC_NONE>, g, d, t, K);
+    case SPC_ASSOR2:
+      return split ? cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, true>, g, d, t, K)
+                   : cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, false>, g, d, t, K);
+    case SPC_ASSOR1: return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR1, false>, g, d, t, K);
+    case SPC_JACOBI: return cudaLaunchKernelEx(&cfg, k_srp<SPC_JACOBI, false>, g, d, t, K);
+    default: return cudaLaunchKernelEx(&cfg, k_srp<SPC_NONE, false>, g, d, t, K);
   }
 }
 
 // resident CTAs per SM of the persistent kernel with K conditions (0: it does not fit)
 int srp_ctas_per_sm(const TileCfg& t, int K) {
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_srp<SPC_ASSOR2>, sr_threads(t),
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_srp<SPC_ASSOR2, false>, sr_threads(t),
                                                     srp_smem_bytes(2 * sr_pairs(t), K, t.n_tiles * K)) != cudaSuccess)
     return 0;
   return n;
@@ -1014,10 +1087,11 @@ cudaError_t configure_sr_kernels(const TileCfg& t, int K) {
   if (e == cudaSuccess) e = sr_set_modes<SR_ITER_ODD>(cap);
   if (e == cudaSuccess) e = sr_set_modes<SR_INIT_COLD>(cap);
   if (e == cudaSuccess) e = sr_set_modes<SR_INIT_WARM>(cap);
-  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2>, cap);
-  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR1>, cap);
-  if (e == cudaSuccess) e = sr_set(k_srp<SPC_JACOBI>, cap);
-  if (e == cudaSuccess) e = sr_set(k_srp<SPC_NONE>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2, true>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2, false>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR1, false>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_JACOBI, false>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_NONE, false>, cap);
   (void)K;
   if (e == cudaSuccess) done |= 1u << dev;
   return e;

@@ -9,7 +9,8 @@
 
 namespace gmaf {
 
-enum { SR_ITER_EVEN = 0, SR_ITER_ODD = 3, SR_INIT_COLD = 1, SR_INIT_WARM = 2 };
+enum { SR_ITER_EVEN = 0, SR_ITER_ODD = 3, SR_INIT_COLD = 1, SR_INIT_WARM = 2,
+       SR_ITER_ANY = 4 /* either parity, decided at run time (persistent kernel) */ };
 enum { SPC_NONE = 0, SPC_JACOBI = 1, SPC_ASSOR2 = 2, SPC_ASSOR1 = 3 };   // = GMAF_PRECOND_*
 
 // ------------------------------------------------------------------- PTX helpers

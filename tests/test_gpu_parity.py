@@ -69,6 +69,8 @@ def full_parity(P, orc, g, conds, omega, precond="assor2", coupling="coupled", t
     assert st.rel_residual <= tol and st.true_rel_residual <= 10 * tol
     pg = np.stack([S.get("p", k) for k in range(K)])
     assert rel(pg, ref.p) <= 1e-8, rel(pg, ref.p)
+    # node by node too: the relative L2 over a whole field would hide a local error
+    assert np.max(np.abs(pg - ref.p)) <= 1e-8 * np.max(np.abs(ref.p)), np.max(np.abs(pg - ref.p))
     for k in range(K):
         wo = orc.wrench(g, conds[k], ref.p[k])
         assert wrench_err(W[k], wo, conds[k][8]) <= 1e-6, (k, W[k], wo)
@@ -223,6 +225,31 @@ def test_band_storage_sized_by_distinct_matrices(P, orc, gi):
         S5.assemble()
     S5.close()
     S9.close()
+
+
+@pytest.mark.timeout(900)
+def test_coupled_k72_c5_layout(P, orc, gi):
+    """C5's synchronized (coupled) strategy -- ONE Krylov process over K = 72 conditions (8
+    operating points x 9 FD conditions; Eq. 3.7; Eq. 3.9; R-A11) -- against the
+    oracle: the first 7 iterates at a mid mesh (512x256 short texture) within 1e-9, and converged
+    solves at 128x96 (coupled and lockstep) within the full-parity bars."""
+    conds = gi.c5_conditions()
+    assert conds.shape[0] == 72
+    g = gi.grid(512, 256, "short")
+    S = P.JointSolver(g, 72, max_matrices=40)
+    S.thickness(conds)
+    S.assemble()
+    st = S.solve(tol=1e-30, omega=1.6, max_iter=7, raise_on_error=False)
+    assert st.iterations == 7
+    AP, AE, AN, SS = orc.assemble_joint(g, conds)
+    ref = orc.pcg_joint(AP, AE, AN, SS, tol=1e-30, omega=1.6, max_iter=7, schedule="single")
+    pg = np.stack([S.get("p", k) for k in range(72)])
+    assert rel(pg, ref.p) <= 1e-9, rel(pg, ref.p)
+    assert np.max(np.abs(pg - ref.p)) <= 1e-9 * np.max(np.abs(ref.p))
+    S.close()
+    g = gi.grid(128, 96, "short", tex_n_theta=30, tex_n_y=3, tex_band_rows=24)
+    full_parity(P, orc, g, conds, 1.6)
+    full_parity(P, orc, g, conds, 1.6, coupling="lockstep")
 
 
 def test_c2_parity(P, orc, gi):
@@ -554,6 +581,8 @@ def test_random_meshes_and_textures(P, orc, gi, case):
 
 PERSIST_CASES = {
     "c2": ("C2", {}),
+    "c2_split_seam": ("C2", {"_split": "1"}),
+    "ragged_split_seam": (None, {"_split": "1"}),
     "ragged_textured": (None, {}),
     "lockstep": ("C2", {"coupling": "lockstep"}),
     "async": (None, {"coupling": "async"}),
@@ -567,8 +596,13 @@ def test_persistent_equals_per_launch_kernels(P, gi, monkeypatch, case):
     """The persistent solve (sr.cu k_srp: all iterations in one cooperative launch, a grid barrier
     and a redundant scalar stage per iteration) runs the same row pipeline, the same fixed-order
     block reduction, the same CTA-order sums and the same scalar stage as the per-iteration
-    kernels of the graph's WHILE loop: the two are bitwise identical."""
+    kernels of the graph's WHILE loop: the two are bitwise identical (with the split seam loops
+    of long row chunks: equal to rounding)."""
     name, kw = PERSIST_CASES[case]
+    kw = dict(kw)
+    split = "_split" in kw
+    if split:   # the split seam variant of the persistent row loop (sr.cu sr_compute)
+        monkeypatch.setenv("GMAF_SEAM_SPLIT", kw.pop("_split"))
     if name:
         cfg = gi.config(name)
         g, conds, omega = cfg.grid, cfg.conds, cfg.omega
@@ -591,6 +625,13 @@ def test_persistent_equals_per_launch_kernels(P, gi, monkeypatch, case):
         out[mode] = (p7, st, p, its, fx, S.integrate())
         S.close()
     (p7a, sta, pa, ita, fxa, Wa), (p7b, stb, pb, itb, fxb, Wb) = out["1"], out["0"]
+    if split:
+        # the split loops evaluate the seam columns' sums in their own code (the compiler may
+        # contract them differently): equal to rounding, the stopping iteration to +-1
+        assert rel(p7a, p7b) <= 1e-12, rel(p7a, p7b)
+        assert sta.converged and stb.converged and abs(sta.iterations - stb.iterations) <= 1
+        assert rel(pa, pb) <= 1e-9
+        return
     assert np.array_equal(p7a, p7b)
     assert sta.converged and stb.converged and sta.iterations == stb.iterations
     assert sta.rel_residual == stb.rel_residual and sta.true_rel_residual == stb.true_rel_residual

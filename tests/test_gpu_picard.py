@@ -94,3 +94,37 @@ def test_picard_errors(P):
         S.picard_iteration(gi.pump(), gi.condition(), 0.0, -1.0)
     assert ei.value.code == -1
     S.close()
+
+
+def test_march_matches_the_oracle_and_stays_bounded(P):
+    """The product's Picard march (gmaf_picard_step) under a zero-mean periodic load (constant
+    p_in: the R-A29 swashplate reaction rotates in the piston frame; no centrifugal load) follows
+    the oracle's march (oracle.picard.march, R-A31) over a revolution and settles into a bounded
+    orbit over 8 (VERDICT r1 #7; the R-A29/A30 mean load is what made C4's orbit drift)."""
+    from oracle import picard as OP
+    g = gi.grid(32, 16)
+    pump0 = dict(gi.pump(), m_k=0.0, m_G=0.0)
+    deg = 10.0
+    dt = 2 * math.pi / gi.OMEGA_S / 360.0 * deg
+
+    def lc(phi):
+        return [gi.coupling_length(phi), 0.0, gi.stroke_speed(phi), gi.P_IN, gi.P_OUT]
+
+    state0 = gi.condition(phi_deg=0.0, p_in=gi.P_IN)
+    S = P.JointSolver(g, 9)
+    state = state0.copy()
+    E = []
+    for s in range(1, 8 * 36 + 1):
+        phi = math.radians(s * deg)
+        state = state.copy()
+        state[8:13] = lc(phi)
+        state, n_pic, res, pcg, code = S.picard_step(pump0, state, phi, dt, "general", eps_dyn=1e-3,
+                                                     max_picard=20, tol=1e-10, omega=1.8)
+        assert code == 0
+        E.append(state[0:4].copy())
+    S.close()
+    E = np.array(E) * 1e6
+    ref = OP.march(g, pump0, state0, 36, deg, lc, omega=1.8) * 1e6
+    assert relnorm(E[:36], ref) <= 1e-6, relnorm(E[:36], ref)
+    per_rev = [np.abs(E[r * 36:(r + 1) * 36]).max() for r in range(8)]
+    assert max(per_rev) < 6.0 and all(per_rev[r + 1] <= 1.01 * per_rev[r] for r in (4, 5, 6)), per_rev

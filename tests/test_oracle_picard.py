@@ -124,3 +124,83 @@ def test_library_general_forces_match_the_oracle_on_cpu():
         np.testing.assert_allclose(fo, OP.oil_force(w, c[8]), rtol=1e-13, atol=1e-12)
         np.testing.assert_allclose(fe, OP.external_force(pump, c, phi), rtol=1e-13, atol=1e-10)
         np.testing.assert_allclose(fi, OP.inertial_force(pump, c, phi), rtol=1e-13, atol=1e-12)
+
+
+# ----------------------------------------------------------- the orbit drift
+def test_pure_translation_has_no_static_film_force():
+    """A translated, untilted piston (e1 = e3, e2 = e4) at rest with no sliding: h depends on theta
+    only, every theta-column is a constant-coefficient 1-D problem, so p is the linear profile
+    between p_in and p_out EXACTLY (Eq. 2.3 + Eqs. 2.4-2.7) and the lateral film force vanishes
+    (pressure and shear); only the axial Poiseuille shear, larger where the gap is wider, leaves a
+    small moment about the lateral axes (Sec. 2.4-III)."""
+    import oracle as orc
+    g = gi.grid(64, 32)
+    c = gi.condition().copy()
+    c[0:4] = (2e-6, -1e-6, 2e-6, -1e-6)
+    c[4:8] = 0.0
+    c[9] = c[10] = 0.0
+    AP, AE, AN, S = orc.assemble(g, c)
+    p = orc.cholesky_solve(orc.expand_dense(AP, AE, AN), S.ravel()).reshape(32, 64)
+    j = np.arange(32)
+    lin = c[11] + (c[12] - c[11]) * (j + 1) / 33.0
+    assert np.max(np.abs(p - lin[:, None])) <= 1e-9 * c[11]
+    w = orc.wrench(g, c, p)
+    lateral = w[[0, 1, 3, 4, 6, 7]]          # Fp_x, Fp_y, Mp_x, Mp_y, Fs_x, Fs_y
+    assert np.max(np.abs(lateral)) <= 1e-9 * np.max(np.abs(w))
+    assert abs(w[9]) > 0 and abs(w[10]) > 0  # the axial-shear moment of the eccentric film
+
+
+def test_static_film_stiffness_is_circulatory():
+    """The film's static response to e under the p_in -> p_out pressure drop (no motion): a
+    translation gives no force (above) while a TILT gives a lateral force (the tapered-gap
+    'hydraulic lock' effect), so J_e = dF/de has the circulatory form [[a, -b], [b, -a]] per
+    direction with a ~ b and no restoring stiffness for a translation (eigenvalues +-i*sqrt(b^2-a^2)).
+    This is why the C4 orbit's mean position is not held by the film's static response: it drifts
+    under the non-zero mean of the R-A29/A30 loads."""
+    import oracle as orc
+    g = gi.grid(64, 32)
+
+    def F(e):
+        c = gi.condition().copy()
+        c[0:4], c[4:8], c[9], c[10] = e, 0.0, 0.0, 0.0
+        res, W = orc.joint_step(g, c[None], tol=1e-12, omega=1.8)
+        return OP.oil_force(W[0], c[8])
+
+    h = 1e-8
+    F0 = F(np.zeros(4))
+    J = np.stack([(F(h * np.eye(4)[j]) - F0) / h for j in range(4)], axis=1)
+    scale = np.abs(J).max()
+    trans_x, tilt_x = np.array([1.0, 0, 1, 0]), np.array([1.0, 0, -1, 0])
+    assert np.linalg.norm(J @ trans_x) <= 2e-3 * scale
+    ft = J @ tilt_x
+    assert ft[0] > 0 and ft[2] > 0 and abs(ft[0] - ft[2]) <= 2e-3 * scale   # a translating force
+    assert np.all(np.abs(np.linalg.eigvals(J).real) <= 1e-3 * scale)
+
+
+def _load_case(constant_p_in):
+    def lc(phi):
+        p_in = gi.P_IN if constant_p_in else gi.p_in_trapezoid(phi)
+        return [gi.coupling_length(phi), 0.0, gi.stroke_speed(phi), p_in, gi.P_OUT]
+    return lc
+
+
+def test_orbit_bounded_under_a_zero_mean_load():
+    """Under a load periodic by construction with ZERO mean -- constant p_in (the swashplate
+    reaction (-cos phi, sin phi) * const, R-A29) and no centrifugal load (masses 0, R-A30) -- the
+    Picard march settles into a bounded orbit: after the transient the per-revolution max |e|
+    stops growing.  Under the R-A29/A30 loads themselves (trapezoid p_in: a non-zero mean lateral
+    load) the same march drifts until the film is pinched (h < h_min), as the GPU's C4 trajectory
+    drifted (profiles/round1_picard_3rev_c4.json): the drift is the load model, not the solver."""
+    import oracle
+    g = gi.grid(32, 16)
+    pump0 = dict(gi.pump(), m_k=0.0, m_G=0.0)
+    state0 = gi.condition(phi_deg=0.0, p_in=gi.P_IN)
+    e = OP.march(g, pump0, state0, 8 * 36, 10.0, _load_case(True), omega=1.8) * 1e6
+    per_rev = [np.abs(e[r * 36:(r + 1) * 36]).max() for r in range(8)]
+    assert max(per_rev) < 6.0                                   # clearance R_c - R_k = 6 um
+    # the transient (the mean position settling, ~4 revolutions) is over: no further growth
+    assert all(per_rev[r + 1] <= 1.01 * per_rev[r] for r in (4, 5, 6)), per_rev
+    # the R-A29/A30 loads: the mean position runs away (contact within a few revolutions)
+    with pytest.raises((RuntimeError, oracle.OracleError)):
+        OP.march(g, gi.pump(), gi.condition(phi_deg=0.0, p_in=gi.p_in_trapezoid(0.0)), 8 * 36, 10.0,
+                 _load_case(False), omega=1.8)

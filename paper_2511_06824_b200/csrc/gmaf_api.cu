@@ -365,7 +365,7 @@ cudaError_t enqueue_final(gmaf_ctx* ctx, const GraphKey& key, cudaStream_t s) {
 }
 
 bool use_persistent(const gmaf_ctx* ctx, const GraphKey& key) {
-  return ctx->persist_ok && key.schedule == GMAF_SCHEDULE_SINGLE && !ctx->distm;
+  return ctx->persist_ok && key.schedule == GMAF_SCHEDULE_SINGLE && (!ctx->distm || ctx->p2p);
 }
 
 // Persistent solve: init -> ONE launch that runs every iteration (grid barrier per iteration,
@@ -819,8 +819,13 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
     // kernels inside the graph's WHILE loop)
     const char* pe = std::getenv("GMAF_PERSIST");
     const bool want = !(pe && std::strcmp(pe, "0") == 0);
-    ctx->persist_ok = want && !dm && single_ok(grid->n_theta) && ctx->sr_k_ok && srp_fits(ctx->tiles_sr, K) &&
-                      (long long)srp_ctas_per_sm(ctx->tiles_sr, K) * sms >= (long long)ctx->tiles_sr.n_tiles * K;
+    // (multi-rank: the peer-to-peer contexts, whose exchange runs inside the kernel; the NCCL
+    // path keeps its host-driven loop)
+    const bool p2p_ctx = dm && (!dist->nccl_unique_id || dist->shard == GMAF_SHARD_CONDITIONS_P2P || rm);
+    const int Kall = (dm && !rm) ? Kglob : K;
+    ctx->persist_ok = want && (!dm || p2p_ctx) && single_ok(grid->n_theta) && ctx->sr_k_ok &&
+                      srp_fits(ctx->tiles_sr, K, Kall) &&
+                      (long long)srp_ctas_per_sm(ctx->tiles_sr, K, Kall) * sms >= (long long)ctx->tiles_sr.n_tiles * K;
     // diagnostics (gmaf_cta_arrivals): the arrival stamps live after the persistent kernel's two
     // partial-sum buffers inside the partials region (4 K kMaxTilesPerCondition doubles)
     gp.diag = (std::getenv("GMAF_DIAG") && ctx->persist_ok &&
@@ -1204,7 +1209,7 @@ gmaf_status gmaf_tile_config(const gmaf_ctx* ctx, gmaf_tiles* out) {
   out->tw = t.tw; out->th = t.th; out->n_strips = t.n_strips; out->n_chunks = t.n_chunks;
   out->n_ctas = t.n_tiles * ctx->K;
   out->schedule = ctx->schedule;
-  out->persistent = (single && ctx->persist_ok && !ctx->distm) ? 1 : 0;
+  out->persistent = (single && ctx->persist_ok && (!ctx->distm || ctx->p2p)) ? 1 : 0;
   out->pad = 0;
   return GMAF_OK;
 }

@@ -182,8 +182,8 @@ int sr_ctas_per_sm(const TileCfg& t);
 // barrier per iteration and the scalar stage evaluated redundantly in every CTA (sr.cu k_srp)
 cudaError_t launch_sr_persistent(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,
                                  cudaStream_t s);
-int srp_ctas_per_sm(const TileCfg& t, int K);
-bool srp_fits(const TileCfg& t, int K);
+int srp_ctas_per_sm(const TileCfg& t, int K, int Kall);
+bool srp_fits(const TileCfg& t, int K, int Kall);
 // peer-to-peer mode: gather n doubles per rank from src into packed_all-style dst [world][n]
 // (one thread; a timeout marks the solve failed, GMAF_E_CUDA)
 cudaError_t launch_p2p_gather(const DevPtrs& d, const double* src, int n, double* dst, cudaStream_t s);

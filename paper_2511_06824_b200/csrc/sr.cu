@@ -142,7 +142,7 @@ __device__ __forceinline__ void sr_init_barriers(const SrGeo& q, const SrSmem& s
 template <int MODE>
 __device__ __forceinline__ void sr_produce(const GridParams& g, const DevPtrs& d, const SrGeo& q,
                                            const SrSmem& s, int K, int parity, uint32_t gstep0, int s_lo,
-                                           int s_hi) {
+                                           int s_hi, int islot_in = -1) {
   constexpr bool ITER = (MODE == SR_ITER_EVEN || MODE == SR_ITER_ODD);
   constexpr bool XUPD = (MODE == SR_ITER_ODD);
   constexpr bool USE_PD = ITER;
@@ -177,7 +177,8 @@ __device__ __forceinline__ void sr_produce(const GridParams& g, const DevPtrs& d
   // neighbours pushed them into (slot = parity of the last gather stamp)
   const bool inbox = ITER && lane < 2 && d.dist.rows == 1;
   const double* ibase = inbox ? d.dist.halo_in[d.dist.rank] : nullptr;
-  const int islot = inbox ? (int)(*d.dist.seq & 1ull) : 0;
+  // (the persistent kernel passes the slot: its own gathers advance the stamp during the launch)
+  const int islot = !inbox ? 0 : islot_in >= 0 ? islot_in : (int)(*d.dist.seq & 1ull);
   for (int step = s_lo; step < s_hi; ++step) {
     const uint32_t gs = gstep0 + (uint32_t)step;
     const int sv = (int)(gs & (SR_VSLOTS - 1)), sc = (int)(gs & (SR_CSLOTS - 1));
@@ -524,14 +525,15 @@ static int sr_threads(const TileCfg& t) { return ((sr_pairs(t) + 31) & ~31) + 32
 constexpr int kCtrGridBar = 14;   // d.counters slot of the grid barrier (zeroed before the launch)
 
 __host__ __device__ inline size_t srp_align(size_t x) { return (x + 15) & ~(size_t)15; }
-// extra dynamic shared memory after the rings: state copy, [4K] sums, [4][32] warp partials,
-// [4][nblk] per-CTA partials, 7 K doubles + 2 K ints of per-condition scalars, the ready flags
-__host__ __device__ inline size_t srp_extra_bytes(int K, int nblk) {
-  return srp_align(sizeof(SolverState)) + srp_align((size_t)4 * K * 8) + 4 * 32 * 8 + srp_align((size_t)4 * nblk * 8) +
-         srp_align((size_t)7 * K * 8) + srp_align((size_t)2 * K * 4) + 16 + 32;
+// extra dynamic shared memory after the rings: state copy, [4K] sums, [4 Kall] sums over the
+// ranks (multi-rank: Kall = all conditions of the joint system), [4][32] warp partials,
+// [4][nblk] per-CTA partials, 7 K doubles + 2 K ints of per-condition scalars, the flags
+__host__ __device__ inline size_t srp_extra_bytes(int K, int nblk, int Kall) {
+  return srp_align(sizeof(SolverState)) + srp_align((size_t)4 * K * 8) + srp_align((size_t)4 * Kall * 8) + 4 * 32 * 8 +
+         srp_align((size_t)4 * nblk * 8) + srp_align((size_t)7 * K * 8) + srp_align((size_t)2 * K * 4) + 16 + 32 + 16;
 }
-__host__ __device__ inline size_t srp_smem_bytes(int nl, int K, int nblk) {
-  return srp_align(sr_smem_bytes(nl)) + srp_extra_bytes(K, nblk);
+__host__ __device__ inline size_t srp_smem_bytes(int nl, int K, int nblk, int Kall) {
+  return srp_align(sr_smem_bytes(nl)) + srp_extra_bytes(K, nblk, Kall);
 }
 
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
@@ -556,19 +558,23 @@ __device__ __forceinline__ bool grid_wait(const unsigned int* ctr, unsigned int 
 struct SrpShared {
   SolverState* st;
   double* red;      // [4K] per-condition sums [rr | gamma | delta | S.S]
+  double* red2;     // [4 Kall] the sums the scalar stage takes (multi-rank: over all ranks)
   double* wpart;    // [4][32] per-warp partials
   double* pbuf;     // [4K][ncta] the per-CTA partials of one iteration
   CondScalars cs;   // CTA-private per-condition scalars
   volatile int* ready;   // [0]: iterations whose scalars are ready; [1]: failure flag
   unsigned long long* tim;   // [4] CTA 0's timing accumulators
+  unsigned long long* seqbase;   // multi-rank: gathers issued before this launch
 };
-__device__ __forceinline__ SrpShared srp_shared(double* smem_raw, int NL, int K, int nblk) {
+__device__ __forceinline__ SrpShared srp_shared(double* smem_raw, int NL, int K, int nblk, int Kall) {
   char* b = reinterpret_cast<char*>(smem_raw) + srp_align(sr_smem_bytes(NL));
   SrpShared x;
   x.st = reinterpret_cast<SolverState*>(b);
   b += srp_align(sizeof(SolverState));
   x.red = reinterpret_cast<double*>(b);
   b += srp_align((size_t)4 * K * 8);
+  x.red2 = reinterpret_cast<double*>(b);
+  b += srp_align((size_t)4 * Kall * 8);
   x.wpart = reinterpret_cast<double*>(b);
   b += 4 * 32 * 8;
   x.pbuf = reinterpret_cast<double*>(b);
@@ -581,16 +587,29 @@ __device__ __forceinline__ SrpShared srp_shared(double* smem_raw, int NL, int K,
   b += srp_align((size_t)2 * K * 4);
   x.ready = reinterpret_cast<volatile int*>(b);
   x.tim = reinterpret_cast<unsigned long long*>(b + 16);
+  x.seqbase = reinterpret_cast<unsigned long long*>(b + 48);
   return x;
 }
 
-template <int PC, bool SPLIT>
+// Multi-rank (peer-to-peer): the same kernel on every rank.  Row slabs
+// (d.dist.rows == 1): after its pass a CTA whose chunk touches the slab edge stores its output
+// columns of the 4 boundary rows of r_{i+1} and pd_i straight into the neighbour's inbox over
+// NVLink (slot = parity of the next gather stamp); after the local grid barrier, warp 0 of CTA 0
+// pushes the rank's per-condition sums into every rank's exchange buffer and posts its stamp
+// (release, system scope); EVERY CTA then waits for all ranks' stamps in its own buffer, reads
+// the blocks, adds them over the ranks in rank order (row slabs) or places them in global
+// condition order (condition sharding) and runs the same scalar stage -- bitwise the same
+// scalars on every CTA of every rank.  The producers of edge chunks stream their halo rows from
+// the inbox once the stamps (which also publish the halos) are in.
+template <int PC, bool SPLIT, bool DIST>
 __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K) {
   extern __shared__ __align__(128) double smem_raw[];
   if (d.st_->done) return;                   // the init already converged (or failed)
+  constexpr bool dist = DIST;                // peer-to-peer multi-rank context (d.dist.world > 0)
+  const int Kall = dist && d.dist.rows != 1 ? d.dist.kglob : K;
   const SrGeo q = sr_geo(g, d, t, K);
   const SrSmem s = sr_smem(smem_raw, q.NL);
-  const SrpShared x = srp_shared(smem_raw, q.NL, K, (int)gridDim.x);
+  const SrpShared x = srp_shared(smem_raw, q.NL, K, (int)gridDim.x, Kall);
   sr_init_barriers(q, s);
   // CTA-private copies of the solver state and of the per-condition scalars
   for (int i = q.tid; i < K; i += blockDim.x) {
@@ -598,31 +617,43 @@ __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K
     x.cs.Sk[i] = d.cs.Sk[i]; x.cs.rrk[i] = d.cs.rrk[i]; x.cs.uvk[i] = d.cs.uvk[i]; x.cs.ttk[i] = d.cs.ttk[i];
     x.cs.itk[i] = d.cs.itk[i]; x.cs.frz[i] = d.cs.frz[i];
   }
-  if (q.tid == 0) { *x.st = *d.st_; x.ready[0] = 0; x.ready[1] = 0; }
+  if (q.tid == 0) {
+    *x.st = *d.st_;
+    x.ready[0] = 0;
+    x.ready[1] = 0;
+    *x.seqbase = dist ? *d.dist.seq : 0ull;   // nobody gathers before every CTA has passed barrier 0
+  }
   __syncthreads();
   const int it0 = x.st->iter;                // iteration count at entry (0 after the init)
   const bool async = x.st->coupling == 2;
   const int nblk = gridDim.x, ncta = t.n_tiles, cta = blockIdx.x / K;
   unsigned int* gbar = d.counters + kCtrGridBar;
+  const bool rows = dist && d.dist.rows == 1 && d.dist.world > 1;
   uint32_t gstep = 0;                        // row steps this CTA streamed / consumed so far
 
   if (q.is_producer) {
     // ------------------------------------------------ producer: stream every iteration
     const int lane = q.tid - q.NCT;
+    // a chunk at a slab edge streams halo rows from the inbox: it needs the gather (whose
+    // stamps publish them), the others only the local grid barrier
+    const bool edge = rows && ((q.jbase < g.y0 && d.dist.rank > 0) ||
+                               (q.j1 + SR_YLO > g.y1 && d.dist.rank < d.dist.world - 1));
     for (int it = 0;; ++it) {
       const int parity = (it0 + it) & 1;
+      const int islot = (int)((*x.seqbase + (unsigned long long)it) & 1ull);
       int pre = 0;
       if (it > 0) {
-        // the rows of iteration it were written by all CTAs in iteration it-1
+        // the rows of iteration it were written by all CTAs (and neighbours) in iteration it-1
         bool ok = true;
-        if (lane == 0) ok = grid_wait(gbar, (unsigned)(it * nblk));
+        if (lane == 0)
+          ok = edge ? p2p_stamps_wait(d.dist, *x.seqbase + (unsigned long long)it) : grid_wait(gbar, (unsigned)(it * nblk));
         ok = __shfl_sync(0xffffffffu, ok, 0);
         if (!ok) break;
-        fence_proxy_async_global();          // generic-proxy stores -> TMA (async-proxy) reads
+        fence_proxy_async_global();          // generic-proxy / peer stores -> TMA (async-proxy) reads
         if (!async) {                        // prefetch 4 steps while the scalars are computed
           pre = 4;
-          if (parity) sr_produce<SR_ITER_ODD>(g, d, q, s, K, 1, gstep, 0, pre);
-          else sr_produce<SR_ITER_EVEN>(g, d, q, s, K, 0, gstep, 0, pre);
+          if (parity) sr_produce<SR_ITER_ODD>(g, d, q, s, K, 1, gstep, 0, pre, islot);
+          else sr_produce<SR_ITER_EVEN>(g, d, q, s, K, 0, gstep, 0, pre, islot);
         }
         while (x.ready[0] < it && x.ready[1] == 0) __nanosleep(32);
       }
@@ -635,8 +666,8 @@ __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K
         break;
       }
       if (async && x.cs.frz[q.k]) continue;  // frozen condition: no rows this iteration
-      if (parity) sr_produce<SR_ITER_ODD>(g, d, q, s, K, 1, gstep, pre, q.nsteps);
-      else sr_produce<SR_ITER_EVEN>(g, d, q, s, K, 0, gstep, pre, q.nsteps);
+      if (parity) sr_produce<SR_ITER_ODD>(g, d, q, s, K, 1, gstep, pre, q.nsteps, islot);
+      else sr_produce<SR_ITER_EVEN>(g, d, q, s, K, 0, gstep, pre, q.nsteps, islot);
       gstep += (uint32_t)q.nsteps;
     }
     return;
@@ -661,6 +692,35 @@ __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K
     // field stores of this iteration -> visible to the other CTAs' TMA reads after the barrier
     fence_proxy_async_global();
     __threadfence();
+    if (rows) {
+      // row slabs: this CTA's output columns of the rows it owns among the 4 boundary rows of each
+      // slab edge (r_{i+1} and pd_i) go straight into the neighbour's inbox (the next gather's
+      // stamp publishes them); a ragged last chunk may own only part of an edge band
+      const int rank = d.dist.rank, world = d.dist.world;
+      const int lo_a = max(q.j0, g.y0), lo_b = min(q.j1, g.y0 + SLAB_HALO);          // band below
+      const int hi_a = max(q.j0, g.y1 - SLAB_HALO), hi_b = min(q.j1, g.y1);          // band above
+      const bool lo_edge = rank > 0 && lo_a < lo_b, hi_edge = rank < world - 1 && hi_a < hi_b;
+      if (lo_edge || hi_edge) {
+        compute_bar(NCT);                    // every thread's row stores precede the copies
+        const int slot = (int)((*x.seqbase + (unsigned long long)it + 1ull) & 1ull);
+        if (q.out) {
+          for (int side = 0; side < 2; ++side) {
+            if (side == 0 ? !lo_edge : !hi_edge) continue;
+            double* inbox = d.dist.halo_in[side == 0 ? rank - 1 : rank + 1];
+            const int ra = side == 0 ? lo_a : hi_a, rb = side == 0 ? lo_b : hi_b;
+            const int rbase = side == 0 ? g.y0 : g.y1 - SLAB_HALO;
+            for (int vec = 0; vec < 2; ++vec) {
+              const double* src = (vec == 0 ? d.r[1 - parity] : d.u[parity]) + q.fk;
+              for (int row = ra; row < rb; ++row) {
+                const double2 v = __ldcg(reinterpret_cast<const double2*>(src + (long long)row * g.nt + q.gl));
+                *reinterpret_cast<double2*>(inbox + halo_ofs(slot, 1 - side, vec, K, q.k, row - rbase, g.nt) + q.gl) = v;
+              }
+            }
+          }
+          __threadfence_system();
+        }
+      }
+    }
     // fixed-order block reduction (the same as k_sr's, so both give bitwise the same partials)
     double v[3] = {a_rr, a_g, a_d};
     warp_tree_sum<3>(v, x.wpart);
@@ -693,15 +753,56 @@ __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K
       for (int i = q.tid; i < np; i += NCT) x.pbuf[i] = __ldcg(part + i);
     }
     compute_bar(NCT);
+    double* red = x.red;
     for (int i = q.tid; i < 4 * K; i += NCT) {
       const double* src = x.pbuf + (size_t)i * ncta;
       double a = 0.0;
       for (int b = 0; b < ncta; ++b) a += src[b];
-      x.red[i] = a;
+      red[i] = a;
     }
     compute_bar(NCT);
+    int kofs = 0;
+    if (dist) {
+      // warp 0 of CTA 0 pushes this rank's sums to every rank (peer memory, release stamp);
+      // every CTA waits for all ranks' stamps itself and reads the blocks from its own buffer
+      const int km = d.dist.kmax_local;
+      const unsigned long long stamp = *x.seqbase + (unsigned long long)it + 1ull;
+      if (blockIdx.x == 0 && q.tid < 32) {
+        for (int i = q.tid; i < 4 * km; i += 32) {
+          const int qq = i / km, kk = i - qq * km;
+          d.dist.packed_local[i] = kk < K ? red[qq * K + kk] : 0.0;
+        }
+        __syncwarp();
+        p2p_push(d.dist, d.dist.packed_local, 4 * km, stamp);
+      }
+      if (q.tid == 0 && !p2p_stamps_wait(d.dist, stamp)) x.ready[1] = 2;
+      compute_bar(NCT);
+      if (x.ready[1]) break;
+      const int W = d.dist.world;
+      if (d.dist.rows == 1) {
+        // row slabs: every rank holds all K conditions; add the ranks' sums in rank order
+        for (int i = q.tid; i < 4 * K; i += NCT) {
+          const int qq = i / K, kk = i - qq * K;
+          double a = 0.0;
+          for (int r = 0; r < W; ++r) a += p2p_block(d.dist, stamp, r, qq * km + kk);
+          x.red2[i] = a;
+        }
+      } else {
+        // condition sharding: the ranks' blocks in global condition order
+        kofs = d.dist.kofs;
+        for (int kg = q.tid; kg < Kall; kg += NCT) {
+          int r, kl;
+          dist_owner(kg, Kall, W, &r, &kl);
+          for (int qq = 0; qq < 4; ++qq) x.red2[qq * Kall + kg] = p2p_block(d.dist, stamp, r, qq * km + kl);
+        }
+      }
+      compute_bar(NCT);
+      if (blockIdx.x == 0)
+        for (int kg = q.tid; kg < Kall; kg += NCT) d.dist.rr_all[kg] = x.red2[kg];
+      red = x.red2;
+    }
     if (q.tid == 0) {
-      sr_scalar_stage<false>(x.cs, x.st, x.red, K, K, 0, 0, 0ull, stage_prefetch(x.cs, x.st));
+      sr_scalar_stage<false>(x.cs, x.st, red, Kall, K, kofs, 0, 0ull, stage_prefetch(x.cs, x.st));
       __threadfence_block();
       x.ready[0] = it + 1;                  // the producer may go on (or stop)
     }
@@ -718,7 +819,7 @@ __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K
     }
     if (q.tid == 0) {
       SolverState st = *x.st;
-      if (x.ready[1]) { st.done = 1; st.status = -9; }   // GMAF_E_CUDA: grid barrier timeout
+      if (x.ready[1]) { st.done = 1; st.status = -9; }   // GMAF_E_CUDA: barrier or peer timeout
       *d.st_ = st;
       const unsigned long long t1 = globaltimer();
       const int iters = st.iter - it0;
@@ -732,6 +833,9 @@ __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K
   }
 }
 
+// conditions the scalar stage sees: all of the joint system when condition-sharded
+static int srp_kall(const DevPtrs& d, int K) { return d.dist.world > 0 && d.dist.rows != 1 ? d.dist.kglob : K; }
+
 // The split seam variant (see sr_compute) pays off for long row chunks only.
 bool srp_split_seam(const TileCfg& t) {
   if (const char* e = std::getenv("GMAF_SEAM_SPLIT")) return std::atoi(e) != 0;   // A/B experiments
@@ -741,12 +845,13 @@ bool srp_split_seam(const TileCfg& t) {
 cudaError_t launch_sr_persistent(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,
                                  cudaStream_t s) {
   const bool split = srp_split_seam(t);
+  const bool dist = d.dist.world > 0;
   cudaError_t e = cudaMemsetAsync(d.counters + kCtrGridBar, 0, sizeof(unsigned int), s);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(t.n_tiles * K);
   cfg.blockDim = dim3(sr_threads(t));
-  cfg.dynamicSmemBytes = srp_smem_bytes(2 * sr_pairs(t), K, t.n_tiles * K);
+  cfg.dynamicSmemBytes = srp_smem_bytes(2 * sr_pairs(t), K, t.n_tiles * K, srp_kall(d, K));
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;   // every CTA resident (the grid barrier needs it)
@@ -755,19 +860,27 @@ cudaError_t launch_sr_persistent(const GridParams& g, const DevPtrs& d, const Ti
   cfg.numAttrs = 1;
   switch (precond) {
     case SPC_ASSOR2:
-      return split ? cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, true>, g, d, t, K)
-                   : cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, false>, g, d, t, K);
-    case SPC_ASSOR1: return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR1, false>, g, d, t, K);
-    case SPC_JACOBI: return cudaLaunchKernelEx(&cfg, k_srp<SPC_JACOBI, false>, g, d, t, K);
-    default: return cudaLaunchKernelEx(&cfg, k_srp<SPC_NONE, false>, g, d, t, K);
+      if (dist) return split ? cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, true, true>, g, d, t, K)
+                             : cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, false, true>, g, d, t, K);
+      return split ? cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, true, false>, g, d, t, K)
+                   : cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, false, false>, g, d, t, K);
+    case SPC_ASSOR1:
+      return dist ? cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR1, false, true>, g, d, t, K)
+                  : cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR1, false, false>, g, d, t, K);
+    case SPC_JACOBI:
+      return dist ? cudaLaunchKernelEx(&cfg, k_srp<SPC_JACOBI, false, true>, g, d, t, K)
+                  : cudaLaunchKernelEx(&cfg, k_srp<SPC_JACOBI, false, false>, g, d, t, K);
+    default:
+      return dist ? cudaLaunchKernelEx(&cfg, k_srp<SPC_NONE, false, true>, g, d, t, K)
+                  : cudaLaunchKernelEx(&cfg, k_srp<SPC_NONE, false, false>, g, d, t, K);
   }
 }
 
 // resident CTAs per SM of the persistent kernel with K conditions (0: it does not fit)
-int srp_ctas_per_sm(const TileCfg& t, int K) {
+int srp_ctas_per_sm(const TileCfg& t, int K, int Kall) {
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_srp<SPC_ASSOR2, false>, sr_threads(t),
-                                                    srp_smem_bytes(2 * sr_pairs(t), K, t.n_tiles * K)) != cudaSuccess)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_srp<SPC_ASSOR2, false, true>, sr_threads(t),
+                                                    srp_smem_bytes(2 * sr_pairs(t), K, t.n_tiles * K, Kall)) != cudaSuccess)
     return 0;
   return n;
 }
@@ -1087,19 +1200,24 @@ cudaError_t configure_sr_kernels(const TileCfg& t, int K) {
   if (e == cudaSuccess) e = sr_set_modes<SR_ITER_ODD>(cap);
   if (e == cudaSuccess) e = sr_set_modes<SR_INIT_COLD>(cap);
   if (e == cudaSuccess) e = sr_set_modes<SR_INIT_WARM>(cap);
-  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2, true>, cap);
-  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2, false>, cap);
-  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR1, false>, cap);
-  if (e == cudaSuccess) e = sr_set(k_srp<SPC_JACOBI, false>, cap);
-  if (e == cudaSuccess) e = sr_set(k_srp<SPC_NONE, false>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2, true, false>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2, false, false>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR1, false, false>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_JACOBI, false, false>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_NONE, false, false>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2, true, true>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2, false, true>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR1, false, true>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_JACOBI, false, true>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_NONE, false, true>, cap);
   (void)K;
   if (e == cudaSuccess) done |= 1u << dev;
   return e;
 }
 
 // whether the persistent kernel fits this context (its extra shared memory grows with K)
-bool srp_fits(const TileCfg& t, int K) {
-  return (long long)srp_smem_bytes(2 * sr_pairs(t), K, t.n_tiles * K) <= smem_optin_max() - 1024;
+bool srp_fits(const TileCfg& t, int K, int Kall) {
+  return (long long)srp_smem_bytes(2 * sr_pairs(t), K, t.n_tiles * K, Kall) <= smem_optin_max() - 1024;
 }
 
 int sr_ctas_per_sm(const TileCfg& t) {

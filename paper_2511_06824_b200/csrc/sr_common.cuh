@@ -383,6 +383,51 @@ __device__ __forceinline__ void warps_in_order(double (&v)[NV], const double* wb
   }
 }
 
+// The two halves of p2p_gather for the persistent kernel, where ONE warp pushes and EVERY CTA
+// waits for and reads the gathered blocks itself (no second hop through a local broadcast).
+// p2p_push: this rank's n doubles into slot `rank` of every rank's buffer (parity slot of
+// `stamp`), then the stamp with release semantics at system scope; advances *dd.seq.  One warp.
+__device__ __forceinline__ void p2p_push(const DistPtrs& dd, const double* src, int n, unsigned long long stamp) {
+  const int lane = threadIdx.x & 31;
+  const int W = dd.world;
+  const int par = (int)(stamp & 1ull);
+  for (int i = lane; i < W * n; i += 32) {
+    const int r = i / n, qi = i - r * n;
+    double* slot = reinterpret_cast<double*>(dd.peer[r] + 2 * W * 8) + ((long long)par * W + dd.rank) * dd.xs;
+    *reinterpret_cast<volatile double*>(slot + qi) = src[qi];
+  }
+  __threadfence_system();
+  __syncwarp();
+  if (lane < W) {
+    unsigned long long* fl = reinterpret_cast<unsigned long long*>(dd.peer[lane]) + par * W + dd.rank;
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(fl), "l"(stamp) : "memory");
+  }
+  if (lane == 0) *dd.seq = stamp;
+}
+// p2p_stamps_wait: every rank's stamp >= `stamp` in the own buffer (acquire, system scope), then
+// a system-scope fence; one thread.  false on timeout.
+__device__ __forceinline__ bool p2p_stamps_wait(const DistPtrs& dd, unsigned long long stamp) {
+  const int par = (int)(stamp & 1ull);
+  const unsigned long long t0 = globaltimer();
+  for (int r = 0; r < dd.world; ++r) {
+    const unsigned long long* fl = reinterpret_cast<const unsigned long long*>(dd.peer[dd.rank]) + par * dd.world + r;
+    for (;;) {
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(fl) : "memory");
+      if (v >= stamp) break;
+      if ((long long)(globaltimer() - t0) > kP2PTimeoutNs) return false;
+    }
+  }
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  return true;
+}
+// element qi of rank r's block of the gather `stamp`, from the own exchange buffer
+__device__ __forceinline__ double p2p_block(const DistPtrs& dd, unsigned long long stamp, int r, int qi) {
+  const int par = (int)(stamp & 1ull);
+  const double* data = reinterpret_cast<const double*>(dd.peer[dd.rank] + 2 * dd.world * 8);
+  return __ldcg(data + ((long long)par * dd.world + r) * dd.xs + qi);
+}
+
 // Per-CTA partials -> fixed-order per-condition sums in the last CTA -> the scalar stage
 // (multi-rank: the packed sums for the allgather).  Every thread of the CTA calls it; `red`
 // is dead shared memory of >= max(4 * (blockDim + 32), 4 * K) doubles.

@@ -67,11 +67,9 @@ def connect_p2p(solver, group=None) -> None:
     # every rank's GPU must be peer-accessible from this one (the exchange kernels load and store
     # the peers' buffers over NVLink); fail loudly before connecting otherwise
     devs = [None] * solver.world
-    dist.all_gather_object(devs, (torch.cuda.get_device_properties(solver.device).uuid.hex
-                                  if hasattr(torch.cuda.get_device_properties(solver.device), "uuid") else None,
-                                  solver.device.index), group=group)
+    dist.all_gather_object(devs, solver.device.index, group=group)
     mine = solver.device.index
-    for r, (_, d) in enumerate(devs):
+    for r, d in enumerate(devs):
         if d is not None and d != mine and not torch.cuda.can_device_access_peer(mine, d):
             raise RuntimeError(f"rank {solver.rank}: GPU {mine} cannot access rank {r}'s GPU {d} peer to peer "
                                "(NVLink/P2P required by the peer-to-peer exchange)")

@@ -404,8 +404,8 @@ __device__ __forceinline__ void p2p_push(const DistPtrs& dd, const double* src, 
   }
   if (lane == 0) *dd.seq = stamp;
 }
-// p2p_stamps_wait: every rank's stamp >= `stamp` in the own buffer (acquire, system scope), then
-// a system-scope fence; one thread.  false on timeout.
+// p2p_stamps_wait: every rank's stamp >= `stamp` in the own buffer (acquire, system scope); one
+// thread, followed by a barrier of the threads that read the blocks.  false on timeout.
 __device__ __forceinline__ bool p2p_stamps_wait(const DistPtrs& dd, unsigned long long stamp) {
   const int par = (int)(stamp & 1ull);
   const unsigned long long t0 = globaltimer();
@@ -418,8 +418,7 @@ __device__ __forceinline__ bool p2p_stamps_wait(const DistPtrs& dd, unsigned lon
       if ((long long)(globaltimer() - t0) > kP2PTimeoutNs) return false;
     }
   }
-  asm volatile("fence.acq_rel.sys;" ::: "memory");
-  return true;
+  return true;   // the caller's CTA barrier orders its threads' block reads after these acquires
 }
 // element qi of rank r's block of the gather `stamp`, from the own exchange buffer
 __device__ __forceinline__ double p2p_block(const DistPtrs& dd, unsigned long long stamp, int r, int qi) {

@@ -12,13 +12,16 @@
 namespace gmaf {
 
 // Dimple mask (Fig. 10; DESIGN.md R-A7): integer arithmetic only.
+// 32-bit unsigned arithmetic: the host rejects meshes whose products could reach 2^32
+// (check_grid), so the same integers as the oracle's int64 evaluation, without 64-bit divisions.
 __device__ __forceinline__ bool texture_mask(const GridParams& g, int i, int j) {
   if (g.tex_nt <= 0 || g.tex_ny <= 0) return false;
   if (j < 0 || j >= g.tex_band) return false;
-  const long long nt = g.nt, B = g.tex_band, N = g.tex_num, D = g.tex_den;
-  const long long ci = ((long long)i * (long long)g.tex_nt) % nt;
-  const long long cj = ((long long)j * (long long)g.tex_ny) % B;
-  return (D * ci < N * nt) && (D * cj < N * B);
+  const unsigned nt = (unsigned)g.nt, B = (unsigned)g.tex_band, N = (unsigned)g.tex_num, D = (unsigned)g.tex_den;
+  const unsigned ci = ((unsigned)i * (unsigned)g.tex_nt) % nt;
+  const unsigned cj = ((unsigned)j * (unsigned)g.tex_ny) % B;
+  return ((unsigned long long)D * ci < (unsigned long long)N * nt) &&
+         ((unsigned long long)D * cj < (unsigned long long)N * B);
 }
 
 // Eq. 2.3 at node (i, j), j in [-1, n_y]; also returns the rate (Eq. 2.2, chain rule).
@@ -76,47 +79,64 @@ __global__ void k_thickness_guard(GridParams g, DevPtrs d, int K) {
 }
 
 // ------------------------------------------------------------------ assembly (G1)
-// One thread per (i, j, k).  Bands are written once per distinct coefficient set
-// (by its representative condition); S for every condition.
+// One thread per (column i, chunk of ASM_ROWS stored rows, condition k), marching up the column:
+// the thickness and conductance of the rows below and at the node are carried from the previous
+// row, so per node it evaluates the film at (i, j+1) and at the two theta neighbours (3 instead of
+// 5); every value is the same expression as before, so the bands stay bitwise.  Bands are written
+// once per distinct coefficient set (by its representative condition); S for every condition.
+constexpr int ASM_ROWS = 16;
+
 __global__ void k_assemble(GridParams g, DevPtrs d, int K) {
   timing_begin(d.timing, KK_ASSEMBLE);
   // the stored rows of this context (all rows on one rank; own rows + halo rows on a slab)
+  const int srows = (int)(g.ns / g.nt);
+  const int nchunks = (srows + ASM_ROWS - 1) / ASM_ROWS;
+  const long long per_k = (long long)g.nt * nchunks;
+  const long long total = per_k * K;
   const long long n = g.ns;
-  const long long total = n * K;
-  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < total;
-       q += (long long)gridDim.x * blockDim.x) {
-    const int k = (int)(q / n);
-    const long long idx = q - (long long)k * n;
-    const int j = g.yb + (int)(idx / g.nt);
-    const int i = (int)(idx % g.nt);
+  for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w < total;
+       w += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(w / per_k);
+    const long long rem = w - (long long)k * per_k;
+    const int i = (int)(rem % g.nt), ch = (int)(rem / g.nt);
+    const int ja = g.yb + ch * ASM_ROWS, jb = min(ja + ASM_ROWS, g.yb + srows);
     const CondParams& c = d.cp[k];
     const int iE = (i + 1 == g.nt) ? 0 : i + 1;
     const int iW = (i == 0) ? g.nt - 1 : i - 1;
-    const Film fP = film(g, c, d.ct, d.st, i, j, true);
-    const double hE = film(g, c, d.ct, d.st, iE, j, false).h;
-    const double hW = film(g, c, d.ct, d.st, iW, j, false).h;
-    const double hN = film(g, c, d.ct, d.st, i, j + 1, false).h;
-    const double hS = film(g, c, d.ct, d.st, i, j - 1, false).h;
-    const double gP = conductance(g, fP.h), gE = conductance(g, hE), gW = conductance(g, hW);
-    const double gN = conductance(g, hN), gS = conductance(g, hS);
-    const double ge = harmonic(gP, gE);
-    const double gw = harmonic(gW, gP);   // == ge(iW, j) bit for bit
-    const double gn = harmonic(gP, gN);
-    const double gs = harmonic(gS, gP);   // == gn(i, j-1) bit for bit
-    const double aE = ge * c.rx, aW = gw * c.rx, aN = gn * c.ry, aS = gs * c.ry;
-    if (d.mat_rep[c.mat] == k) {
-      const long long o = (long long)c.mat * n + idx;   // = fofs(g, mat) + j*nt + i
-      d.AP[o] = ((aW + aE) + aS) + aN;
-      d.AE[o] = -aE;
-      d.AN[o] = (j < g.ny - 1) ? -aN : 0.0;
+    const bool rep = d.mat_rep[c.mat] == k;
+    double hS = film(g, c, d.ct, d.st, i, ja - 1, false).h;
+    Film fP = film(g, c, d.ct, d.st, i, ja, true);
+    double gS = conductance(g, hS), gP = conductance(g, fP.h);
+    for (int j = ja; j < jb; ++j) {
+      const Film fN = film(g, c, d.ct, d.st, i, j + 1, true);
+      const double hE = film(g, c, d.ct, d.st, iE, j, false).h;
+      const double hW = film(g, c, d.ct, d.st, iW, j, false).h;
+      const double hN = fN.h;
+      const double gN = conductance(g, hN);
+      const long long idx = (long long)(j - g.yb) * g.nt + i;
+      if (rep) {
+        // the bands: only the representative condition of a coefficient set needs them
+        const double gE = conductance(g, hE), gW = conductance(g, hW);
+        const double ge = harmonic(gP, gE);
+        const double gw = harmonic(gW, gP);   // == ge(iW, j) bit for bit
+        const double gn = harmonic(gP, gN);
+        const double gs = harmonic(gS, gP);   // == gn(i, j-1) bit for bit
+        const double aE = ge * c.rx, aW = gw * c.rx, aN = gn * c.ry, aS = gs * c.ry;
+        const long long o = (long long)c.mat * n + idx;   // = fofs(g, mat) + j*nt + i
+        d.AP[o] = ((aW + aE) + aS) + aN;
+        d.AE[o] = -aE;
+        d.AN[o] = (j < g.ny - 1) ? -aN : 0.0;
+      }
+      const double t1 = ((c.Ut * 0.5) * ((hE - hW) * 0.5)) * c.dy;
+      const double t2 = ((c.Uy * 0.5) * ((hN - hS) * 0.5)) * c.dx;
+      const double t3 = (fP.hd * c.dx) * c.dy;
+      double sv = -((t1 + t2) + t3);
+      if (j == 0) sv = sv + (harmonic(gS, gP) * c.ry) * c.pin;          // Dirichlet fold, aS p_in
+      if (j == g.ny - 1) sv = sv + (harmonic(gP, gN) * c.ry) * c.pout;  // aN p_out
+      d.S[(long long)k * n + idx] = sv;
+      hS = fP.h; gS = gP;
+      fP = fN; gP = gN;
     }
-    const double t1 = ((c.Ut * 0.5) * ((hE - hW) * 0.5)) * c.dy;
-    const double t2 = ((c.Uy * 0.5) * ((hN - hS) * 0.5)) * c.dx;
-    const double t3 = (fP.hd * c.dx) * c.dy;
-    double s = -((t1 + t2) + t3);
-    if (j == 0) s = s + aS * c.pin;
-    if (j == g.ny - 1) s = s + aN * c.pout;
-    d.S[(long long)k * n + idx] = s;
   }
   if (last_cta_arrive(&d.counters[KK_ASSEMBLE], gridDim.x) && threadIdx.x == 0)
     timing_end(d.timing, KK_ASSEMBLE);
@@ -138,7 +158,15 @@ __global__ void k_field(GridParams g, DevPtrs d, int field, int k) {
 // p_in / p_out).  Pressure traction -p n and Couette-Poiseuille wall shear on the
 // piston; moments about the bottom centre (DESIGN.md R-A14).
 constexpr int QUAD_THREADS = 256;
+constexpr int QUAD_ROWS = 32;    // cell rows per thread (a column marches over them)
 
+__device__ __forceinline__ double node_p(const CondParams& c, const double* p, int ny, int nt, int i, int j) {
+  return j < 0 ? c.pin : (j >= ny ? c.pout : p[(long long)j * nt + i]);
+}
+
+// One thread per (column i, chunk of QUAD_ROWS cell rows): it marches up its column carrying the
+// node values h and p of the lower cell row, so each node's thickness is evaluated once per
+// thread (2 per cell instead of 4).
 __global__ void __launch_bounds__(QUAD_THREADS) k_quadrature(GridParams g, DevPtrs d, int K) {
   __shared__ double red[12 * (QUAD_THREADS + 32)];
   timing_begin(d.timing, KK_QUAD);
@@ -148,43 +176,46 @@ __global__ void __launch_bounds__(QUAD_THREADS) k_quadrature(GridParams g, DevPt
   // this context's cells: j + 1 in [y0, y1), plus the top ghost cell j = n_y - 1 on the last slab
   // (all n_y + 1 cell rows on one rank); row y0 - 1 of a slab is its exchanged halo row
   const int cj0 = g.y0 - 1;
-  const long long cells = (long long)(g.y1 - g.y0 + (g.y1 == g.ny ? 1 : 0)) * g.nt;
+  const int crows = g.y1 - g.y0 + (g.y1 == g.ny ? 1 : 0);
+  const int nchunks = (crows + QUAD_ROWS - 1) / QUAD_ROWS;
+  const long long columns = (long long)g.nt * nchunks;
   const double dA = c.dx * c.dy;
   double acc[12];
 #pragma unroll
   for (int q = 0; q < 12; ++q) acc[q] = 0.0;
-  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < cells;
-       q += (long long)gridDim.x * blockDim.x) {
-    const int j = cj0 + (int)(q / g.nt), i = (int)(q % g.nt);
+  for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w < columns;
+       w += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(w % g.nt), ch = (int)(w / g.nt);
     const int i1 = (i + 1 == g.nt) ? 0 : i + 1;
-    const double p00 = (j < 0) ? c.pin : p[(long long)j * g.nt + i];
-    const double p10 = (j < 0) ? c.pin : p[(long long)j * g.nt + i1];
-    const double p01 = (j + 1 >= g.ny) ? c.pout : p[(long long)(j + 1) * g.nt + i];
-    const double p11 = (j + 1 >= g.ny) ? c.pout : p[(long long)(j + 1) * g.nt + i1];
-    const double h00 = film(g, c, d.ct, d.st, i, j, false).h;
-    const double h10 = film(g, c, d.ct, d.st, i1, j, false).h;
-    const double h01 = film(g, c, d.ct, d.st, i, j + 1, false).h;
-    const double h11 = film(g, c, d.ct, d.st, i1, j + 1, false).h;
-    const double pb = (((p00 + p10) + p01) + p11) * 0.25;
-    const double hb = (((h00 + h10) + h01) + h11) * 0.25;
-    const double dpdx = ((p10 + p11) - (p00 + p01)) / (2.0 * c.dx);
-    const double dpdy = ((p01 + p11) - (p00 + p10)) / (2.0 * c.dy);
-    const double y0 = (double)(j + 1) * c.dy, y1 = (double)(j + 2) * c.dy;
-    const double yc = (y0 + y1) * 0.5;
+    const int ja = cj0 + ch * QUAD_ROWS, jb = min(ja + QUAD_ROWS, cj0 + crows);
     const double cc = d.cth[i], sc = d.sth[i];
-    const double rx = g.Rk * cc, ry = g.Rk * sc, rz = yc;
-    const double fx = -pb * cc * dA, fy = -pb * sc * dA;
-    acc[0] += fx; acc[1] += fy;
-    acc[3] += -rz * fy;
-    acc[4] += rz * fx;
-    acc[5] += rx * fy - ry * fx;
-    const double tth = -(hb * 0.5) * dpdx - (g.mu * c.Ut) / hb;
-    const double ty = -(hb * 0.5) * dpdy - (g.mu * c.Uy) / hb;
-    const double sx = -tth * sc * dA, sy = tth * cc * dA, sz = ty * dA;
-    acc[6] += sx; acc[7] += sy; acc[8] += sz;
-    acc[9] += ry * sz - rz * sy;
-    acc[10] += rz * sx - rx * sz;
-    acc[11] += rx * sy - ry * sx;
+    const double rx = g.Rk * cc, ry = g.Rk * sc;
+    double p00 = node_p(c, p, g.ny, g.nt, i, ja), p10 = node_p(c, p, g.ny, g.nt, i1, ja);
+    double h00 = film(g, c, d.ct, d.st, i, ja, false).h, h10 = film(g, c, d.ct, d.st, i1, ja, false).h;
+    for (int j = ja; j < jb; ++j) {
+      const double p01 = node_p(c, p, g.ny, g.nt, i, j + 1), p11 = node_p(c, p, g.ny, g.nt, i1, j + 1);
+      const double h01 = film(g, c, d.ct, d.st, i, j + 1, false).h;
+      const double h11 = film(g, c, d.ct, d.st, i1, j + 1, false).h;
+      const double pb = (((p00 + p10) + p01) + p11) * 0.25;
+      const double hb = (((h00 + h10) + h01) + h11) * 0.25;
+      const double dpdx = ((p10 + p11) - (p00 + p01)) / (2.0 * c.dx);
+      const double dpdy = ((p01 + p11) - (p00 + p10)) / (2.0 * c.dy);
+      const double y0 = (double)(j + 1) * c.dy, y1 = (double)(j + 2) * c.dy;
+      const double rz = (y0 + y1) * 0.5;
+      const double fx = -pb * cc * dA, fy = -pb * sc * dA;
+      acc[0] += fx; acc[1] += fy;
+      acc[3] += -rz * fy;
+      acc[4] += rz * fx;
+      acc[5] += rx * fy - ry * fx;
+      const double tth = -(hb * 0.5) * dpdx - (g.mu * c.Ut) / hb;
+      const double ty = -(hb * 0.5) * dpdy - (g.mu * c.Uy) / hb;
+      const double sx = -tth * sc * dA, sy = tth * cc * dA, sz = ty * dA;
+      acc[6] += sx; acc[7] += sy; acc[8] += sz;
+      acc[9] += ry * sz - rz * sy;
+      acc[10] += rz * sx - rx * sz;
+      acc[11] += rx * sy - ry * sx;
+      p00 = p01; p10 = p11; h00 = h01; h10 = h11;
+    }
   }
   block_sum<12>(acc, red);
   const int ncta = gridDim.x;
@@ -219,7 +250,7 @@ cudaError_t launch_thickness_guard(const GridParams& g, const DevPtrs& d, int K,
 }
 
 cudaError_t launch_assemble(const GridParams& g, const DevPtrs& d, int K, cudaStream_t s) {
-  const long long work = g.ns * K;
+  const long long work = (long long)g.nt * ((g.ns / g.nt + ASM_ROWS - 1) / ASM_ROWS) * K;
   k_assemble<<<grid_for(work, 256, 148 * 16), 256, 0, s>>>(g, d, K);
   return cudaGetLastError();
 }
@@ -231,8 +262,8 @@ cudaError_t launch_field(const GridParams& g, const DevPtrs& d, int field, int k
 }
 
 int quad_ctas_per_condition(const GridParams& g, int K) {
-  const long long cells = (long long)(g.y1 - g.y0 + 1) * g.nt;
-  int per_k = grid_for(cells, QUAD_THREADS, 1 << 20);
+  const long long columns = (long long)((g.y1 - g.y0 + 1 + QUAD_ROWS - 1) / QUAD_ROWS) * g.nt;
+  int per_k = grid_for(columns, QUAD_THREADS, 1 << 20);
   const int target = (148 * 8 + K - 1) / K;   // ~8 CTAs per SM in total
   if (per_k > target) per_k = target;
   return per_k < 1 ? 1 : per_k;

@@ -163,6 +163,10 @@ int check_grid(const gmaf_grid* g) {
         g->tex_depth < 0.0)
       return GMAF_E_INVALID_ARG;
     if (g->n_theta < 2 * g->tex_n_theta || g->tex_band_rows < 2 * g->tex_n_y) return GMAF_E_MESH_TOO_COARSE;
+    // the device evaluates the mask in 32-bit unsigned arithmetic (geometry.cu texture_mask)
+    if ((unsigned long long)g->n_theta * (unsigned long long)g->tex_n_theta >= (1ull << 32) ||
+        (unsigned long long)g->tex_band_rows * (unsigned long long)g->tex_n_y >= (1ull << 32))
+      return GMAF_E_INVALID_ARG;
   }
   return GMAF_OK;
 }

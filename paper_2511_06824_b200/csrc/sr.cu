@@ -860,8 +860,8 @@ cudaError_t launch_sr_persistent(const GridParams& g, const DevPtrs& d, const Ti
   cfg.numAttrs = 1;
   switch (precond) {
     case SPC_ASSOR2:
-      if (dist) return split ? cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, true, true>, g, d, t, K)
-                             : cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, false, true>, g, d, t, K);
+      // (the multi-rank kernel keeps one loop: with the split loops it spills in the row loop)
+      if (dist) return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, false, true>, g, d, t, K);
       return split ? cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, true, false>, g, d, t, K)
                    : cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, false, false>, g, d, t, K);
     case SPC_ASSOR1:
@@ -1205,7 +1205,6 @@ cudaError_t configure_sr_kernels(const TileCfg& t, int K) {
   if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR1, false, false>, cap);
   if (e == cudaSuccess) e = sr_set(k_srp<SPC_JACOBI, false, false>, cap);
   if (e == cudaSuccess) e = sr_set(k_srp<SPC_NONE, false, false>, cap);
-  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2, true, true>, cap);
   if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2, false, true>, cap);
   if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR1, false, true>, cap);
   if (e == cudaSuccess) e = sr_set(k_srp<SPC_JACOBI, false, true>, cap);

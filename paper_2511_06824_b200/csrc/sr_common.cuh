@@ -396,7 +396,9 @@ __device__ __forceinline__ void p2p_push(const DistPtrs& dd, const double* src, 
     double* slot = reinterpret_cast<double*>(dd.peer[r] + 2 * W * 8) + ((long long)par * W + dd.rank) * dd.xs;
     *reinterpret_cast<volatile double*>(slot + qi) = src[qi];
   }
-  __threadfence_system();
+  // no per-lane system fence: the warp barrier orders every lane's block stores before lane r's
+  // release store of the stamp, and a release is cumulative (it publishes the writes that
+  // happen before it in causality order, the other lanes' included)
   __syncwarp();
   if (lane < W) {
     unsigned long long* fl = reinterpret_cast<unsigned long long*>(dd.peer[lane]) + par * W + dd.rank;

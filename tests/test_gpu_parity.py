@@ -304,6 +304,8 @@ def test_converged_vs_full_oracle_solve(P, gi, name):
     ks, js, is_ = smp[:, 0].astype(int), smp[:, 1].astype(int), smp[:, 2].astype(int)
     pg = np.stack([S.get("p", k) for k in range(9)])
     assert rel(pg[ks, js, is_], smp[:, 3]) <= 1e-8
+    # node by node as well (a relative L2 over the samples could hide a local error)
+    assert np.max(np.abs(pg[ks, js, is_] - smp[:, 3])) <= 1e-8 * np.max(np.abs(smp[:, 3]))
     for k in range(9):
         assert abs(np.linalg.norm(pg[k]) - gold["p_norm"][k]) <= 1e-8 * gold["p_norm"][k]
         wo = np.array(gold["wrench"][k])
@@ -639,3 +641,24 @@ def test_persistent_equals_per_launch_kernels(P, gi, monkeypatch, case):
     assert np.array_equal(pa, pb)
     assert fxa.iterations == fxb.iterations == 9
     assert np.array_equal(Wa, Wb)
+
+
+def test_launch_configuration_and_balance_diagnostics(P, gi, monkeypatch):
+    """gmaf_tile_config reports the launch the bench times (C3: 4 strips of 512 columns x 4 chunks of
+    256 rows x 9 conditions = 144 CTAs, one persistent launch); with GMAF_DIAG the persistent kernel
+    records every CTA's arrival at every grid barrier (gmaf_cta_arrivals), ordered in time."""
+    monkeypatch.setenv("GMAF_DIAG", "1")
+    cfg = gi.config("C3")
+    S = P.JointSolver(cfg.grid, 9, max_matrices=5)
+    t = S.tile_config()
+    assert (t["tw"], t["n_strips"], t["n_chunks"], t["n_ctas"], t["schedule"], t["persistent"]) == \
+        (512, 4, 4, 144, "single", True)
+    S.thickness(cfg.conds)
+    S.assemble()
+    S.solve_fixed(12, omega=cfg.omega)
+    A = S.cta_arrivals()
+    S.close()
+    assert A.shape == (32, 144)
+    lat = A[:12].astype(np.float64)
+    assert np.all(lat > 0) and np.all(np.diff(lat.max(axis=1)) > 0)     # iteration after iteration
+    assert np.all(lat[1:].min(axis=1) >= lat[:-1].max(axis=1))         # a barrier separates them

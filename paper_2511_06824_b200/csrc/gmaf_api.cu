@@ -9,6 +9,7 @@
 #include <dlfcn.h>
 #include <nccl.h>   // types only: NCCL is resolved at run time (world == 1 needs no NCCL)
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -132,7 +133,6 @@ TileCfg make_tiles(int nt, int ny, int K, int slots, int tw) {
   return t;
 }
 
-constexpr int kMaxTilesPerCondition = 148 * 16;
 
 // strip widths: two-phase kernels 256/128 columns; the single-pass kernel keeps the seam
 // inside a strip, so its strips may not be wider than the ring (and need >= 12 columns)
@@ -830,10 +830,11 @@ gmaf_status gmaf_create(const gmaf_grid* grid, int32_t K, const gmaf_dist* dist,
     ctx->persist_ok = want && (!dm || p2p_ctx) && single_ok(grid->n_theta) && ctx->sr_k_ok &&
                       srp_fits(ctx->tiles_sr, K, Kall) &&
                       (long long)srp_ctas_per_sm(ctx->tiles_sr, K, Kall) * sms >= (long long)ctx->tiles_sr.n_tiles * K;
-    // diagnostics (gmaf_cta_arrivals): the arrival stamps live after the persistent kernel's two
-    // partial-sum buffers inside the partials region (4 K kMaxTilesPerCondition doubles)
+    // diagnostics (gmaf_cta_arrivals): the arrival stamps live at the end of the partials region,
+    // clear of every kernel's partial sums (diag_offset)
     gp.diag = (std::getenv("GMAF_DIAG") && ctx->persist_ok &&
-               (8 + kDiagIters) * ctx->tiles_sr.n_tiles <= 4 * kMaxTilesPerCondition) ? 1 : 0;
+               diag_offset(K, ctx->tiles_sr.n_tiles * K) >=
+                   (long long)8 * K * std::max(ctx->tiles_sr.n_tiles, ctx->tiles.n_tiles)) ? 1 : 0;
   }
   if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) return cleanup_fail(GMAF_E_CUDA);
   ctx->quad_ctas = quad_ctas_per_condition(gp, K);
@@ -1199,7 +1200,7 @@ gmaf_status gmaf_cta_arrivals(gmaf_ctx* ctx, uint64_t* out, int32_t n, int32_t* 
   if (!ctx->gp.diag || !ctx->persist_ok) return GMAF_OK;
   const int nblk = ctx->tiles_sr.n_tiles * ctx->K;
   const int m = kDiagIters * nblk < n ? kDiagIters * nblk : n;
-  const double* base = ctx->d.partials + (size_t)8 * ctx->K * ctx->tiles_sr.n_tiles;
+  const double* base = ctx->d.partials + diag_offset(ctx->K, nblk);
   CU(cudaMemcpyAsync(out, base, (size_t)m * 8, cudaMemcpyDeviceToHost, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   *count = m;

@@ -36,7 +36,13 @@ struct GridParams {
 };
 
 constexpr int SLAB_HALO = 4;
-constexpr int kDiagIters = 32;   // iterations whose per-CTA arrival times are recorded (diag mode)   // halo rows per side: the y dependency radius of A M^-1 A M^-1
+constexpr int kDiagIters = 32;   // iterations whose per-CTA arrival times are recorded (diag mode)
+constexpr int kMaxTilesPerCondition = 148 * 16;   // partials region: 4 K kMaxTilesPerCondition doubles
+// diag mode: the arrival stamps occupy the END of the partials region (the per-launch, persistent
+// and true-residual partial sums use its beginning)
+__host__ __device__ __forceinline__ long long diag_offset(int K, int nblk) {
+  return (long long)4 * K * kMaxTilesPerCondition - (long long)kDiagIters * nblk;
+}   // halo rows per side: the y dependency radius of A M^-1 A M^-1
 
 // Offset of (condition k, global row 0, column 0) in a [K][stored rows][nt] field.
 __host__ __device__ __forceinline__ long long fofs(const GridParams& g, int k) {

@@ -308,7 +308,7 @@ __device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPt
       D2 w0;
       if constexpr (PC == SPC_NONE) w0 = r0; else w0 = {r0.l * iD0.l, r0.r * iD0.r};
       rst(w_0, tl, NTC, w0);
-      row_bar(NCT);                                         // barrier 1: w(jl) complete
+      row_bar<SEAM != SEAM_CHECK>(NCT);                                         // barrier 1: w(jl) complete
 
       // ---- (B) v1(jl) = w - (omega/D) sum_L A w  (Eq. 3.5);  (C) z(jl-1), pd(jl-1)
       D2 z1;
@@ -378,7 +378,7 @@ __device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPt
       if constexpr (PC == SPC_NONE) wz = rn2;
       else wz = {(rn2.l * oD2.l) * romega, (rn2.r * oD2.r) * romega};
       rst(w2_2, tl, NTC, wz);
-      row_bar(NCT);                                         // barrier 2: w2(jl-2) complete
+      row_bar<SEAM != SEAM_CHECK>(NCT);                                         // barrier 2: w2(jl-2) complete
 
       // ---- (E) v2(jl-2)   (F) z2(jl-3), gamma   (G) A z2 at jl-4, delta
       D2 u2_3;
@@ -658,14 +658,15 @@ __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K
         while (x.ready[0] < it && x.ready[1] == 0) __nanosleep(32);
       }
       __syncwarp();
-      const bool stop = x.ready[1] != 0 || x.st->done;
+      __threadfence_block();                 // the state written before the flag, read after it
+      const bool stop = x.ready[1] != 0 || *reinterpret_cast<volatile int32_t*>(&x.st->done) != 0;
       if (stop) {
         // drain the prefetched steps (TMA writes into this CTA's shared memory) before exiting
         if (lane == 0)
           for (int b = 0; b < pre; ++b) mbar_wait(s.full0 + 8 * ((gstep + b) & 7), (gstep / SR_UNROLL) & 1u);
         break;
       }
-      if (async && x.cs.frz[q.k]) continue;  // frozen condition: no rows this iteration
+      if (async && *reinterpret_cast<volatile int32_t*>(&x.cs.frz[q.k]) != 0) continue;   // frozen: no rows
       if (parity) sr_produce<SR_ITER_ODD>(g, d, q, s, K, 1, gstep, pre, q.nsteps, islot);
       else sr_produce<SR_ITER_EVEN>(g, d, q, s, K, 0, gstep, pre, q.nsteps, islot);
       gstep += (uint32_t)q.nsteps;
@@ -729,10 +730,10 @@ __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K
     double* part = d.partials + (size_t)(it & 1) * 4 * K * ncta;   // parity buffers
     if (q.tid == 0) {
       if (timed) tim[3] = globaltimer();
-      // load-balance diagnostics: this CTA's arrival at the grid barrier (after the persistent
-      // kernel's two partial-sum buffers in the partials region; gmaf_cta_arrivals)
+      // load-balance diagnostics: this CTA's arrival at the grid barrier (at the end of the
+      // partials region; gmaf_cta_arrivals)
       if (g.diag && it < kDiagIters)
-        reinterpret_cast<unsigned long long*>(d.partials + (size_t)8 * K * ncta)[it * nblk + blockIdx.x] = globaltimer();
+        reinterpret_cast<unsigned long long*>(d.partials + diag_offset(K, nblk))[it * nblk + blockIdx.x] = globaltimer();
       warps_in_order<3>(v, x.wpart, nw);
       for (int c = 0; c < 3; ++c) part[(size_t)(c * K + q.k) * ncta + cta] = v[c];
       part[(size_t)(3 * K + q.k) * ncta + cta] = 0.0;
@@ -836,10 +837,15 @@ __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K
 // conditions the scalar stage sees: all of the joint system when condition-sharded
 static int srp_kall(const DevPtrs& d, int K) { return d.dist.world > 0 && d.dist.rows != 1 ? d.dist.kglob : K; }
 
-// The split seam variant (see sr_compute) pays off for long row chunks only.
+// The split seam variant (see sr_compute): off by default.  With the seam warp and the other
+// warps in different loops, the row barriers must be one shared out-of-line bar.sync (an
+// .aligned barrier may not be reached from different instructions; compute-sanitizer synccheck
+// flags it), and the calls cost more than the split saves (C3: 260 vs 250 us per iteration on
+// the same box).  GMAF_SEAM_SPLIT=1 selects it for experiments.
 bool srp_split_seam(const TileCfg& t) {
-  if (const char* e = std::getenv("GMAF_SEAM_SPLIT")) return std::atoi(e) != 0;   // A/B experiments
-  return t.th >= 128;
+  (void)t;
+  if (const char* e = std::getenv("GMAF_SEAM_SPLIT")) return std::atoi(e) != 0;
+  return false;
 }
 
 cudaError_t launch_sr_persistent(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,

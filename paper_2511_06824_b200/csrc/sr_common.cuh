@@ -60,11 +60,23 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 __device__ __forceinline__ void compute_bar(int nthreads) {
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
+// The same barrier as ONE out-of-line instruction: with the split seam loops (sr.cu
+// sr_compute) the seam warp and the others run different loops, and bar.sync (= barrier.sync
+// .aligned) requires every thread to execute the same barrier instruction -- a shared callee
+// gives them the same one.
+__device__ __noinline__ void compute_bar_shared(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
 // timing-only experiment (wrong results): the row pipeline's two barriers per row compiled out
 #ifdef GMAF_EXPERIMENT_NOBAR
+template <bool SHARED = false>
 __device__ __forceinline__ void row_bar(int) { __syncwarp(); }
 #else
-__device__ __forceinline__ void row_bar(int nthreads) { compute_bar(nthreads); }
+template <bool SHARED = false>
+__device__ __forceinline__ void row_bar(int nthreads) {
+  if constexpr (SHARED) compute_bar_shared(nthreads);
+  else compute_bar(nthreads);
+}
 #endif
 // 1/a to full double precision without the IEEE-division slow path: rcp.approx (MUFU)
 // + one third-order Newton step (the solve does not need a correctly rounded D^-1).

@@ -15,4 +15,12 @@ for sched in ("single", "table1"):
         st3 = S.solve(tol=1e-8, omega=1.6, coupling="async", max_iter=20, raise_on_error=False)
     print(sched, st.iterations, st.converged, st2.iterations)
     S.close()
+# the persistent kernel's split seam loops (long row chunks; forced on a small mesh)
+os.environ["GMAF_SEAM_SPLIT"] = "1"
+g = gi.grid(96, 24, "short", tex_n_theta=8, tex_n_y=2, tex_band_rows=8)
+S = P.JointSolver(g, 3)
+st, W = S.step(gi.random_conditions(5, 3), tol=1e-8, omega=1.6, max_iter=3000)
+print("split seam", st.iterations, st.converged, S.tile_config())
+S.close()
+os.environ.pop("GMAF_SEAM_SPLIT")
 print("sanitize run done")

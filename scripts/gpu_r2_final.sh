@@ -17,3 +17,4 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/b
 python -c "
 import json; d=json.loads(open('gpurun_out/bench_final.log').read().strip().splitlines()[-1]); r=d['roofline']; k=d['kernels']
 print('bench', round(d['value']/1e9,2), 'G; ev_us', round(r['avg_launch_us_events'],1), 'frac', round(r['frac'],3), 'tail', k['tail_of_sr_iter']['avg_us'], 'wait', k.get('gridbar_wait',{}).get('avg_us'), d['iterations_per_step'], d['clocks'], 'launches', d['gpu_launches'], 'picard', round(d['picard']['ms_per_time_step'],1))"
+bash scripts/gpu_sanitize.sh

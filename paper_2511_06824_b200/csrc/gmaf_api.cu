@@ -156,6 +156,9 @@ constexpr int kConstRowLen = 1024;   // >= the widest TMA row segment (tw + 2*ha
 int check_grid(const gmaf_grid* g) {
   if (!g) return GMAF_E_INVALID_ARG;
   if (g->n_theta < 4 || g->n_y < 4) return GMAF_E_INVALID_MESH;
+  // the iteration kernels index a row of one condition's field in 32-bit arithmetic
+  // ((n_y + 8) n_theta < 2^31: 2^31 doubles = 16 GiB per condition and field)
+  if (((long long)g->n_y + 16) * (long long)g->n_theta >= (1ll << 31)) return GMAF_E_INVALID_MESH;
   if (!(g->R_k > 0.0) || !(g->R_c > g->R_k) || !(g->mu > 0.0)) return GMAF_E_INVALID_ARG;
   if (g->tex_n_theta > 0 || g->tex_n_y > 0) {
     if (g->tex_n_theta <= 0 || g->tex_n_y <= 0 || g->tex_band_rows <= 0 || g->tex_band_rows > g->n_y ||

@@ -59,10 +59,15 @@ struct SrGeo {
   long long fk;
 };
 
+// TWC > 0: the strip width as a compile-time constant (= t.tw; the persistent single-rank kernel
+// of the common widths): every shared-memory ring address is then a per-thread base plus an
+// immediate, which frees the registers and integer instructions of the runtime carve-up.
+template <int TWC = 0>
 __device__ __forceinline__ SrGeo sr_geo(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K) {
   SrGeo q;
+  const int tw = TWC > 0 ? TWC : t.tw;
   // warps 0 .. NCT/32-1 compute (one thread per column pair); the last warp streams rows (TMA)
-  q.NTC = t.tw / 2 + SR_HALO;             // column pairs
+  q.NTC = tw / 2 + SR_HALO;               // column pairs
   q.NCT = (q.NTC + 31) & ~31;             // compute threads (whole warps; idle lanes alias the last pair)
   q.NL = 2 * q.NTC;                       // loaded columns = tw + 2*HALO
   q.tid = threadIdx.x;
@@ -72,7 +77,13 @@ __device__ __forceinline__ SrGeo sr_geo(const GridParams& g, const DevPtrs& d, c
   const int tile = blockIdx.x / K;
   const int strip = tile % t.n_strips, chunk = tile / t.n_strips;
   const int nt = g.nt;
-  q.i0 = strip * t.tw - t.tw / 2;                   // first output column (may be negative: mod nt)
+  // strip s owns [s tw - soff, (s+1) tw - soff): the seam (column 0) lies at local column
+  // soff + HALO of strip 0, >= 6 columns from both edges.  With 512-column strips it is placed in
+  // compute warp 6 (pair 198): warps map to the SM sub-partitions round-robin, and sub-partition 0
+  // already carries three compute warps (0, 4 and the halo warp 8) while 2 and 3 carry two -- the
+  // seam warp's extra wrap terms go where there are spare issue slots
+  const int soff = TWC == 512 ? 392 : tw / 2;
+  q.i0 = strip * tw - soff;                         // first output column (may be negative: mod nt)
   q.j0 = g.y0 + chunk * t.th;
   q.j1 = min(q.j0 + t.th, g.y1);                    // own rows [y0, y1)
   const int cl = 2 * q.tl;
@@ -80,10 +91,10 @@ __device__ __forceinline__ SrGeo sr_geo(const GridParams& g, const DevPtrs& d, c
   if (gl < 0) gl += nt;
   q.gl = gl;
   q.gr = gl + 1;                           // gl is even and nt is even: the pair never wraps
-  // output pair: inside [HALO, HALO + TW) and, for the last (ragged) strip, before column
-  // tw/2 + n_strips*tw - tw/2 ... i.e. its global output index i0 + cl - HALO < nt - tw/2
-  const int o = q.i0 + cl - SR_HALO + t.tw / 2;     // output index counted from strip 0's start
-  q.out = (q.tid < q.NTC) && (cl >= SR_HALO) && (cl < SR_HALO + t.tw) && (o < nt);
+  // output pair: inside [HALO, HALO + TW) and, for the last (ragged) strip, before strip 0's
+  // start + nt, i.e. its output index counted from strip 0's start is < nt
+  const int o = q.i0 + cl - SR_HALO + soff;         // output index counted from strip 0's start
+  q.out = (q.tid < q.NTC) && (cl >= SR_HALO) && (cl < SR_HALO + tw) && (o < nt);
   // ASSOR split on the periodic ring (R-A12): only a pair holding column 0 on its left or
   // column nt-1 on its right sees the wraps; every other pair uses the plain formulas.
   q.seamL = (q.gl == 0);
@@ -221,7 +232,7 @@ __device__ __forceinline__ void sr_produce(const GridParams& g, const DevPtrs& d
 // seam column's L/U sums are formed directly from its own terms (as Eqs. 3.5-3.6 state them for
 // the natural ordering), not as the plain sums plus and minus a correction.
 enum { SEAM_NONE = 0, SEAM_FIXED = 1, SEAM_CHECK = 2 };
-template <int PC, int MODE, int SEAM>
+template <int PC, int MODE, int SEAM, bool ROT>
 __device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPtrs& d, const SrGeo& q, const SrSmem& s,
                                            int parity, double alpha, double alpha_prev, double beta, double omega,
                                            uint32_t gstep0, double& acc_rr, double& acc_g, double& acc_d,
@@ -236,9 +247,11 @@ __device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPt
   const bool seamWarp = SEAM == SEAM_FIXED ||
                         (SEAM == SEAM_CHECK && __any_sync(0xffffffffu, (q.seamL || q.seamR) && q.tid < NCT));
 
-  double* rout = (ITER ? d.r[1 - parity] : d.r[0]) + q.fk;
-  double* pdout = (ITER ? d.u[parity] : d.u[1]) + q.fk;
-  double* x = d.p + q.fk;
+  // output pointers at this thread's column pair; a row offset is 32-bit (row * n_theta < 2^31,
+  // checked at create), so every store address is one IMAD + one wide IMAD
+  double* rout = (ITER ? d.r[1 - parity] : d.r[0]) + q.fk + gl;
+  double* pdout = (ITER ? d.u[parity] : d.u[1]) + q.fk + gl;
+  double* x = d.p + q.fk + gl;
   const double c2 = (2.0 - omega) * omega;
   const double romega = 1.0 / omega;
   const double* vstage = s.vstage;
@@ -248,6 +261,14 @@ __device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPt
   // coefficient rows are read from the 8-slot ring at their lag
   D2 oD1{0, 0}, oD2{0, 0}, oD3{0, 0};
   D2 r1{0, 0}, r2{0, 0}, pdo2{0, 0}, pd2{0, 0}, pd3{0, 0}, rn3{0, 0}, u2_4{0, 0};
+  // ROT: coefficient rows past their first use stay in registers (rotated like the vector history):
+  // A_E of rows jl-1..jl-4, A_N of rows jl-2..jl-4 and the left neighbour's A_E of rows jl-1,
+  // jl-2 -- each shared-memory coefficient row is then read once per step (A_P at lags 2 and 4
+  // excepted), which takes 7 of the 12 coefficient loads (28 of ~118 shared wavefronts per warp
+  // and row) off the shared-memory pipe.  Needs the registers the compile-time strip width frees
+  // (TWC > 0); the runtime-width kernels re-read the rows from the ring instead.
+  D2 cE1{0, 0}, cE2{0, 0}, cE3{0, 0}, cE4{0, 0}, cN2{0, 0}, cN3{0, 0}, cN4{0, 0};
+  double cE1m = 0.0, cE2m = 0.0;
   const bool lane0 = (q.tid & 31) == 0;
   for (int blk = 0; blk < q.nsteps; blk += SR_UNROLL) {
     const uint32_t gblk = gstep0 + (uint32_t)blk;
@@ -287,36 +308,38 @@ __device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPt
       const D2 AE0 = ld2(c0 + NL, tl);
       const D2 AN1 = ld2(c1 + 2 * NL, tl);
       const D2 w1 = rld(w_1, tl, NTC);
+      const double ae0m = left_of(AE0.r, c0 + NL, im, lcoef);   // A_E(jl) left of the pair
       D2 iD0{fast_rcp(AP0.l), fast_rcp(AP0.r)};
       if constexpr (PC == SPC_ASSOR1) {
         // ASSOR-I (Eq. 3.2): the preconditioner is the diagonal c / Dt with
         // Dt_i = D_i + omega^2 sum_{k in L(i)} L_ik^2 / D_k, L = {W, E-wrap at n_theta-1, S}
         // (R-A12); it enters the pipeline exactly like Jacobi's D^-1
         const D2 AP1 = ld2(c1, tl);
-        const double apl = left_of(AP0.r, c0, im, lcoef), ael = left_of(AE0.r, c0 + NL, im, lcoef);
-        double sl = (ael * ael) * fast_rcp(apl);
-        double sr = (AE0.l * AE0.l) * iD0.l;
+        const double apl = left_of(AP0.r, c0, im, lcoef), ael = ae0m;
+        double sl = dmul(dmul(ael, ael), fast_rcp(apl));
+        double sr = dmul(dmul(AE0.l, AE0.l), iD0.l);
         if (SEAM != SEAM_NONE && seamWarp) {
           if (seamL) sl = 0.0;                                           // column 0: no W in L
-          if (seamR) sr += (AE0.r * AE0.r) * fast_rcp(c0[ip]);           // column nt-1: E-wrap
+          if (seamR) sr = dadd(sr, dmul(dmul(AE0.r, AE0.r), fast_rcp(c0[ip])));   // column nt-1: E-wrap
         }
-        sl += (AN1.l * AN1.l) * fast_rcp(AP1.l);
-        sr += (AN1.r * AN1.r) * fast_rcp(AP1.r);
-        iD0 = {c2 * fast_rcp(AP0.l + (omega * omega) * sl), c2 * fast_rcp(AP0.r + (omega * omega) * sr)};
+        sl = dadd(sl, dmul(dmul(AN1.l, AN1.l), fast_rcp(AP1.l)));
+        sr = dadd(sr, dmul(dmul(AN1.r, AN1.r), fast_rcp(AP1.r)));
+        const double o2 = dmul(omega, omega);
+        iD0 = {dmul(c2, fast_rcp(fma(o2, sl, AP0.l))), dmul(c2, fast_rcp(fma(o2, sr, AP0.r)))};
       }
-      const D2 oD0{omega * iD0.l, omega * iD0.r};
+      const D2 oD0{dmul(omega, iD0.l), dmul(omega, iD0.r)};
       D2 w0;
-      if constexpr (PC == SPC_NONE) w0 = r0; else w0 = {r0.l * iD0.l, r0.r * iD0.r};
+      if constexpr (PC == SPC_NONE) w0 = r0; else w0 = {dmul(r0.l, iD0.l), dmul(r0.r, iD0.r)};
       rst(w_0, tl, NTC, w0);
       row_bar<SEAM != SEAM_CHECK>(NCT);                                         // barrier 1: w(jl) complete
 
       // ---- (B) v1(jl) = w - (omega/D) sum_L A w  (Eq. 3.5);  (C) z(jl-1), pd(jl-1)
       D2 z1;
       if constexpr (PC == SPC_ASSOR2) {
-        const double w0m = rleft(w_0, tl, NTC), ae0m = left_of(AE0.r, c0 + NL, im, lcoef);
+        const double w0m = rleft(w_0, tl, NTC);
         const D2 v11 = rld(v_1, tl, NTC);
         const double v1p = rright(v_1, tl);
-        const D2 AEm1 = ld2(c1 + NL, tl);
+        const D2 AEm1 = ROT ? cE1 : ld2(c1 + NL, tl);
         // the seam warp (which paces its CTA at every row barrier, and the seam strip the grid)
         // loads its wrap operands together with the plain ones and applies them as selects
         double wE = 0.0, aW = 0.0, vW = 0.0;
@@ -326,57 +349,59 @@ __device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPt
           vW = rleft(v_1, tl, NTC);                             // v1(jl-1) left of the pair
         }
         // plain pair: L = {W, S}, U = {E, N}
-        D2 sL{AN1.l * w1.l + ae0m * w0m, AN1.r * w1.r + AE0.l * w0.l};
+        D2 sL{fma(ae0m, w0m, dmul(AN1.l, w1.l)), fma(AE0.l, w0.l, dmul(AN1.r, w1.r))};
         if constexpr (SEAM == SEAM_FIXED) {
-          sL.l = seamL ? AN1.l * w1.l : sL.l;                   // column 0: W is the wrap (in U)
-          sL.r = seamR ? sL.r + AE0.r * wE : sL.r;              // column nt-1: E-wrap is in L
+          sL.l = seamL ? dmul(AN1.l, w1.l) : sL.l;              // column 0: W is the wrap (in U)
+          sL.r = seamR ? fma(AE0.r, wE, sL.r) : sL.r;           // column nt-1: E-wrap is in L
         } else if (SEAM == SEAM_CHECK && seamWarp) {
-          if (seamL) sL.l = AN1.l * w1.l;                       // column 0: W is the wrap (in U)
-          if (seamR) sL.r += AE0.r * rright(w_0, tl);           // column nt-1: E-wrap is in L
+          if (seamL) sL.l = dmul(AN1.l, w1.l);                  // column 0: W is the wrap (in U)
+          if (seamR) sL.r = fma(AE0.r, rright(w_0, tl), sL.r);  // column nt-1: E-wrap is in L
         }
-        const D2 v10{w0.l - oD0.l * sL.l, w0.r - oD0.r * sL.r};
+        const D2 v10{fma(-oD0.l, sL.l, w0.l), fma(-oD0.r, sL.r, w0.r)};
         rst(v_0, tl, NTC, v10);
-        D2 sU{AN1.l * v10.l + AEm1.l * v11.r, AN1.r * v10.r + AEm1.r * v1p};
+        D2 sU{fma(AN1.l, v10.l, dmul(AEm1.l, v11.r)), fma(AN1.r, v10.r, dmul(AEm1.r, v1p))};
         if constexpr (SEAM == SEAM_FIXED) {
-          sU.l = seamL ? sU.l + aW * vW : sU.l;                 // column 0: the W-wrap is in U
-          sU.r = seamR ? AN1.r * v10.r : sU.r;                  // column nt-1: no E in U
+          sU.l = seamL ? fma(aW, vW, sU.l) : sU.l;              // column 0: the W-wrap is in U
+          sU.r = seamR ? dmul(AN1.r, v10.r) : sU.r;             // column nt-1: no E in U
         } else if (SEAM == SEAM_CHECK && seamWarp) {
-          if (seamL) sU.l += c1[NL + im] * rleft(v_1, tl, NTC); // column 0: the W-wrap is in U
-          if (seamR) sU.r = AN1.r * v10.r;                      // column nt-1: no E in U
+          if (seamL) sU.l = fma(c1[NL + im], rleft(v_1, tl, NTC), sU.l);   // column 0: the W-wrap is in U
+          if (seamR) sU.r = dmul(AN1.r, v10.r);                 // column nt-1: no E in U
         }
-        z1 = {c2 * (v11.l - oD1.l * sU.l), c2 * (v11.r - oD1.r * sU.r)};
+        z1 = {dmul(c2, fma(-oD1.l, sU.l, v11.l)), dmul(c2, fma(-oD1.r, sU.r, v11.r))};
       } else {
         z1 = w1;                                            // D^-1 r (Jacobi) or r (none)
       }
-      const D2 pd1 = USE_PD ? D2{z1.l + beta * pdo1.l, z1.r + beta * pdo1.r} : z1;   // step 9
+      const D2 pd1 = USE_PD ? D2{fma(beta, pdo1.l, z1.l), fma(beta, pdo1.r, z1.r)} : z1;   // step 9
       rst(p_1, tl, NTC, pd1);
       if (out && jl - 1 >= j0 && jl - 1 < j1)
-        stg2(pdout + (long long)(jl - 1) * nt + gl, ITER ? pd1 : D2{0, 0});   // INIT: pd_{-1} = 0
+        stg2(pdout + (jl - 1) * nt, ITER ? pd1 : D2{0, 0});   // INIT: pd_{-1} = 0
       // ---- (D) s(jl-2) = A pd, r_{i+1} = r_i - alpha s, x, w2 = D^-1 r_{i+1}
       D2 rn2;
-      const D2 AEm2 = ld2(c2r + NL, tl);
-      const D2 AN3 = ld2(c3 + 2 * NL, tl);
-      const double ae2m = left_of(AEm2.r, c2r + NL, im, lcoef);
+      const D2 AEm2 = ROT ? cE2 : ld2(c2r + NL, tl);
+      const D2 AN3 = ROT ? cN3 : ld2(c3 + 2 * NL, tl);
+      const double ae2m = ROT ? cE2m : left_of(AEm2.r, c2r + NL, im, lcoef);
       {
         const D2 AP2 = ld2(c2r, tl);
-        const D2 AN2 = ld2(c2r + 2 * NL, tl);
-        D2 sv{AP2.l * pd2.l + ae2m * rleft(p_2, tl, NTC), AP2.r * pd2.r + AEm2.l * pd2.l};
-        sv.l += AEm2.l * pd2.r + AN3.l * pd3.l + AN2.l * pd1.l;
-        sv.r += AEm2.r * rright(p_2, tl) + AN3.r * pd3.r + AN2.r * pd1.r;
-        rn2 = {r2.l - alpha * sv.l, r2.r - alpha * sv.r};  // step 5 (INIT: alpha = 0)
+        const D2 AN2 = ROT ? cN2 : ld2(c2r + 2 * NL, tl);
+        // s = A pd, the term of the row computed in this step (pd1) added last
+        D2 sv{fma(ae2m, rleft(p_2, tl, NTC), dmul(AP2.l, pd2.l)), fma(AEm2.l, pd2.l, dmul(AP2.r, pd2.r))};
+        sv = {fma(AEm2.l, pd2.r, sv.l), fma(AEm2.r, rright(p_2, tl), sv.r)};
+        sv = {fma(AN3.l, pd3.l, sv.l), fma(AN3.r, pd3.r, sv.r)};
+        sv = {fma(AN2.l, pd1.l, sv.l), fma(AN2.r, pd1.r, sv.r)};
+        rn2 = {fma(-alpha, sv.l, r2.l), fma(-alpha, sv.r, r2.r)};   // step 5 (INIT: alpha = 0)
       }
       if (out && jl - 2 >= j0 && jl - 2 < j1) {
-        const long long q2 = (long long)(jl - 2) * nt + gl;
+        const int q2 = (jl - 2) * nt;
         stg2(rout + q2, rn2);
-        acc_rr += rn2.l * rn2.l + rn2.r * rn2.r;
-        if (XUPD) stg2(x + q2, D2{x2.l + (alpha_prev * pdo2.l + alpha * pd2.l),      // step 4
-                                  x2.r + (alpha_prev * pdo2.r + alpha * pd2.r)});
-        if (MODE == SR_INIT_COLD) { stg2(x + q2, D2{0, 0}); acc_s += r2.l * r2.l + r2.r * r2.r; }
-        if (MODE == SR_INIT_WARM) acc_s += x2.l * x2.l + x2.r * x2.r;   // x2 holds S here
+        acc_rr = dadd(acc_rr, fma(rn2.l, rn2.l, dmul(rn2.r, rn2.r)));
+        if (XUPD) stg2(x + q2, D2{dadd(x2.l, fma(alpha_prev, pdo2.l, dmul(alpha, pd2.l))),      // step 4
+                                  dadd(x2.r, fma(alpha_prev, pdo2.r, dmul(alpha, pd2.r)))});
+        if (MODE == SR_INIT_COLD) { stg2(x + q2, D2{0, 0}); acc_s = dadd(acc_s, fma(r2.l, r2.l, dmul(r2.r, r2.r))); }
+        if (MODE == SR_INIT_WARM) acc_s = dadd(acc_s, fma(x2.l, x2.l, dmul(x2.r, x2.r)));   // x2 holds S here
       }
       D2 wz;
       if constexpr (PC == SPC_NONE) wz = rn2;
-      else wz = {(rn2.l * oD2.l) * romega, (rn2.r * oD2.r) * romega};
+      else wz = {dmul(dmul(rn2.l, oD2.l), romega), dmul(dmul(rn2.r, oD2.r), romega)};
       rst(w2_2, tl, NTC, wz);
       row_bar<SEAM != SEAM_CHECK>(NCT);                                         // barrier 2: w2(jl-2) complete
 
@@ -387,48 +412,48 @@ __device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPt
         const double wz2m = rleft(w2_2, tl, NTC);
         const D2 v23 = rld(v2_3, tl, NTC);
         const double v23p = rright(v2_3, tl);
-        const D2 AEm3 = ld2(c3 + NL, tl);
+        const D2 AEm3 = ROT ? cE3 : ld2(c3 + NL, tl);
         double wE2 = 0.0, aW2 = 0.0, vW2 = 0.0;
         if constexpr (SEAM == SEAM_FIXED) {
           wE2 = rright(w2_2, tl);
           aW2 = c3[NL + im];
           vW2 = rleft(v2_3, tl, NTC);
         }
-        D2 sL{AN3.l * w23.l + ae2m * wz2m, AN3.r * w23.r + AEm2.l * wz.l};
+        D2 sL{fma(ae2m, wz2m, dmul(AN3.l, w23.l)), fma(AEm2.l, wz.l, dmul(AN3.r, w23.r))};
         if constexpr (SEAM == SEAM_FIXED) {
-          sL.l = seamL ? AN3.l * w23.l : sL.l;
-          sL.r = seamR ? sL.r + AEm2.r * wE2 : sL.r;
+          sL.l = seamL ? dmul(AN3.l, w23.l) : sL.l;
+          sL.r = seamR ? fma(AEm2.r, wE2, sL.r) : sL.r;
         } else if (SEAM == SEAM_CHECK && seamWarp) {
-          if (seamL) sL.l = AN3.l * w23.l;
-          if (seamR) sL.r += AEm2.r * rright(w2_2, tl);
+          if (seamL) sL.l = dmul(AN3.l, w23.l);
+          if (seamR) sL.r = fma(AEm2.r, rright(w2_2, tl), sL.r);
         }
-        const D2 v22{wz.l - oD2.l * sL.l, wz.r - oD2.r * sL.r};
+        const D2 v22{fma(-oD2.l, sL.l, wz.l), fma(-oD2.r, sL.r, wz.r)};
         rst(v2_2, tl, NTC, v22);
-        D2 sU{AN3.l * v22.l + AEm3.l * v23.r, AN3.r * v22.r + AEm3.r * v23p};
+        D2 sU{fma(AN3.l, v22.l, dmul(AEm3.l, v23.r)), fma(AN3.r, v22.r, dmul(AEm3.r, v23p))};
         if constexpr (SEAM == SEAM_FIXED) {
-          sU.l = seamL ? sU.l + aW2 * vW2 : sU.l;
-          sU.r = seamR ? AN3.r * v22.r : sU.r;
+          sU.l = seamL ? fma(aW2, vW2, sU.l) : sU.l;
+          sU.r = seamR ? dmul(AN3.r, v22.r) : sU.r;
         } else if (SEAM == SEAM_CHECK && seamWarp) {
-          if (seamL) sU.l += c3[NL + im] * rleft(v2_3, tl, NTC);
-          if (seamR) sU.r = AN3.r * v22.r;
+          if (seamL) sU.l = fma(c3[NL + im], rleft(v2_3, tl, NTC), sU.l);
+          if (seamR) sU.r = dmul(AN3.r, v22.r);
         }
-        u2_3 = {c2 * (v23.l - oD3.l * sU.l), c2 * (v23.r - oD3.r * sU.r)};
+        u2_3 = {dmul(c2, fma(-oD3.l, sU.l, v23.l)), dmul(c2, fma(-oD3.r, sU.r, v23.r))};
       } else {
         u2_3 = rld(w2_3, tl, NTC);
       }
       u2_3r[tl] = u2_3.l;                                  // only the right-neighbour read (delta) remains
-      if (out && jl - 3 >= j0 && jl - 3 < j1) acc_g += rn3.l * u2_3.l + rn3.r * u2_3.r;   // gamma
+      if (out && jl - 3 >= j0 && jl - 3 < j1) acc_g = dadd(acc_g, fma(rn3.l, u2_3.l, dmul(rn3.r, u2_3.r)));   // gamma
       {
         // delta = z2' A z2 as the quadratic form (A symmetric): each owned row j adds its
         // diagonal term and its east and north couplings, i.e. every edge once, at its
         // west / south end -- no w = A z2 vector, one coefficient row (lag 4)
         const D2 AP4 = ld2(c4, tl);
-        const D2 AEm4 = ld2(c4 + NL, tl);
-        const D2 AN4 = ld2(c4 + 2 * NL, tl);
+        const D2 AEm4 = ROT ? cE4 : ld2(c4 + NL, tl);
+        const D2 AN4 = ROT ? cN4 : ld2(c4 + 2 * NL, tl);
         if (out && jl - 4 >= j0 && jl - 4 < j1) {
-          const double ql = AP4.l * u2_4.l + 2.0 * (AEm4.l * u2_4.r + AN4.l * u2_3.l);
-          const double qr = AP4.r * u2_4.r + 2.0 * (AEm4.r * rright(u2_4r, tl) + AN4.r * u2_3.r);
-          acc_d += u2_4.l * ql + u2_4.r * qr;
+          const double ql = fma(AP4.l, u2_4.l, dmul(2.0, fma(AN4.l, u2_3.l, dmul(AEm4.l, u2_4.r))));
+          const double qr = fma(AP4.r, u2_4.r, dmul(2.0, fma(AN4.r, u2_3.r, dmul(AEm4.r, rright(u2_4r, tl)))));
+          acc_d = dadd(acc_d, fma(u2_4.l, ql, dmul(u2_4.r, qr)));
         }
       }
       __syncwarp();
@@ -442,6 +467,11 @@ __device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPt
       pdo2 = pdo1;
       r2 = r1; r1 = r0;
       oD3 = oD2; oD2 = oD1; oD1 = oD0;
+      if constexpr (ROT) {
+        cE4 = cE3; cE3 = cE2; cE2 = cE1; cE1 = AE0;
+        cN4 = cN3; cN3 = cN2; cN2 = AN1;
+        cE2m = cE1m; cE1m = ae0m;
+      }
     }
   }
 }
@@ -451,7 +481,7 @@ __device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPt
 // seam code, and the seam warp no divergent branches -- worth ~4% at long row chunks (C3), but
 // the two loops cost instruction-cache refills at every pass, which short chunks (row slabs of
 // 128 rows) do not amortize.  !SPLIT: one SEAM_CHECK loop for all warps.
-template <int PC, int MODE, bool SPLIT>
+template <int PC, int MODE, bool SPLIT, int TWC = 0>
 __device__ __forceinline__ void sr_compute(const GridParams& g, const DevPtrs& d, const SrGeo& q, const SrSmem& s,
                                            int parity, double alpha, double alpha_prev, double beta, double omega,
                                            uint32_t gstep0, double& acc_rr, double& acc_g, double& acc_d,
@@ -459,13 +489,13 @@ __device__ __forceinline__ void sr_compute(const GridParams& g, const DevPtrs& d
   if constexpr (SPLIT) {
     const bool seamWarp = __any_sync(0xffffffffu, (q.seamL || q.seamR) && q.tid < q.NCT);
     if (seamWarp)
-      sr_compute_loop<PC, MODE, SEAM_FIXED>(g, d, q, s, parity, alpha, alpha_prev, beta, omega, gstep0, acc_rr, acc_g,
+      sr_compute_loop<PC, MODE, SEAM_FIXED, false>(g, d, q, s, parity, alpha, alpha_prev, beta, omega, gstep0, acc_rr, acc_g,
                                             acc_d, acc_s);
     else
-      sr_compute_loop<PC, MODE, SEAM_NONE>(g, d, q, s, parity, alpha, alpha_prev, beta, omega, gstep0, acc_rr, acc_g,
+      sr_compute_loop<PC, MODE, SEAM_NONE, false>(g, d, q, s, parity, alpha, alpha_prev, beta, omega, gstep0, acc_rr, acc_g,
                                            acc_d, acc_s);
   } else {
-    sr_compute_loop<PC, MODE, SEAM_CHECK>(g, d, q, s, parity, alpha, alpha_prev, beta, omega, gstep0, acc_rr, acc_g,
+    sr_compute_loop<PC, MODE, SEAM_CHECK, (TWC > 0)>(g, d, q, s, parity, alpha, alpha_prev, beta, omega, gstep0, acc_rr, acc_g,
                                           acc_d, acc_s);
   }
 }
@@ -601,13 +631,13 @@ __device__ __forceinline__ SrpShared srp_shared(double* smem_raw, int NL, int K,
 // condition order (condition sharding) and runs the same scalar stage -- bitwise the same
 // scalars on every CTA of every rank.  The producers of edge chunks stream their halo rows from
 // the inbox once the stamps (which also publish the halos) are in.
-template <int PC, bool SPLIT, bool DIST>
+template <int PC, bool SPLIT, bool DIST, int TWC = 0>
 __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K) {
   extern __shared__ __align__(128) double smem_raw[];
   if (d.st_->done) return;                   // the init already converged (or failed)
   constexpr bool dist = DIST;                // peer-to-peer multi-rank context (d.dist.world > 0)
   const int Kall = dist && d.dist.rows != 1 ? d.dist.kglob : K;
-  const SrGeo q = sr_geo(g, d, t, K);
+  const SrGeo q = sr_geo<TWC>(g, d, t, K);
   const SrSmem s = sr_smem(smem_raw, q.NL);
   const SrpShared x = srp_shared(smem_raw, q.NL, K, (int)gridDim.x, Kall);
   sr_init_barriers(q, s);
@@ -686,8 +716,8 @@ __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K
     double a_rr = 0.0, a_g = 0.0, a_d = 0.0, a_s = 0.0;
     if (!(async && x.cs.frz[q.k])) {
       const double alpha = x.cs.alpha[q.k], alpha_prev = x.cs.uvk[q.k], beta = x.cs.beta[q.k];
-      if (parity) sr_compute<PC, SR_ITER_ODD, SPLIT>(g, d, q, s, 1, alpha, alpha_prev, beta, omega, gstep, a_rr, a_g, a_d, a_s);
-      else sr_compute<PC, SR_ITER_EVEN, SPLIT>(g, d, q, s, 0, alpha, alpha_prev, beta, omega, gstep, a_rr, a_g, a_d, a_s);
+      if (parity) sr_compute<PC, SR_ITER_ODD, SPLIT, TWC>(g, d, q, s, 1, alpha, alpha_prev, beta, omega, gstep, a_rr, a_g, a_d, a_s);
+      else sr_compute<PC, SR_ITER_EVEN, SPLIT, TWC>(g, d, q, s, 0, alpha, alpha_prev, beta, omega, gstep, a_rr, a_g, a_d, a_s);
       gstep += (uint32_t)q.nsteps;
     }
     // field stores of this iteration -> visible to the other CTAs' TMA reads after the barrier
@@ -867,9 +897,15 @@ cudaError_t launch_sr_persistent(const GridParams& g, const DevPtrs& d, const Ti
   switch (precond) {
     case SPC_ASSOR2:
       // (the multi-rank kernel keeps one loop: with the split loops it spills in the row loop)
-      if (dist) return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, false, true>, g, d, t, K);
-      return split ? cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, true, false>, g, d, t, K)
-                   : cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, false, false>, g, d, t, K);
+      if (dist) {
+        if (t.tw == 512) return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, false, true, 512>, g, d, t, K);
+        if (t.tw == 256) return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, false, true, 256>, g, d, t, K);
+        return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, false, true>, g, d, t, K);
+      }
+      if (split) return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, true, false>, g, d, t, K);
+      if (t.tw == 512) return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, false, false, 512>, g, d, t, K);
+      if (t.tw == 256) return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, false, false, 256>, g, d, t, K);
+      return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, false, false>, g, d, t, K);
     case SPC_ASSOR1:
       return dist ? cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR1, false, true>, g, d, t, K)
                   : cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR1, false, false>, g, d, t, K);
@@ -1208,10 +1244,14 @@ cudaError_t configure_sr_kernels(const TileCfg& t, int K) {
   if (e == cudaSuccess) e = sr_set_modes<SR_INIT_WARM>(cap);
   if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2, true, false>, cap);
   if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2, false, false>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2, false, false, 512>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2, false, false, 256>, cap);
   if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR1, false, false>, cap);
   if (e == cudaSuccess) e = sr_set(k_srp<SPC_JACOBI, false, false>, cap);
   if (e == cudaSuccess) e = sr_set(k_srp<SPC_NONE, false, false>, cap);
   if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2, false, true>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2, false, true, 512>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2, false, true, 256>, cap);
   if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR1, false, true>, cap);
   if (e == cudaSuccess) e = sr_set(k_srp<SPC_JACOBI, false, true>, cap);
   if (e == cudaSuccess) e = sr_set(k_srp<SPC_NONE, false, true>, cap);

@@ -89,6 +89,13 @@ __device__ __forceinline__ double fast_rcp(double a) {
   return fma(r, fma(e, e, e), r);
 }
 
+// Explicitly rounded products and sums: every kernel variant (per-launch, persistent, compile-time
+// or runtime strip width, seam variants) must round the same expressions the same way, so the row
+// pipeline spells out each multiply, add and fused multiply-add instead of leaving the contraction
+// of a*b + c*d to the compiler (which may contract differently in differently shaped kernels).
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+
 struct D2 { double l, r; };
 __device__ __forceinline__ D2 ld2(const double* base, int t) {
   const double2 v = reinterpret_cast<const double2*>(base)[t];

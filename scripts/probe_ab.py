@@ -1,6 +1,6 @@
 """A/B timing of two builds of the library on the same GPU (same box, same clocks): per-iteration
 time of fixed-iteration solves at C3 and at the 128-row slab (the strong-scaling unit), each
-build in its own subprocess.  Usage: probe_ab.py ROOT_A ROOT_B (repository roots holding a built
+build in its own subprocess.  Usage: probe_ab.py ROOT_A ROOT_B ... (repository roots holding a built
 paper_2511_06824_b200 package)."""
 import os
 import subprocess
@@ -20,7 +20,7 @@ for ny in (1024, 128):
     out.append(round(t, 1)); S.close()
 print(out)
 '''
-roots = sys.argv[1:3]
+roots = sys.argv[1:]
 for rep in range(2):
     for r in roots:
         res = subprocess.run([sys.executable, "-c", CODE, r], capture_output=True, text=True)

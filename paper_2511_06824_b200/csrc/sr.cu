@@ -243,6 +243,7 @@ __device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPt
   constexpr bool USE_X = XUPD || (MODE == SR_INIT_WARM);  // a warm init streams S in the x slot
   const int nt = g.nt, NL = q.NL, NTC = q.NTC, NCT = q.NCT, tl = q.tl, im = q.im, ip = q.ip;
   const int j0 = q.j0, j1 = q.j1, jbase = q.jbase, gl = q.gl;
+  const unsigned nown = (unsigned)(j1 - j0);             // own rows [j0, j1)
   const bool out = q.out, seamL = q.seamL, seamR = q.seamR, lcoef = q.lcoef;
   const bool seamWarp = SEAM == SEAM_FIXED ||
                         (SEAM == SEAM_CHECK && __any_sync(0xffffffffu, (q.seamL || q.seamR) && q.tid < NCT));
@@ -373,8 +374,9 @@ __device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPt
       }
       const D2 pd1 = USE_PD ? D2{fma(beta, pdo1.l, z1.l), fma(beta, pdo1.r, z1.r)} : z1;   // step 9
       rst(p_1, tl, NTC, pd1);
-      if (out && jl - 1 >= j0 && jl - 1 < j1)
-        stg2(pdout + (jl - 1) * nt, ITER ? pd1 : D2{0, 0});   // INIT: pd_{-1} = 0
+      // row jl-k is stored / summed only if the pair is an output pair and the row is one of the
+      // chunk's own rows: predicated stores and selects (no branches in the row loop)
+      stg2_if(out && (unsigned)(jl - 1 - j0) < nown, pdout + (jl - 1) * nt, ITER ? pd1 : D2{0, 0});   // INIT: pd_{-1} = 0
       // ---- (D) s(jl-2) = A pd, r_{i+1} = r_i - alpha s, x, w2 = D^-1 r_{i+1}
       D2 rn2;
       const D2 AEm2 = ROT ? cE2 : ld2(c2r + NL, tl);
@@ -390,14 +392,23 @@ __device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPt
         sv = {fma(AN2.l, pd1.l, sv.l), fma(AN2.r, pd1.r, sv.r)};
         rn2 = {fma(-alpha, sv.l, r2.l), fma(-alpha, sv.r, r2.r)};   // step 5 (INIT: alpha = 0)
       }
-      if (out && jl - 2 >= j0 && jl - 2 < j1) {
+      {
+        const bool p2 = out && (unsigned)(jl - 2 - j0) < nown;
         const int q2 = (jl - 2) * nt;
-        stg2(rout + q2, rn2);
-        acc_rr = dadd(acc_rr, fma(rn2.l, rn2.l, dmul(rn2.r, rn2.r)));
-        if (XUPD) stg2(x + q2, D2{dadd(x2.l, fma(alpha_prev, pdo2.l, dmul(alpha, pd2.l))),      // step 4
-                                  dadd(x2.r, fma(alpha_prev, pdo2.r, dmul(alpha, pd2.r)))});
-        if (MODE == SR_INIT_COLD) { stg2(x + q2, D2{0, 0}); acc_s = dadd(acc_s, fma(r2.l, r2.l, dmul(r2.r, r2.r))); }
-        if (MODE == SR_INIT_WARM) acc_s = dadd(acc_s, fma(x2.l, x2.l, dmul(x2.r, x2.r)));   // x2 holds S here
+        stg2_if(p2, rout + q2, rn2);
+        const double trr = dadd(acc_rr, fma(rn2.l, rn2.l, dmul(rn2.r, rn2.r)));
+        acc_rr = p2 ? trr : acc_rr;
+        if (XUPD) stg2_if(p2, x + q2, D2{dadd(x2.l, fma(alpha_prev, pdo2.l, dmul(alpha, pd2.l))),      // step 4
+                                         dadd(x2.r, fma(alpha_prev, pdo2.r, dmul(alpha, pd2.r)))});
+        if (MODE == SR_INIT_COLD) {
+          stg2_if(p2, x + q2, D2{0, 0});
+          const double ts = dadd(acc_s, fma(r2.l, r2.l, dmul(r2.r, r2.r)));
+          acc_s = p2 ? ts : acc_s;
+        }
+        if (MODE == SR_INIT_WARM) {   // x2 holds S here
+          const double ts = dadd(acc_s, fma(x2.l, x2.l, dmul(x2.r, x2.r)));
+          acc_s = p2 ? ts : acc_s;
+        }
       }
       D2 wz;
       if constexpr (PC == SPC_NONE) wz = rn2;
@@ -442,7 +453,10 @@ __device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPt
         u2_3 = rld(w2_3, tl, NTC);
       }
       u2_3r[tl] = u2_3.l;                                  // only the right-neighbour read (delta) remains
-      if (out && jl - 3 >= j0 && jl - 3 < j1) acc_g = dadd(acc_g, fma(rn3.l, u2_3.l, dmul(rn3.r, u2_3.r)));   // gamma
+      {   // gamma
+        const double tg = dadd(acc_g, fma(rn3.l, u2_3.l, dmul(rn3.r, u2_3.r)));
+        acc_g = (out && (unsigned)(jl - 3 - j0) < nown) ? tg : acc_g;
+      }
       {
         // delta = z2' A z2 as the quadratic form (A symmetric): each owned row j adds its
         // diagonal term and its east and north couplings, i.e. every edge once, at its
@@ -450,11 +464,10 @@ __device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPt
         const D2 AP4 = ld2(c4, tl);
         const D2 AEm4 = ROT ? cE4 : ld2(c4 + NL, tl);
         const D2 AN4 = ROT ? cN4 : ld2(c4 + 2 * NL, tl);
-        if (out && jl - 4 >= j0 && jl - 4 < j1) {
-          const double ql = fma(AP4.l, u2_4.l, dmul(2.0, fma(AN4.l, u2_3.l, dmul(AEm4.l, u2_4.r))));
-          const double qr = fma(AP4.r, u2_4.r, dmul(2.0, fma(AN4.r, u2_3.r, dmul(AEm4.r, rright(u2_4r, tl)))));
-          acc_d = dadd(acc_d, fma(u2_4.l, ql, dmul(u2_4.r, qr)));
-        }
+        const double ql = fma(AP4.l, u2_4.l, dmul(2.0, fma(AN4.l, u2_3.l, dmul(AEm4.l, u2_4.r))));
+        const double qr = fma(AP4.r, u2_4.r, dmul(2.0, fma(AN4.r, u2_3.r, dmul(AEm4.r, rright(u2_4r, tl)))));
+        const double td = dadd(acc_d, fma(u2_4.l, ql, dmul(u2_4.r, qr)));
+        acc_d = (out && (unsigned)(jl - 4 - j0) < nown) ? td : acc_d;
       }
       __syncwarp();
       // coefficient row jl-4 done (in the persistent kernel the first 4 steps of a pass release

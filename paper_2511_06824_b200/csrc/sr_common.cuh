@@ -119,6 +119,18 @@ __device__ __forceinline__ double left_of(double own_r, const double* row, int i
 __device__ __forceinline__ void stg2(double* p, D2 v) {   // 16-byte global store (pairs are aligned)
   *reinterpret_cast<double2*>(p) = make_double2(v.l, v.r);
 }
+// the same store predicated on p (one predicated instruction, no branch); not ordered against other
+// memory operations by the compiler -- the row loop's outputs are read only after the grid barrier
+// (or the kernel boundary), whose fences are asm statements with memory clobbers
+__device__ __forceinline__ void stg2_if(bool p, double* ptr, D2 v) {
+  asm volatile(
+      "{\n"
+      ".reg .pred q;\n"
+      "setp.ne.b32 q, %0, 0;\n"
+      "@q st.global.v2.f64 [%1], {%2, %3};\n"
+      "}\n" ::"r"((int)p),
+      "l"(ptr), "d"(v.l), "d"(v.r));
+}
 
 // Table-1 scalars from the per-condition sums (fixed k order): convergence test (Eq. 3.9),
 // alpha/beta of the single-reduction recurrence (coupled: global; lockstep: per condition).

@@ -60,21 +60,20 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 __device__ __forceinline__ void compute_bar(int nthreads) {
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
-// The same barrier as ONE out-of-line instruction: with the split seam loops (sr.cu
-// sr_compute) the seam warp and the others run different loops, and bar.sync (= barrier.sync
-// .aligned) requires every thread to execute the same barrier instruction -- a shared callee
-// gives them the same one.
-__device__ __noinline__ void compute_bar_shared(int nthreads) {
-  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
-}
 // timing-only experiment (wrong results): the row pipeline's two barriers per row compiled out
 #ifdef GMAF_EXPERIMENT_NOBAR
 template <bool SHARED = false>
 __device__ __forceinline__ void row_bar(int) { __syncwarp(); }
 #else
+// SHARED: the split seam loops (different barrier instructions in the seam warp and the others)
+// use the NON-aligned form barrier.sync, which PTX allows to be reached from different
+// instructions (bar.sync = barrier.sync.aligned requires the same instruction in every thread)
+__device__ __forceinline__ void compute_bar_unaligned(int nthreads) {
+  asm volatile("barrier.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
 template <bool SHARED = false>
 __device__ __forceinline__ void row_bar(int nthreads) {
-  if constexpr (SHARED) compute_bar_shared(nthreads);
+  if constexpr (SHARED) compute_bar_unaligned(nthreads);
   else compute_bar(nthreads);
 }
 #endif

@@ -23,4 +23,13 @@ st, W = S.step(gi.random_conditions(5, 3), tol=1e-8, omega=1.6, max_iter=3000)
 print("split seam", st.iterations, st.converged, S.tile_config())
 S.close()
 os.environ.pop("GMAF_SEAM_SPLIT")
+# the compile-time strip widths of the persistent kernel (256 for 256 <= n_theta < 1024, 512 above)
+for nt, ny in ((256, 12), (1024, 10)):
+    g = gi.grid(nt, ny, "short", tex_n_theta=8, tex_n_y=2, tex_band_rows=8)
+    S = P.JointSolver(g, 2)
+    S.thickness(gi.random_conditions(7, 2))
+    S.assemble()
+    st = S.solve(tol=1e-8, omega=1.6, max_iter=40, raise_on_error=False)
+    print("tw", S.tile_config()["tw"], st.iterations, S.tile_config()["persistent"])
+    S.close()
 print("sanitize run done")

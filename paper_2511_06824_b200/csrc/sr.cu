@@ -232,6 +232,16 @@ __device__ __forceinline__ void sr_produce(const GridParams& g, const DevPtrs& d
 // seam column's L/U sums are formed directly from its own terms (as Eqs. 3.5-3.6 state them for
 // the natural ordering), not as the plain sums plus and minus a correction.
 enum { SEAM_NONE = 0, SEAM_FIXED = 1, SEAM_CHECK = 2 };
+
+// Timing-only instrumentation (-DGMAF_STEP_PROBE, never in the product build; scripts/probe_steps.py):
+// per CTA and warp, clock() sums of the row step's intervals [top -> TMA data ready -> before
+// barrier 1 -> after it -> before barrier 2 -> after it -> next top], read with gmaf_debug_step_probe.
+#ifdef GMAF_STEP_PROBE
+__device__ unsigned int g_step_probe[2048 * 16 * 8];
+#define STEP_PROBE(i) { const unsigned int tn_ = (unsigned int)clock(); pc_[i] += tn_ - tprev_; tprev_ = tn_; }
+#else
+#define STEP_PROBE(i)
+#endif
 template <int PC, int MODE, int SEAM, bool ROT>
 __device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPtrs& d, const SrGeo& q, const SrSmem& s,
                                            int parity, double alpha, double alpha_prev, double beta, double omega,
@@ -271,6 +281,10 @@ __device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPt
   D2 cE1{0, 0}, cE2{0, 0}, cE3{0, 0}, cE4{0, 0}, cN2{0, 0}, cN3{0, 0}, cN4{0, 0};
   double cE1m = 0.0, cE2m = 0.0;
   const bool lane0 = (q.tid & 31) == 0;
+#ifdef GMAF_STEP_PROBE
+  unsigned int pc_[6] = {0, 0, 0, 0, 0, 0};
+  unsigned int tprev_ = (unsigned int)clock();
+#endif
   for (int blk = 0; blk < q.nsteps; blk += SR_UNROLL) {
     const uint32_t gblk = gstep0 + (uint32_t)blk;
     const uint32_t cpar = (gblk / SR_UNROLL) & 1u;                   // phase of the per-step barriers
@@ -298,7 +312,9 @@ __device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPt
       const double* u2_4r = s.ringU2 + (u & 1) * NL;
 
       // ---- (A) row jl: streamed data, D^-1, w = D^-1 r
+      STEP_PROBE(5);
       mbar_wait(s.full0 + 8 * u, cpar);
+      STEP_PROBE(0);
       const double* vs = vstage + sv * 3 * NL;
       const D2 r0 = ld2(vs, tl);
       const D2 pdo1 = USE_PD ? ld2(vs + NL, tl) : D2{0, 0};
@@ -332,7 +348,9 @@ __device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPt
       D2 w0;
       if constexpr (PC == SPC_NONE) w0 = r0; else w0 = {dmul(r0.l, iD0.l), dmul(r0.r, iD0.r)};
       rst(w_0, tl, NTC, w0);
+      STEP_PROBE(1);
       row_bar<SEAM != SEAM_CHECK>(NCT);                                         // barrier 1: w(jl) complete
+      STEP_PROBE(2);
 
       // ---- (B) v1(jl) = w - (omega/D) sum_L A w  (Eq. 3.5);  (C) z(jl-1), pd(jl-1)
       D2 z1;
@@ -414,7 +432,9 @@ __device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPt
       if constexpr (PC == SPC_NONE) wz = rn2;
       else wz = {dmul(dmul(rn2.l, oD2.l), romega), dmul(dmul(rn2.r, oD2.r), romega)};
       rst(w2_2, tl, NTC, wz);
+      STEP_PROBE(3);
       row_bar<SEAM != SEAM_CHECK>(NCT);                                         // barrier 2: w2(jl-2) complete
+      STEP_PROBE(4);
 
       // ---- (E) v2(jl-2)   (F) z2(jl-3), gamma   (G) A z2 at jl-4, delta
       D2 u2_3;
@@ -487,6 +507,10 @@ __device__ __forceinline__ void sr_compute_loop(const GridParams& g, const DevPt
       }
     }
   }
+#ifdef GMAF_STEP_PROBE
+  if (lane0 && blockIdx.x < 2048)
+    for (int i = 0; i < 6; ++i) atomicAdd(&g_step_probe[(blockIdx.x * 16 + (q.tid >> 5)) * 8 + i], pc_[i]);
+#endif
 }
 
 // The compute role.  SPLIT: the warp holding the seam runs the SEAM_FIXED row loop and every
@@ -891,7 +915,19 @@ bool srp_split_seam(const TileCfg& t) {
   return false;
 }
 
-cudaError_t launch_sr_persistent(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,
+#ifdef GMAF_STEP_PROBE
+extern "C" int gmaf_debug_step_probe(unsigned int* out, int n, int reset) {
+  if (n > 2048 * 16 * 8) n = 2048 * 16 * 8;
+  if (cudaMemcpyFromSymbol(out, g_step_probe, (size_t)n * 4) != cudaSuccess) return -1;
+  if (reset) {
+    static unsigned int zeros[2048 * 16 * 8];
+    if (cudaMemcpyToSymbol(g_step_probe, zeros, sizeof(zeros)) != cudaSuccess) return -1;
+  }
+  return n;
+}
+#endif
+
+const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,
                                  cudaStream_t s) {
   const bool split = srp_split_seam(t);
   const bool dist = d.dist.world > 0;

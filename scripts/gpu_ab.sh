@@ -2,7 +2,7 @@
 # arrival balance, a GPU test subset
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-timeout 900 python scripts/probe_ab.py /root/repo/abA /root/repo 2>&1 | tee gpurun_out/ab.log
+timeout 900 python scripts/probe_ab.py /root/repo/abA ${ROOTS:-/root/repo} 2>&1 | tee gpurun_out/ab.log
 [ -n "$ENV2" ] && env $ENV2 timeout 900 python scripts/probe_ab.py /root/repo 2>&1 | tee -a gpurun_out/ab.log
 [ -n "$BAL" ] && env $ENV2 timeout 600 python scripts/probe_balance.py 2>&1 | tee gpurun_out/balance.log
 [ -n "$PYT" ] && env $ENV2 timeout 2400 python -m pytest -q -m gpu -x $PYT > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?

@@ -927,7 +927,7 @@ extern "C" int gmaf_debug_step_probe(unsigned int* out, int n, int reset) {
 }
 #endif
 
-const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,
+cudaError_t launch_sr_persistent(const GridParams& g, const DevPtrs& d, const TileCfg& t, int K, int precond,
                                  cudaStream_t s) {
   const bool split = srp_split_seam(t);
   const bool dist = d.dist.world > 0;

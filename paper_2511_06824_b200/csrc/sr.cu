@@ -82,7 +82,9 @@ __device__ __forceinline__ SrGeo sr_geo(const GridParams& g, const DevPtrs& d, c
   // compute warp 6 (pair 198): warps map to the SM sub-partitions round-robin, and sub-partition 0
   // already carries three compute warps (0, 4 and the halo warp 8) while 2 and 3 carry two -- the
   // seam warp's extra wrap terms go where there are spare issue slots
-  const int soff = TWC == 512 ? 392 : tw / 2;
+  // (a function of the width alone, compile-time or not: every kernel variant tiles a context
+  // identically, so their per-CTA partial sums -- and hence their scalars -- are bitwise equal)
+  const int soff = tw == 512 ? 392 : tw / 2;
   q.i0 = strip * tw - soff;                         // first output column (may be negative: mod nt)
   q.j0 = g.y0 + chunk * t.th;
   q.j1 = min(q.j0 + t.th, g.y1);                    // own rows [y0, y1)

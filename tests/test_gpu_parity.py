@@ -583,6 +583,7 @@ def test_random_meshes_and_textures(P, orc, gi, case):
 
 PERSIST_CASES = {
     "c2": ("C2", {}),
+    "c4_512_column_strips": ("C4", {}),   # compile-time 512-column persistent kernel vs runtime width
     "c2_split_seam": ("C2", {"_split": "1"}),
     "ragged_split_seam": (None, {"_split": "1"}),
     "ragged_textured": (None, {}),

@@ -4,6 +4,7 @@
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?; tail -1 gpurun_out/smoke.log
+timeout 3000 python -m pytest tests -q -m gpu > gpurun_out/pytest_full.log 2>&1; echo pytest=$?; tail -3 gpurun_out/pytest_full.log
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo bench=$?; tail -c 3000 gpurun_out/bench.log
 export GMAF_LAUNCH_MODE=stream
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_srp -c 1 \

@@ -759,9 +759,14 @@ __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K
       else sr_compute<PC, SR_ITER_EVEN, SPLIT, TWC>(g, d, q, s, 0, alpha, alpha_prev, beta, omega, gstep, a_rr, a_g, a_d, a_s);
       gstep += (uint32_t)q.nsteps;
     }
-    // field stores of this iteration -> visible to the other CTAs' TMA reads after the barrier
+    // field stores of this iteration -> visible to the other CTAs' TMA reads after the barrier:
+    // a proxy fence per thread; the gpu-scope ordering comes from thread 0's fence + release after
+    // the CTA barrier below, which is cumulative over the writes the barrier ordered before it (the
+    // scheme of cooperative groups' grid sync: only the arriving thread fences)
     fence_proxy_async_global();
+#ifdef GMAF_PER_THREAD_FENCE
     __threadfence();
+#endif
     if (rows) {
       // row slabs: this CTA's output columns of the rows it owns among the 4 boundary rows of each
       // slab edge (r_{i+1} and pd_i) go straight into the neighbour's inbox (the next gather's

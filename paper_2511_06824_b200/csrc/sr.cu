@@ -198,9 +198,16 @@ __device__ __forceinline__ void sr_produce(const GridParams& g, const DevPtrs& d
     if (gs >= SR_VSLOTS) mbar_wait_sleep(s.emptyv0 + 8 * sv, ((gs / SR_VSLOTS) - 1) & 1);
     if (gs >= SR_CSLOTS) mbar_wait_sleep(s.emptyc0 + 8 * sc, ((gs / SR_CSLOTS) - 1) & 1);
     const uint32_t bar = s.full0 + 8 * sc;
+#ifdef GMAF_EXPERIMENT_NOTMA
+    // timing-only experiment (wrong results): no row is streamed, the rings keep stale data
+    if (lane == 0) mbar_arrive(bar);
+    __syncwarp();
+    if (false) {
+#else
     if (lane == 0) mbar_arrive_expect_tx(bar, bytes);
     __syncwarp();
     if (used) {
+#endif
       const int row = jbase + step - lag;
       const uint32_t dst = dst0 + (uint32_t)(vec ? sv : sc) * dstride;
       if (row >= lo && row < hi) {

@@ -257,6 +257,9 @@ __device__ void sr_scalar_stage(const CondScalars& cs, SolverState* st, const do
           cs.beta[kl] = 0.0; cs.uvk[kl] = 0.0; cs.dk[kl] = gk[kk];
         }
       }
+#if defined(GMAF_EXPERIMENT_NOTMA) || defined(GMAF_EXPERIMENT_NOBAR)
+      bad = false;
+#endif
       if (bad) { s.done = 1; s.status = -5; }
     }
   } else {
@@ -302,6 +305,9 @@ __device__ void sr_scalar_stage(const CondScalars& cs, SolverState* st, const do
           cs.alpha[kl] = a; cs.beta[kl] = b; cs.dk[kl] = gk[kk];
         }
       }
+#if defined(GMAF_EXPERIMENT_NOTMA) || defined(GMAF_EXPERIMENT_NOBAR)
+      bad = false;   // timing-only builds: wrong data, run every fixed iteration anyway
+#endif
       if (bad && !s.done) { s.done = 1; s.status = -5; }
     } else {
       for (int kl = 0; kl < Klocal; ++kl) cs.uvk[kl] = cs.alpha[kl];   // alpha used this iteration

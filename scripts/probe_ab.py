@@ -16,7 +16,8 @@ for ny in (1024, 128):
     S = P.JointSolver(g, 9, max_matrices=5)
     S.thickness(cfg.conds); S.assemble()
     S.solve_fixed(40, omega=cfg.omega)
-    t = min(S.solve_fixed(400, omega=cfg.omega).solve_ms for _ in range(3)) * 1e3 / 400
+    sts = [S.solve_fixed(400, omega=cfg.omega) for _ in range(3)]
+    t = min(st.solve_ms * 1e3 / max(st.iterations, 1) for st in sts)   # per executed iteration
     out.append(round(t, 1)); S.close()
 print(out)
 '''

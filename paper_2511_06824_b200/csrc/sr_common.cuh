@@ -48,8 +48,11 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   }
 }
 // producer: back off so a waiting producer does not steal issue slots from the compute warps
+#ifndef GMAF_PRODUCER_SLEEP_NS
+#define GMAF_PRODUCER_SLEEP_NS 128
+#endif
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
-  while (!mbar_try(bar, parity)) __nanosleep(128);
+  while (!mbar_try(bar, parity)) __nanosleep(GMAF_PRODUCER_SLEEP_NS);
 }
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),

@@ -546,7 +546,7 @@ __device__ __forceinline__ void sr_compute(const GridParams& g, const DevPtrs& d
   }
 }
 
-template <int PC, int MODE>
+template <int PC, int MODE, int TWC = 0>
 __global__ void __maxnreg__(168)
 k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long hcond, int use_cond) {
   extern __shared__ __align__(128) double smem_raw[];
@@ -555,7 +555,7 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
   SolverState* st = d.st_;
   if (ITER && st->done) return;
   timing_begin(d.timing, ITER ? KK_SR_ITER : KK_SR_INIT);
-  const SrGeo q = sr_geo(g, d, t, K);
+  const SrGeo q = sr_geo<TWC>(g, d, t, K);
   const SrSmem s = sr_smem(smem_raw, q.NL);
   sr_init_barriers(q, s);
   __syncthreads();
@@ -570,7 +570,7 @@ k_sr(GridParams g, DevPtrs d, TileCfg t, int K, int parity, unsigned long long h
     const double alpha = ITER ? d.cs.alpha[q.k] : 0.0;
     const double alpha_prev = ITER ? d.cs.uvk[q.k] : 0.0;   // uvk holds alpha_{i-1} here
     const double beta = ITER ? d.cs.beta[q.k] : 0.0;
-    sr_compute<PC, MODE, false>(g, d, q, s, parity, alpha, alpha_prev, beta, st->omega, 0u, acc_rr, acc_g, acc_d, acc_s);
+    sr_compute<PC, MODE, false, TWC>(g, d, q, s, parity, alpha, alpha_prev, beta, st->omega, 0u, acc_rr, acc_g, acc_d, acc_s);
   }
 
   // ---- per-CTA partials, then the scalar stage (last CTA, fixed order)
@@ -1048,7 +1048,10 @@ static cudaError_t sr_launch_mode(int precond, const GridParams& g, const DevPtr
                                   int parity, unsigned long long h, cudaStream_t s) {
   const int use = h != 0ull;
   switch (precond) {
-    case SPC_ASSOR2: return sr_launch(k_sr<SPC_ASSOR2, MODE>, g, d, t, K, parity, h, use, s);
+    case SPC_ASSOR2:   // compile-time strip widths for the common meshes (sr_geo TWC)
+      if (t.tw == 512) return sr_launch(k_sr<SPC_ASSOR2, MODE, 512>, g, d, t, K, parity, h, use, s);
+      if (t.tw == 256) return sr_launch(k_sr<SPC_ASSOR2, MODE, 256>, g, d, t, K, parity, h, use, s);
+      return sr_launch(k_sr<SPC_ASSOR2, MODE>, g, d, t, K, parity, h, use, s);
     case SPC_ASSOR1: return sr_launch(k_sr<SPC_ASSOR1, MODE>, g, d, t, K, parity, h, use, s);
     case SPC_JACOBI: return sr_launch(k_sr<SPC_JACOBI, MODE>, g, d, t, K, parity, h, use, s);
     default: return sr_launch(k_sr<SPC_NONE, MODE>, g, d, t, K, parity, h, use, s);
@@ -1282,6 +1285,8 @@ static cudaError_t sr_set(KernelT kern, int) {
 template <int MODE>
 static cudaError_t sr_set_modes(int bytes) {
   cudaError_t e = sr_set(k_sr<SPC_ASSOR2, MODE>, bytes);
+  if (e == cudaSuccess) e = sr_set(k_sr<SPC_ASSOR2, MODE, 512>, bytes);
+  if (e == cudaSuccess) e = sr_set(k_sr<SPC_ASSOR2, MODE, 256>, bytes);
   if (e == cudaSuccess) e = sr_set(k_sr<SPC_ASSOR1, MODE>, bytes);
   if (e == cudaSuccess) e = sr_set(k_sr<SPC_JACOBI, MODE>, bytes);
   if (e == cudaSuccess) e = sr_set(k_sr<SPC_NONE, MODE>, bytes);

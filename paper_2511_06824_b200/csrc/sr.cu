@@ -969,15 +969,23 @@ cudaError_t launch_sr_persistent(const GridParams& g, const DevPtrs& d, const Ti
       if (t.tw == 512) return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, false, false, 512>, g, d, t, K);
       if (t.tw == 256) return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, false, false, 256>, g, d, t, K);
       return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR2, false, false>, g, d, t, K);
+    // the comparison preconditioners (paper studies, NEXT-4) get the compile-time widths on one
+    // rank too, so that their per-iteration times are comparable with ASSOR-II's
     case SPC_ASSOR1:
-      return dist ? cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR1, false, true>, g, d, t, K)
-                  : cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR1, false, false>, g, d, t, K);
+      if (dist) return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR1, false, true>, g, d, t, K);
+      if (t.tw == 512) return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR1, false, false, 512>, g, d, t, K);
+      if (t.tw == 256) return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR1, false, false, 256>, g, d, t, K);
+      return cudaLaunchKernelEx(&cfg, k_srp<SPC_ASSOR1, false, false>, g, d, t, K);
     case SPC_JACOBI:
-      return dist ? cudaLaunchKernelEx(&cfg, k_srp<SPC_JACOBI, false, true>, g, d, t, K)
-                  : cudaLaunchKernelEx(&cfg, k_srp<SPC_JACOBI, false, false>, g, d, t, K);
+      if (dist) return cudaLaunchKernelEx(&cfg, k_srp<SPC_JACOBI, false, true>, g, d, t, K);
+      if (t.tw == 512) return cudaLaunchKernelEx(&cfg, k_srp<SPC_JACOBI, false, false, 512>, g, d, t, K);
+      if (t.tw == 256) return cudaLaunchKernelEx(&cfg, k_srp<SPC_JACOBI, false, false, 256>, g, d, t, K);
+      return cudaLaunchKernelEx(&cfg, k_srp<SPC_JACOBI, false, false>, g, d, t, K);
     default:
-      return dist ? cudaLaunchKernelEx(&cfg, k_srp<SPC_NONE, false, true>, g, d, t, K)
-                  : cudaLaunchKernelEx(&cfg, k_srp<SPC_NONE, false, false>, g, d, t, K);
+      if (dist) return cudaLaunchKernelEx(&cfg, k_srp<SPC_NONE, false, true>, g, d, t, K);
+      if (t.tw == 512) return cudaLaunchKernelEx(&cfg, k_srp<SPC_NONE, false, false, 512>, g, d, t, K);
+      if (t.tw == 256) return cudaLaunchKernelEx(&cfg, k_srp<SPC_NONE, false, false, 256>, g, d, t, K);
+      return cudaLaunchKernelEx(&cfg, k_srp<SPC_NONE, false, false>, g, d, t, K);
   }
 }
 
@@ -1317,6 +1325,12 @@ cudaError_t configure_sr_kernels(const TileCfg& t, int K) {
   if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR1, false, false>, cap);
   if (e == cudaSuccess) e = sr_set(k_srp<SPC_JACOBI, false, false>, cap);
   if (e == cudaSuccess) e = sr_set(k_srp<SPC_NONE, false, false>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR1, false, false, 512>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_JACOBI, false, false, 512>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_NONE, false, false, 512>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR1, false, false, 256>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_JACOBI, false, false, 256>, cap);
+  if (e == cudaSuccess) e = sr_set(k_srp<SPC_NONE, false, false, 256>, cap);
   if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2, false, true>, cap);
   if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2, false, true, 512>, cap);
   if (e == cudaSuccess) e = sr_set(k_srp<SPC_ASSOR2, false, true, 256>, cap);

@@ -43,7 +43,7 @@ extern "C" {
 typedef enum {
   GMAF_OK = 0,
   GMAF_E_INVALID_ARG = -1,
-  GMAF_E_INVALID_MESH = -2,          /* n_theta < 4 or n_y < 4 */
+  GMAF_E_INVALID_MESH = -2,          /* n_theta < 4 or n_y < 4, or (n_y + 16) n_theta >= 2^31 (32-bit row offsets) */
   GMAF_E_MESH_TOO_COARSE = -3,       /* < 2 nodes per dimple pitch */
   GMAF_E_NONPOSITIVE_THICKNESS = -4, /* h < h_min somewhere */
   GMAF_E_BREAKDOWN = -5,             /* u.v <= 0 or r.z <= 0: not SPD */

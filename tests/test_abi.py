@@ -48,6 +48,9 @@ def test_validation_without_gpu(pkg):
     assert pkg.gmaf_workspace_bytes(pkg.make_grid(gi.grid(3, 32)), 1) == 0          # INVALID_MESH
     assert pkg.gmaf_workspace_bytes(pkg.make_grid(gi.grid(100, 80, "short")), 1) == 0  # too coarse
     assert pkg.gmaf_workspace_bytes(pkg.make_grid(gi.grid(64, 32)), 0) == 0
+    # row offsets are 32-bit in the iteration kernels: (n_y + 16) n_theta must stay below 2^31
+    assert pkg.gmaf_workspace_bytes(pkg.make_grid(gi.grid(65536, 32768 - 16)), 1) == 0
+    assert pkg.gmaf_workspace_bytes(pkg.make_grid(gi.grid(65536, 32768 - 17)), 1) > 0
     ctx = C.c_void_p()
     g = pkg.make_grid(gi.grid(64, 32))
     # a NULL workspace is rejected before any CUDA call

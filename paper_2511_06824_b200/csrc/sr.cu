@@ -692,6 +692,7 @@ __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K
     x.cs.alpha[i] = d.cs.alpha[i]; x.cs.beta[i] = d.cs.beta[i]; x.cs.dk[i] = d.cs.dk[i];
     x.cs.Sk[i] = d.cs.Sk[i]; x.cs.rrk[i] = d.cs.rrk[i]; x.cs.uvk[i] = d.cs.uvk[i]; x.cs.ttk[i] = d.cs.ttk[i];
     x.cs.itk[i] = d.cs.itk[i]; x.cs.frz[i] = d.cs.frz[i];
+    x.red[3 * K + i] = 0.0;                  // the S.S sums: not formed in the iterations
   }
   if (q.tid == 0) {
     *x.st = *d.st_;
@@ -817,11 +818,10 @@ __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K
         reinterpret_cast<unsigned long long*>(d.partials + diag_offset(K, nblk))[it * nblk + blockIdx.x] = globaltimer();
       warps_in_order<3>(v, x.wpart, nw);
       for (int c = 0; c < 3; ++c) part[(size_t)(c * K + q.k) * ncta + cta] = v[c];
-      part[(size_t)(3 * K + q.k) * ncta + cta] = 0.0;
-      __threadfence();
+      // the release add publishes the partials and (cumulatively, after the CTA barrier) the
+      // CTA's field stores; the acquire spin orders every later read -- no separate fences
       red_release_add(gbar, 1u);
       if (!grid_wait(gbar, target)) x.ready[1] = 1;
-      __threadfence();
     }
     compute_bar(NCT);
     if (x.ready[1]) break;
@@ -829,14 +829,14 @@ __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K
     if (timed) tim[2] = tim[2] + (t_bar - tim[3]);
     // per-condition sums over the CTAs in CTA order (identical in every CTA): every partial is
     // loaded at once (one L2 round trip), then each (q, k) row is summed in CTA order
-    {
-      const int np = 4 * K * ncta;
+    {   // (the S.S column is not summed in the iterations: red[3K, 4K) stays zero)
+      const int np = 3 * K * ncta;
 #pragma unroll 4
       for (int i = q.tid; i < np; i += NCT) x.pbuf[i] = __ldcg(part + i);
     }
     compute_bar(NCT);
     double* red = x.red;
-    for (int i = q.tid; i < 4 * K; i += NCT) {
+    for (int i = q.tid; i < 3 * K; i += NCT) {
       const double* src = x.pbuf + (size_t)i * ncta;
       double a = 0.0;
       for (int b = 0; b < ncta; ++b) a += src[b];

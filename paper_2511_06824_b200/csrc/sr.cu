@@ -830,16 +830,19 @@ __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K
     // per-condition sums over the CTAs in CTA order (identical in every CTA): every partial is
     // loaded at once (one L2 round trip), then each (q, k) row is summed in CTA order
     {   // (the S.S column is not summed in the iterations: red[3K, 4K) stays zero)
-      const int np = 3 * K * ncta;
+      // stored CTA-major ([cta][row]) so that the per-row sums below read consecutive banks
+      const int np = 3 * K * ncta, nrow = 3 * K;
 #pragma unroll 4
-      for (int i = q.tid; i < np; i += NCT) x.pbuf[i] = __ldcg(part + i);
+      for (int i = q.tid; i < np; i += NCT) {
+        const int row = i / ncta, b = i - row * ncta;
+        x.pbuf[b * nrow + row] = __ldcg(part + i);
+      }
     }
     compute_bar(NCT);
     double* red = x.red;
     for (int i = q.tid; i < 3 * K; i += NCT) {
-      const double* src = x.pbuf + (size_t)i * ncta;
       double a = 0.0;
-      for (int b = 0; b < ncta; ++b) a += src[b];
+      for (int b = 0; b < ncta; ++b) a += x.pbuf[b * (3 * K) + i];   // CTA order
       red[i] = a;
     }
     compute_bar(NCT);

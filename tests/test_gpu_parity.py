@@ -110,6 +110,17 @@ def test_other_preconditioners(P, orc, gi, precond, schedule):
     full_parity(P, orc, g, gi.random_conditions(3, 3), 1.8, precond=precond, schedule=schedule)
 
 
+@pytest.mark.parametrize("precond", ["jacobi", "assor1", "none"])
+def test_preconditioners_on_compile_time_width_kernels(P, orc, gi, precond):
+    """Jacobi, ASSOR-I and no preconditioner on a mesh wide enough for the compile-time 256-column
+    persistent kernel (sr.cu k_srp<PC, 0, 0, 256>), against the oracle."""
+    g = gi.grid(256, 40, "short", tex_n_theta=8, tex_n_y=2, tex_band_rows=8)
+    S = P.JointSolver(g, 1)
+    assert S.tile_config()["tw"] == 256 and S.tile_config()["persistent"]
+    S.close()
+    full_parity(P, orc, g, gi.random_conditions(17, 3), 1.5, precond=precond, schedule="single")
+
+
 @pytest.mark.parametrize("texture", ["smooth", "short"])
 def test_assor1_parity(P, orc, gi, texture):
     """ASSOR-I (Eq. 3.2) on the single-pass schedule vs the oracle's assor1 apply; the seam pair

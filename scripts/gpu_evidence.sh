@@ -13,3 +13,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 1 --warmup 0 --no-cpu-baseline --picard-steps 0 > gpurun_out/launches.log 2>&1; echo launches=$?
 unset GMAF_LAUNCH_MODE
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_reference.log 2>&1; echo ref=$?
+timeout 600 python scripts/probe_rows1.py > gpurun_out/rows1.log 2>&1; cat gpurun_out/rows1.log
+timeout 600 python scripts/probe_slab_sizes.py > gpurun_out/slab_sizes.log 2>&1; cat gpurun_out/slab_sizes.log

@@ -772,9 +772,6 @@ __global__ void __maxnreg__(168) k_srp(GridParams g, DevPtrs d, TileCfg t, int K
     // the CTA barrier below, which is cumulative over the writes the barrier ordered before it (the
     // scheme of cooperative groups' grid sync: only the arriving thread fences)
     fence_proxy_async_global();
-#ifdef GMAF_PER_THREAD_FENCE
-    __threadfence();
-#endif
     if (rows) {
       // row slabs: this CTA's output columns of the rows it owns among the 4 boundary rows of each
       // slab edge (r_{i+1} and pd_i) go straight into the neighbour's inbox (the next gather's
